@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the MHFD hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mhfd|reference]
+
+One *step* = one pass of the whole hot path over one
+batch of synthetic EM tiles resident in HBM: percentiles -> fused stretch/blur/DoG/
+argmax -> NMS + threshold + compaction -> overlap pruning -> focus scores, plus (N>1)
+the NCCL all-gather of every rank's (count, score).  Workload (config C4 of
+SURVEY.md §8(d)): per GPU a batch of 64 tiles of 4096x4096 u8 (image g: seed 1000+g,
+defocus 0.5*(g mod 9) px, dose 300), sigma 1-10, 10 scales, tau = 0.1*dt = 0.09,
+overlap 0.5.  Images are independent, so per-GPU work is fixed as N grows ("weak").
+The 1.07 GB batch per GPU is larger than L2 (126 MB), so no L2 flush is needed.
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
+cudaDeviceSynchronize and CUDA events on the launching stream; max over ranks.
+Per-stage device times come from events the library records on the same stream
+(mhfd_timing_*), which gives the dominant kernel's (k_scale_space) duration for
+the roofline.  `e2e` repeats the measurement through mhfd_focus_score_host with the
+batch in pinned host memory (H2D copies and the D2H of scores inside the timed
+region).  `cpu_baseline` times the oracle (oracle/, f64, plain C) on rank 0 on a
+bounded sample (a band of rows of one tile).
+
+`--impl reference`: the oracle IS the reference arm for this tier (there is no
+reference implementation to install): rank 0 times it on the host
+cores, each step a band of the same workload; other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPix/s and ms/image (4096² tile, 10 scales) at 1/2/4/8 B200 vs HBM roofline"
+SIZE = 4096
+SIGMA = (1.0, 10.0)
+NSCALES = 10
+TAU = 0.1 * (SIGMA[1] - SIGMA[0]) / NSCALES
+OVERLAP = 0.5
+# Derived ALU peak (B200_PROFILING.md unit counts): 148 SMs x 128 FP32 FMA/clk x 2 FLOP
+# x 1.965 GHz (clocks.max.sm).  The FFMA microbenchmark measured 36.1 TFMA/s = 72.2
+# TFLOP/s sustained (profiles/r01_ubench_ffma.json).
+ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def radii():
+    dt = (SIGMA[1] - SIGMA[0]) / NSCALES
+    return [math.ceil(5.0 * (SIGMA[0] + i * dt)) for i in range(NSCALES + 1)]
+
+
+def alg_flops_per_px():
+    """Algorithmic FLOPs of the fused kernel per pixel: the direct
+    separable blur at the parity radius R_i = ceil(5 t_i) — 2 passes x (2R_i+1) FMA
+    x 2 FLOP per level — plus DoG (2 FLOP) and the running max (1) per plane."""
+    return sum(2 * (2 * R + 1) * 2 for R in radii()) + 3 * NSCALES
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock and throttle reasons."""
+
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            log("clock sampling unavailable:", e)
+            self.max = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def make_batch(rank: int, B: int, device) -> torch.Tensor:
+    import synth
+    imgs = torch.empty((B, SIZE, SIZE), dtype=torch.uint8, device=device)
+    for b in range(B):
+        g = rank * B + b
+        imgs[b] = synth.em_tile(SIZE, SIZE, 1000 + g, defocus=0.5 * (g % 9), dose=300.0, device=device)
+    return imgs
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_band(img: np.ndarray, rows: int) -> tuple[float, dict]:
+    """The oracle as it stands on a band of `rows` rows of one tile: percentiles and
+    stretch of the tile, Eq. 2 DoG of the band, Eq. 3 NMS, pruning.  Returns seconds."""
+    import oracle
+    t0 = time.perf_counter()
+    lo, hi = oracle.percentiles(img)
+    f = oracle.stretch(img, lo, hi)
+    y0 = (SIZE - rows) // 2
+    D = oracle.dog_stack(f, SIGMA[0], SIGMA[1], NSCALES, rows=(y0, y0 + rows))
+    cand = oracle.nms_paper(D, TAU)
+    keep = oracle.prune(cand, SIGMA[0], SIGMA[1], NSCALES, OVERLAP)
+    dt = time.perf_counter() - t0
+    return dt, {"candidates": int(len(cand)), "kept": int(keep.sum())}
+
+
+def cpu_baseline(img: np.ndarray, rows: int = 256) -> dict:
+    import oracle
+    oracle.set_threads(os.cpu_count() or 1)
+    dt, info = oracle_band(img, rows)
+    px = rows * SIZE
+    return {"value": px / dt / 1e6, "unit": "MPix/s", "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"{rows} rows x {SIZE} cols (= {px / 1e6:.2f} MPix) of tile 0 (4096^2 u8): percentiles+stretch "
+                      f"of the tile, DoG/NMS/pruning of the band, f64, {dt:.1f} s",
+            "seconds": dt, **info}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    oracle.set_threads(os.cpu_count() or 1)
+    img = synth.em_tile_np(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, bits=8)
+    # size the per-step band so the whole run stays within ~150 s of CPU time
+    probe, _ = oracle_band(img, 16)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    rows = int(max(16, min(SIZE, 16 * budget / max(probe, 1e-3))))
+    rows = max(16, rows // 16 * 16)
+    times = []
+    for k in range(args.warmup + args.steps):
+        dt, info = oracle_band(img, rows)
+        if k >= args.warmup:
+            times.append(dt)
+    ms = statistics.median(times) * 1e3
+    px = rows * SIZE
+    value = px / (ms * 1e-3) / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4 tile (4096x4096 u8 synthetic EM, sigma 1-10, 10 scales, tau 0.09, "
+                                   "overlap 0.5); each step a band of rows of tile 0", "rows_per_step": rows,
+                       "parallelism": "host cores (OpenMP)"},
+            "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": oracle.get_threads(), "kind": "oracle",
+                             "sample": f"{rows} rows x {SIZE} cols per step"},
+            "e2e": {"value": value, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mhfd", choices=["mhfd", "reference"])
+    ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.warmup < 3:
+        log("warning: the contract asks for >= 3 warm-up steps")
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2108_12050_b200 as mhfd
+
+    B = args.batch
+    t0 = time.time()
+    imgs = make_batch(rank, B, dev)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated {B} tiles in {time.time() - t0:.1f} s")
+    det = mhfd.Detector(SIZE, SIZE, min_sigma=SIGMA[0], max_sigma=SIGMA[1], num_scales=NSCALES, threshold=TAU,
+                        overlap=OVERLAP, device=local)
+    gathered = torch.empty((world, B, 2), dtype=torch.float64, device=dev)
+
+    def step():
+        scores, counts = det.focus_score(imgs, counts=True)
+        if dist is not None:
+            local_res = torch.stack([counts.to(torch.float64), scores], 1)
+            dist.all_gather_into_tensor(gathered, local_res.contiguous())
+        return scores
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_call = mhfd.Detector.last_launch_count()
+
+    det.timing_enable(args.steps)
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            scores = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stages = det.timing_read()
+    det.timing_enable(0)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    px_step = world * B * SIZE * SIZE
+    value = px_step / (ms_max * 1e-3) / 1e6
+
+    # dominant kernel: k_scale_space (stage 1), averaged over the timed steps
+    ss_ms = statistics.mean(s[1] for s in stages)
+    stage_ms = {k: statistics.mean(s[i] for s in stages) for i, k in
+                enumerate(["percentiles_a1", "scale_space_a2_a6", "nms_compact_a7_a8", "prune_score_a9_a10"])}
+    flops = alg_flops_per_px() * B * SIZE * SIZE
+    achieved = flops / (ss_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_scale_space_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            t = json.load(f)
+        traffic = t["dram_bytes_per_image"] * B
+    roofline = {"bound": "alu", "kernel": "k_scale_space", "achieved": achieved, "peak": ALU_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / ALU_PEAK_TFLOPS, "traffic": traffic,
+                "alg_flops_per_px": alg_flops_per_px(), "kernel_ms_per_launch": ss_ms,
+                "share_of_step": ss_ms / ms,
+                "peak_note": "derived: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (B200_PROFILING.md); "
+                             "measured FFMA microbenchmark 72.2 TFLOP/s",
+                "hbm_gbs": (B * SIZE * SIZE * (1 + 5)) / (ss_ms * 1e-3) / 1e9,
+                "hbm_note": "k_scale_space HBM bytes: 1 B/px read + 5 B/px (v f32 + argmax u8) written"}
+
+    # e2e through the host-buffer C-ABI entry point
+    e2e = None
+    if not args.no_e2e:
+        host = imgs.cpu().pin_memory()
+        for _ in range(2):
+            det.focus_score_host(host, chunk=8)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            hs = det.focus_score_host(host, chunk=8)
+            if dist is not None:
+                res = torch.stack([hs, hs], 1).to(dev)
+                dist.all_gather_into_tensor(gathered, res)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - e0) * 1e3 / args.steps
+        ems = torch.tensor([ev0.elapsed_time(ev1) / args.steps], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e_ms = float(ems.item())
+        assert torch.equal(hs, scores.cpu()), "host-path scores differ from the device path"
+        e2e = {"value": px_step / (e_ms * 1e-3) / 1e6, "unit": "MPix/s", "ms_per_step": e_ms,
+               "wall_ms_per_step": wall, "h2d_bytes_per_step": B * SIZE * SIZE, "d2h_bytes_per_step": B * 12,
+               "api": "mhfd_focus_score_host (pinned host batch, chunks of 8, copy/compute overlap)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(imgs[0].cpu().numpy())
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_image": ms_max / B,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": "C4: per GPU a batch of 64 synthetic EM tiles 4096x4096 u8 (seed 1000+g, "
+                                       "defocus 0.5*(g mod 9) px, dose 300); sigma 1-10, 10 scales, tau 0.09, "
+                                       "overlap 0.5, Eq. 3 NMS",
+                           "batch_per_gpu": B, "global_batch": world * B, "width": SIZE, "height": SIZE,
+                           "parallelism": f"dp{world} (image sharding, NCCL all-gather of (count, score))",
+                           "l2": "inputs larger than L2 (1.07 GB per GPU per step)"},
+                "roofline": roofline, "stage_ms": stage_ms, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_call * args.steps, "clocks": clk.summary(),
+                "mean_score": float(scores.mean())}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

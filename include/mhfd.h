@@ -1,0 +1,209 @@
+/*
+ * mhfd.h — C ABI of the B200-native MHFD hot path.
+ *
+ * Multi-scale Histologic Feature Detection (Levental et al., arXiv 2108.12050,
+ * "Ultrafast Focus Detection for Automated Microscopy").  Per image the library
+ * computes Algorithm 1 with a separable spatial blur in place
+ * of the FFT, plus the threshold and blob-overlap pruning that the north star adds:
+ *
+ *   u8/u16 image I
+ *   -> histogram stretch I' (saturate sat_low / sat_high of the darkest /
+ *      lightest pixels, map to [0,1])
+ *   -> L(x,y,t_i) = G(.,.,t_i) * I', t_i = min_t + (i-1) dt,
+ *      dt = (max_t - min_t)/n, i = 1..n+1 (periodic)
+ *   -> DoG(x,y,i) = t_i (L(x,y,t_{i+1}) - L(x,y,t_i))       Eq. 2
+ *   -> C = argmaxlocal_{x,y} argmax_i DoG  (Eq. 3) or the
+ *      conventional 3x3x3 scale-space maxima; response > threshold
+ *   -> blob-overlap pruning (north star) -> DOF = |C|
+ *
+ * Every reading the paper leaves open (sigma = t, n+1 levels, periodic blur,
+ * -inf NMS padding, first argmax on ties, nearest-rank percentiles, the pruning
+ * rule ...) is listed in DESIGN.md §3 ("reading Rk").
+ *
+ * Conventions (apply to every entry point):
+ *  - Pure C99; no torch or CUDA types.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = the legacy default stream).
+ *  - Device pointers ("d_") must be device-accessible CUDA allocations on the
+ *    context's device; the CALLER owns every buffer (images, workspace and
+ *    outputs).  The library never allocates device memory inside
+ *    mhfd_detect_batch / mhfd_focus_score; the context owns only its immutable
+ *    parameters and tap tables (host memory).
+ *  - Asynchrony: argument validation happens synchronously and, on failure,
+ *    enqueues nothing and returns an error.  On MHFD_OK all work has been
+ *    enqueued on `stream`; outputs are valid once the caller synchronises it.
+ *    Launch failures return MHFD_ERR_CUDA; asynchronous faults surface at the
+ *    caller's synchronisation.
+ *  - Thread safety: a context is immutable after mhfd_create; concurrent calls
+ *    with distinct workspaces (and outputs) on distinct streams are safe.
+ *  - Determinism: results are bitwise reproducible run to run and independent
+ *    of the batch composition and of how a batch is split across GPUs.
+ *  - Image layout: batch images back to back, image b at
+ *    d_images + b * height * pitch_bytes; row-major, rows pitch_bytes apart;
+ *    pixel (x = column, y = row).  pitch_bytes % 16 == 0 and
+ *    pitch_bytes >= width * bytes_per_pixel; d_images 16-byte aligned.
+ *  - Coordinates in outputs are 0-based; `scale` is the 0-based DoG plane
+ *    index s = i^ - 1, i.e. sigma = min_sigma + s * dt.
+ */
+#ifndef MHFD_H
+#define MHFD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MHFD_ABI_VERSION 1
+
+typedef struct mhfd_ctx mhfd_ctx; /* opaque, immutable after mhfd_create */
+
+typedef enum {
+  MHFD_OK = 0,
+  MHFD_ERR_INVALID_ARGUMENT = 1, /* bad parameter value, NULL pointer, bad enum */
+  MHFD_ERR_SHAPE = 2,            /* width/height/pitch/batch not supported */
+  MHFD_ERR_CAPACITY = 3,         /* blob_capacity < 0 or too large */
+  MHFD_ERR_WORKSPACE = 4,        /* workspace NULL or smaller than mhfd_workspace_bytes */
+  MHFD_ERR_CUDA = 5,             /* CUDA runtime / launch error (text: mhfd_last_error) */
+  MHFD_ERR_DEVICE = 6            /* no CUDA device, or device is not sm_100 (B200) */
+} mhfd_status;
+
+typedef enum { MHFD_U8 = 1, MHFD_U16 = 2 } mhfd_dtype;
+
+typedef enum {
+  MHFD_NMS_PAPER = 0, /* Eq. 3: global argmax over scale, 3x3 local max in space (default) */
+  MHFD_NMS_26 = 1     /* conventional 3x3x3 scale-space maxima, 26 neighbours */
+} mhfd_nms;
+
+/* Parameters of Algorithm 1's "Require I, n, min_t, max_t" plus
+ * the north star's threshold and overlap.  Fill with mhfd_params_default()
+ * and override. */
+typedef struct {
+  uint32_t struct_size;   /* = sizeof(mhfd_params) (forward-compatible ABI) */
+  int32_t width, height;  /* image shape, fixed per context; 2*R_max+1 <= W,H <= 65535,
+                             R_max = ceil(5*max_sigma) (GPU truncation radius) */
+  float min_sigma;        /* min_t = t_1 > 0 (sigma = t)           */
+  float max_sigma;        /* max_t = t_{n+1} > min_t, ceil(5*max_sigma) <= 160       */
+  int32_t num_scales;     /* n >= 1: n+1 Gaussian levels, n DoG planes; n <= 62      */
+  float threshold;        /* keep response > threshold; finite, >= 0                 */
+  float overlap;          /* in [0,1]: drop a blob whose disk overlaps a kept,
+                             higher-priority blob by a fraction > overlap; 1 = off  */
+  float sat_low;          /* fraction of darkest pixels saturated (paper: 0.00175)   */
+  float sat_high;         /* fraction of lightest pixels saturated (paper: 0.00175)  */
+  int32_t nms;            /* mhfd_nms                                                */
+  int32_t strict;         /* 0: v == maxpool(v) (paper); 1: strictly
+                             greater than every neighbour                            */
+  int32_t device;         /* CUDA device ordinal the context is bound to             */
+  int32_t max_candidates; /* per-image candidate capacity before pruning;
+                             0 = default ceil(W/2)*ceil(H/2) (PAPER mode) or
+                             n*ceil(W/2)*ceil(H/2) (26 mode)                         */
+} mhfd_params;
+
+/* One detected feature (x^_j, y^_j, i^_j) of Eq. 3 and its DoG
+ * response. 16 bytes. */
+typedef struct {
+  int32_t x, y, scale;
+  float response;
+} mhfd_blob;
+
+/* Paper defaults: sigma 1..10, n = 10, threshold 0.1*dt, overlap 0.5, 0.175% per
+ * tail, Eq. 3 NMS, non-strict.  width/height are set to 0 (caller must set). */
+void mhfd_params_default(mhfd_params* p);
+
+/* Validate parameters and build the context (scale grid, f32 tap tables).
+ * Errors: INVALID_ARGUMENT (p/out NULL, struct_size too small, sigma <= 0,
+ * max <= min, n < 1 or n > 62, threshold < 0 or not finite, overlap not in
+ * [0,1], sat fractions not in [0,0.5), nms/strict out of range,
+ * ceil(5*max_sigma) > 160), SHAPE (width/height out of range),
+ * DEVICE (device ordinal invalid or not compute capability 10.0). */
+mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out);
+
+/* Bytes of device workspace one call with `batch` images needs (batch >= 1).
+ * Linear in batch; for 4096^2 PAPER mode about 5.5 B/px + 3*max_candidates*16 B
+ * per image. */
+mhfd_status mhfd_workspace_bytes(const mhfd_ctx* c, int32_t batch, size_t* bytes);
+
+/* Detect blobs in `batch` images.
+ *  d_images     : batch x height rows of pitch_bytes (u8 or u16 per `dtype`)
+ *  d_workspace  : >= mhfd_workspace_bytes(c, batch) bytes, 256-byte aligned
+ *  d_blobs      : batch x blob_capacity records; image b's kept blobs are at
+ *                 d_blobs + b*blob_capacity, sorted by (y, x, scale); only the
+ *                 first min(count, blob_capacity) are written
+ *  d_counts     : batch int32, the exact number of kept blobs per image (the
+ *                 focus score |C|), also when it exceeds blob_capacity
+ *  d_flags      : nullable; batch int32, bit0 = candidate capacity exceeded
+ *                 (pruning saw only the first max_candidates candidates in
+ *                 raster order), bit1 = list truncated to blob_capacity
+ * Errors: INVALID_ARGUMENT, SHAPE, CAPACITY (blob_capacity < 0), WORKSPACE, CUDA. */
+mhfd_status mhfd_detect_batch(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch,
+                              int64_t pitch_bytes, void* d_workspace, size_t workspace_bytes,
+                              mhfd_blob* d_blobs, int32_t blob_capacity, int32_t* d_counts,
+                              int32_t* d_flags, void* stream);
+
+/* Focus score only: d_scores[b] = (double)|C_b|; d_counts
+ * (nullable) receives the int32 counts.  Same work as mhfd_detect_batch minus
+ * writing the blob list. */
+mhfd_status mhfd_focus_score(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch,
+                             int64_t pitch_bytes, void* d_workspace, size_t workspace_bytes,
+                             double* d_scores, int32_t* d_counts, void* stream);
+
+/* End-to-end call with HOST buffers (the e2e path): h_images is batch x height
+ * rows of pitch_bytes in host memory (pinned for overlap; pageable works but
+ * serialises).  The batch is processed in chunks of
+ *   chunk = staging_bytes / (2 * height * pitch_bytes)   images (>= 1 required):
+ * chunk k+1 is copied host->device into one half of d_staging on a context-owned
+ * copy stream while chunk k is processed on `stream`; each chunk's scores are
+ * copied device->host into h_scores (batch doubles) and, if non-NULL, h_counts.
+ * d_workspace must hold mhfd_workspace_bytes(c, chunk).  Outputs are valid after
+ * the caller synchronises `stream`.  Uses context-owned streams/events: do not call
+ * concurrently on the same context.
+ * Errors: as mhfd_focus_score; WORKSPACE if the staging holds < 1 image per half. */
+mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dtype, int32_t batch,
+                                  int64_t pitch_bytes, void* d_staging, size_t staging_bytes,
+                                  void* d_workspace, size_t workspace_bytes, double* h_scores,
+                                  int32_t* h_counts, void* stream);
+
+/* Per-stage device timing (bench instrumentation; not thread-safe).
+ * mhfd_timing_enable(c, k) arms k records (k = 0 disables); each subsequent
+ * mhfd_detect_batch / mhfd_focus_score call records CUDA events on its stream
+ * around its 4 stages: [0] percentiles (a1), [1] k_scale_space (a2-a6),
+ * [2] NMS + compaction (a7-a8), [3] pruning + score (a9-a10).
+ * mhfd_timing_read waits for the recorded events and writes ms[call*4 + stage]
+ * for *ncalls (<= k) calls. */
+mhfd_status mhfd_timing_enable(mhfd_ctx* c, int32_t max_calls);
+mhfd_status mhfd_timing_read(mhfd_ctx* c, float* ms, int32_t* ncalls);
+
+/* Introspection for parity tests (same kernels as the two calls above):
+ *  d_lohi  : nullable, batch x 2 int32 (percentile values lo, hi)
+ *  d_dog   : nullable, batch x n x height x width f32 DoG planes (Eq. 2)
+ *  d_v     : nullable, batch x height x width f32 max_i DoG (Eq. 3 inner argmax)
+ *  d_idx   : nullable, batch x height x width u8 first argmax (0-based)
+ *  d_cands : nullable, batch x max_candidates blobs before pruning (raster order)
+ *  d_ncand : nullable, batch int32 exact candidate counts before pruning */
+mhfd_status mhfd_debug_dump(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch,
+                            int64_t pitch_bytes, void* d_workspace, size_t workspace_bytes,
+                            int32_t* d_lohi, float* d_dog, float* d_v, uint8_t* d_idx,
+                            mhfd_blob* d_cands, int32_t* d_ncand, void* stream);
+
+/* Read back the parameters a context was built with (derived fields filled). */
+mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int32_t mhfd_last_launch_count(void);
+
+/* NULL-safe. */
+void mhfd_destroy(mhfd_ctx* c);
+
+/* Static string for a status code. */
+const char* mhfd_status_string(mhfd_status s);
+
+/* Thread-local detail of the last failing call on this thread ("" if none). */
+const char* mhfd_last_error(void);
+
+/* MHFD_ABI_VERSION of the built library. */
+int32_t mhfd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHFD_H */

@@ -1,0 +1,200 @@
+"""B200-native MHFD hot path (arXiv 2108.12050): Python binding of ``libmhfd.so``.
+
+The binding only marshals arguments: every step of the path (percentiles,
+stretch, blur, DoG, NMS, compaction, pruning, score) runs in the CUDA kernels
+behind the C ABI of ``include/mhfd.h``.  PyTorch provides device memory,
+streams and (in ``dist``) the NCCL process group.  There is no CPU fallback:
+without a CUDA device the context cannot be created and the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _abi
+from ._abi import MHFDError, mhfd_blob, mhfd_params  # noqa: F401
+
+__all__ = ["Detector", "MHFDError", "BLOB_FIELDS"]
+
+BLOB_FIELDS = ("x", "y", "scale", "response")
+
+
+def _params(**kw) -> mhfd_params:
+    p = mhfd_params()
+    _abi.load().mhfd_params_default(ctypes.byref(p))
+    for k, v in kw.items():
+        if v is not None:
+            setattr(p, k, v)
+    return p
+
+
+class Detector:
+    """One MHFD context (fixed image shape and parameters) on one CUDA device.
+
+    Parameters follow Algorithm 1's ``Require I, n, min_t, max_t``
+    plus the north star's threshold and overlap.  ``threshold=None`` means
+    0.1 * dt (reading R11).
+    """
+
+    def __init__(self, width: int, height: int, min_sigma: float = 1.0, max_sigma: float = 10.0,
+                 num_scales: int = 10, threshold: float | None = None, overlap: float = 0.5,
+                 sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
+                 strict: bool = False, device: int | None = None, max_candidates: int = 0):
+        lib = _abi.load()
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        if threshold is None:
+            threshold = 0.1 * (max_sigma - min_sigma) / num_scales
+        self.params = _params(width=int(width), height=int(height), min_sigma=float(min_sigma),
+                              max_sigma=float(max_sigma), num_scales=int(num_scales), threshold=float(threshold),
+                              overlap=float(overlap), sat_low=float(sat_low), sat_high=float(sat_high),
+                              nms={"paper": _abi.MHFD_NMS_PAPER, "26": _abi.MHFD_NMS_26}[str(nms)],
+                              strict=int(bool(strict)), device=int(device), max_candidates=int(max_candidates))
+        h = ctypes.c_void_p()
+        _abi.check(lib.mhfd_create(ctypes.byref(self.params), ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        got = mhfd_params()
+        _abi.check(lib.mhfd_get_params(self._h, ctypes.byref(got)))
+        self.max_candidates = int(got.max_candidates)
+        self.width, self.height, self.n = int(width), int(height), int(num_scales)
+        self.device = torch.device("cuda", int(device))
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.mhfd_destroy(h)
+            self._h = None
+
+    # -------------------------------------------------------------- helpers
+    def workspace_bytes(self, batch: int) -> int:
+        n = ctypes.c_size_t()
+        _abi.check(self._lib.mhfd_workspace_bytes(self._h, int(batch), ctypes.byref(n)))
+        return int(n.value)
+
+    def _workspace(self, batch: int) -> torch.Tensor:
+        need = self.workspace_bytes(batch)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need + 256, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    @staticmethod
+    def _ws_ptr(ws: torch.Tensor) -> int:
+        p = ws.data_ptr()
+        return (p + 255) & ~255
+
+    def prepare(self, images: torch.Tensor) -> tuple[torch.Tensor, int, int, int]:
+        """(B,H,W) or (H,W) uint8/uint16 tensor -> device tensor with a 16-byte-multiple pitch."""
+        if images.dim() == 2:
+            images = images.unsqueeze(0)
+        if images.dim() != 3 or images.shape[1] != self.height or images.shape[2] != self.width:
+            raise ValueError(f"images must be (B, {self.height}, {self.width}); got {tuple(images.shape)}")
+        if images.dtype == torch.uint8:
+            dt, bpp = _abi.MHFD_U8, 1
+        elif images.dtype == torch.uint16:
+            dt, bpp = _abi.MHFD_U16, 2
+        else:
+            raise TypeError("images must be torch.uint8 or torch.uint16")
+        images = images.to(self.device, non_blocking=True)
+        B = images.shape[0]
+        wp = (self.width * bpp + 15) // 16 * 16 // bpp
+        if wp != self.width or not images.is_contiguous() or images.data_ptr() % 16:
+            padded = torch.zeros((B, self.height, wp), dtype=images.dtype, device=self.device)
+            padded[:, :, :self.width] = images
+            images = padded
+        return images, dt, B, wp * bpp
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # -------------------------------------------------------------- entry points
+    def focus_score(self, images: torch.Tensor, counts: bool = False):
+        """DOF = |C| per image as a float64 device tensor."""
+        imgs, dt, B, pitch = self.prepare(images)
+        ws = self._workspace(B)
+        scores = torch.empty(B, dtype=torch.float64, device=self.device)
+        cnt = torch.empty(B, dtype=torch.int32, device=self.device)
+        _abi.check(self._lib.mhfd_focus_score(self._h, imgs.data_ptr(), dt, B, pitch, self._ws_ptr(ws),
+                                              ws.numel() - 256, scores.data_ptr(), cnt.data_ptr(), self._stream()))
+        return (scores, cnt) if counts else scores
+
+    def detect(self, images: torch.Tensor, blob_capacity: int | None = None):
+        """Kept blobs per image: (blobs int32/float view (B, cap, 4), counts (B,), flags (B,))."""
+        imgs, dt, B, pitch = self.prepare(images)
+        ws = self._workspace(B)
+        cap = self.max_candidates if blob_capacity is None else int(blob_capacity)
+        blobs = torch.empty((B, max(cap, 1), 4), dtype=torch.int32, device=self.device)
+        cnt = torch.empty(B, dtype=torch.int32, device=self.device)
+        flags = torch.empty(B, dtype=torch.int32, device=self.device)
+        _abi.check(self._lib.mhfd_detect_batch(self._h, imgs.data_ptr(), dt, B, pitch, self._ws_ptr(ws),
+                                               ws.numel() - 256, blobs.data_ptr(), cap, cnt.data_ptr(),
+                                               flags.data_ptr(), self._stream()))
+        return blobs, cnt, flags
+
+    def debug_dump(self, images: torch.Tensor, dog: bool = True, cands: bool = True) -> dict:
+        """Intermediates for parity tests: lo/hi, DoG planes, v, argmax, candidates."""
+        imgs, dt, B, pitch = self.prepare(images)
+        ws = self._workspace(B)
+        H, W, n = self.height, self.width, self.n
+        out = {"lohi": torch.empty((B, 2), dtype=torch.int32, device=self.device),
+               "ncand": torch.empty(B, dtype=torch.int32, device=self.device)}
+        out["dog"] = torch.empty((B, n, H, W), dtype=torch.float32, device=self.device) if dog else None
+        paper = self.params.nms == _abi.MHFD_NMS_PAPER
+        out["v"] = torch.empty((B, H, W), dtype=torch.float32, device=self.device) if paper else None
+        out["idx"] = torch.empty((B, H, W), dtype=torch.uint8, device=self.device) if paper else None
+        out["cands"] = torch.empty((B, self.max_candidates, 4), dtype=torch.int32, device=self.device) if cands else None
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _abi.check(self._lib.mhfd_debug_dump(self._h, imgs.data_ptr(), dt, B, pitch, self._ws_ptr(ws),
+                                             ws.numel() - 256, ptr(out["lohi"]), ptr(out["dog"]), ptr(out["v"]),
+                                             ptr(out["idx"]), ptr(out["cands"]), ptr(out["ncand"]), self._stream()))
+        return out
+
+    def focus_score_host(self, host_images: torch.Tensor, chunk: int = 8, counts: bool = False):
+        """End-to-end call with HOST buffers (mhfd_focus_score_host): chunked H2D copies
+        from (pinned) host memory overlapped with compute; returns host float64 scores."""
+        if host_images.dim() == 2:
+            host_images = host_images.unsqueeze(0)
+        if host_images.device.type != "cpu":
+            raise ValueError("focus_score_host takes host tensors")
+        dt, bpp = ((_abi.MHFD_U8, 1) if host_images.dtype == torch.uint8 else (_abi.MHFD_U16, 2))
+        B, H, W = host_images.shape
+        if (H, W) != (self.height, self.width) or (W * bpp) % 16 or not host_images.is_contiguous():
+            raise ValueError("host images must be contiguous (B, H, W) with W*bytes % 16 == 0")
+        pitch = W * bpp
+        chunk = max(1, min(int(chunk), B))
+        need_stage = 2 * chunk * H * pitch
+        if getattr(self, "_stage", None) is None or self._stage.numel() < need_stage + 256:
+            self._stage = torch.empty(need_stage + 256, dtype=torch.uint8, device=self.device)
+        ws = self._workspace(chunk)
+        if getattr(self, "_hs", None) is None or self._hs.numel() < B:
+            self._hs = torch.empty(B, dtype=torch.float64).pin_memory()
+            self._hc = torch.empty(B, dtype=torch.int32).pin_memory()
+        _abi.check(self._lib.mhfd_focus_score_host(self._h, host_images.data_ptr(), dt, B, pitch,
+                                                   self._ws_ptr(self._stage), need_stage, self._ws_ptr(ws),
+                                                   ws.numel() - 256, self._hs.data_ptr(), self._hc.data_ptr(),
+                                                   self._stream()))
+        return (self._hs[:B], self._hc[:B]) if counts else self._hs[:B]
+
+    def timing_enable(self, max_calls: int) -> None:
+        _abi.check(self._lib.mhfd_timing_enable(self._h, int(max_calls)))
+
+    def timing_read(self) -> list[list[float]]:
+        """Per recorded call: [percentiles, scale_space, nms, prune] device ms."""
+        cap = 4 * 100000
+        buf = (ctypes.c_float * cap)()
+        n = ctypes.c_int32()
+        _abi.check(self._lib.mhfd_timing_read(self._h, buf, ctypes.byref(n)))
+        return [[buf[4 * k + j] for j in range(4)] for k in range(n.value)]
+
+    @staticmethod
+    def last_launch_count() -> int:
+        return int(_abi.load().mhfd_last_launch_count())
+
+
+def blob_rows(blobs: torch.Tensor, count: int) -> list[tuple[int, int, int, float]]:
+    """(x, y, scale, response) tuples from one image's (cap, 4) int32 blob block."""
+    b = blobs[:count].cpu()
+    resp = b[:, 3].view(torch.float32) if b.numel() else torch.empty(0)
+    return [(int(x), int(y), int(s), float(r)) for (x, y, s), r in zip(b[:, :3].tolist(), resp.tolist())]

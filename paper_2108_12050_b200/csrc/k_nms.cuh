@@ -1,0 +1,217 @@
+// k_nms.cuh — scale-space NMS + threshold + ordered stream compaction (rows a7, a8).
+//
+// PAPER mode (Eq. 3): p is a candidate iff v(p) >= v(q) for every
+//   in-image q in its 3x3 neighbourhood (the "comparison against maxpool_2d(3,3)",
+//   -inf padding: reading R8; strict: v(p) > v(q), reading R9) and v(p) > tau (R11).
+// 26 mode: (p, i) is a candidate iff D_i(p) >= D_j(q) for every existing
+//   (q, j) of the 3x3x3 box other than itself (scale window truncated at the first and
+//   last plane: reading R16) and D_i(p) > tau.
+//
+// Compaction: a "segment" is 1024 consecutive pixels in raster order, one per warp.
+// k_nms_count writes per-segment candidate counts, k_seg_scan turns them into exclusive
+// offsets per image, k_nms_write re-evaluates the predicate and writes records at
+// segment offset + warp-ballot prefix.  The list is therefore in (y, x, scale) order
+// without a sort and is identical run to run (no atomics decide positions).
+#pragma once
+#include "common.cuh"
+
+namespace mhfd {
+
+constexpr int kSeg = 1024;
+
+struct NmsArgs {
+  int W, H, n;
+  float tau;
+  int strict;
+  const float* v;        // PAPER: B x H x W
+  const uint8_t* idx;    // PAPER: B x H x W
+  const float* dog;      // 26:    B x n x H x W
+};
+
+__device__ __forceinline__ bool dominates(float c, float q, int strict) { return strict ? (c > q) : (c >= q); }
+
+__device__ __forceinline__ bool paper_cand(const float* __restrict__ v, int W, int H, int y, int x, float tau,
+                                           int strict, float* val) {
+  const float c = __ldg(v + (int64_t)y * W + x);
+  *val = c;
+  if (!(c > tau)) return false;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int yy = y + dy;
+    if (yy < 0 || yy >= H) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dy == 0 && dx == 0) continue;
+      const int xx = x + dx;
+      if (xx < 0 || xx >= W) continue;
+      if (!dominates(c, __ldg(v + (int64_t)yy * W + xx), strict)) return false;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool cand26(const float* __restrict__ dog, int W, int H, int n, int64_t plane, int i,
+                                       int y, int x, float tau, int strict, float* val) {
+  const float c = __ldg(dog + (int64_t)i * plane + (int64_t)y * W + x);
+  *val = c;
+  if (!(c > tau)) return false;
+  for (int di = -1; di <= 1; ++di) {
+    const int j = i + di;
+    if (j < 0 || j >= n) continue;
+    const float* P = dog + (int64_t)j * plane;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int yy = y + dy;
+      if (yy < 0 || yy >= H) continue;
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (di == 0 && dy == 0 && dx == 0) continue;
+        const int xx = x + dx;
+        if (xx < 0 || xx >= W) continue;
+        if (!dominates(c, __ldg(P + (int64_t)yy * W + xx), strict)) return false;
+      }
+    }
+  }
+  return true;
+}
+
+// Number of candidates at pixel p (0/1 in PAPER mode, 0..n in 26 mode); optionally
+// writes them (in scale order) to out[].
+template <int MODE>
+__device__ __forceinline__ int pixel_cands(const NmsArgs& a, int b, int64_t p, mhfd_blob* out, int64_t base,
+                                           int64_t cap) {
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);
+  int c = 0;
+  if (MODE == MHFD_NMS_PAPER) {
+    float val;
+    if (paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val)) {
+      if (out && base < cap) {
+        mhfd_blob r;
+        r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
+        out[base] = r;
+      }
+      c = 1;
+    }
+  } else {
+    const float* dog = a.dog + (int64_t)b * a.n * plane;
+    for (int i = 0; i < a.n; ++i) {
+      float val;
+      if (cand26(dog, a.W, a.H, a.n, plane, i, y, x, a.tau, a.strict, &val)) {
+        if (out && base + c < cap) {
+          mhfd_blob r;
+          r.x = x; r.y = y; r.scale = i; r.response = val;
+          out[base + c] = r;
+        }
+        ++c;
+      }
+    }
+  }
+  return c;
+}
+
+// grid (ceil(nseg/8), B), 256 threads: warp w of CTA t owns segment 8t + w.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_nms_count(NmsArgs a, int nseg, int32_t* __restrict__ segcnt) {
+  const int b = blockIdx.y;
+  const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int64_t p0 = (int64_t)seg * kSeg;
+  int cnt = 0;
+  for (int k = 0; k < kSeg; k += 32) {
+    const int64_t p = p0 + k + lane;
+    int c = (p < plane) ? pixel_cands<MODE>(a, b, p, nullptr, 0, 0) : 0;
+    cnt += c;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  if (lane == 0) segcnt[(int64_t)b * nseg + seg] = cnt;
+}
+
+// One CTA (1024 threads) per image: exclusive scan of the segment counts.
+__global__ void __launch_bounds__(1024) k_seg_scan(const int32_t* __restrict__ segcnt, int nseg,
+                                                   int32_t* __restrict__ segoff, int32_t* __restrict__ ncand) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nseg; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = (i < nseg) ? segcnt[(int64_t)b * nseg + i] : 0;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int s = wsum[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, s, off);
+        if (lane >= off) s += y;
+      }
+      wsum[lane] = s;
+    }
+    __syncthreads();
+    const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+    if (i < nseg) segoff[(int64_t)b * nseg + i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ncand[b] = carry;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_nms_write(NmsArgs a, int nseg, const int32_t* __restrict__ segoff,
+                                                   mhfd_blob* __restrict__ cand, int64_t cap) {
+  const int b = blockIdx.y;
+  const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int64_t p0 = (int64_t)seg * kSeg;
+  int64_t off = segoff[(int64_t)b * nseg + seg];
+  mhfd_blob* out = cand + (int64_t)b * cap;
+  for (int k = 0; k < kSeg; k += 32) {
+    const int64_t p = p0 + k + lane;
+    if (MODE == MHFD_NMS_PAPER) {
+      float val = 0.f;
+      bool c = false;
+      int y = 0, x = 0;
+      if (p < plane) {
+        y = (int)(p / a.W); x = (int)(p - (int64_t)y * a.W);
+        c = paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val);
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, c);
+      if (c) {
+        const int64_t pos = off + __popc(m & ((1u << lane) - 1u));
+        if (pos < cap) {
+          mhfd_blob r;
+          r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
+          out[pos] = r;
+        }
+      }
+      off += __popc(m);
+    } else {
+      const int c = (p < plane) ? pixel_cands<MODE>(a, b, p, nullptr, 0, 0) : 0;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c) pixel_cands<MODE>(a, b, p, out, off + x - c, cap);
+      off += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+}
+
+}  // namespace mhfd

@@ -1,0 +1,126 @@
+// k_percentile.cuh — histogram + nearest-rank percentile selection (hot-path row a1).
+//
+// PAPER.md:255-259 (§3): "saturating .175% of the darkest pixels, saturating .175%
+// of the lightest pixels, and mapping the entire range to [0,1] ... parallelized
+// using GPU primitives".  Nearest rank (reading R13): lo is the pixel value of
+// rank floor(sat_low*N), hi the value of rank N-1-floor(sat_high*N) in the sorted
+// image.  Exact integer radix select: pass 1 histograms the top byte (the whole
+// value for u8); for u16 pass 2 histograms the low byte of the pixels in the two
+// selected top-byte bins.  HBM-bound: the image is read once per pass with
+// 128-bit loads; histograms are privatised per warp in shared memory.
+#pragma once
+#include "common.cuh"
+
+namespace mhfd {
+
+struct SelState {      // per image, between the two passes
+  int32_t bin_lo, bin_hi;   // selected top-byte bins
+  int64_t rem_lo, rem_hi;   // ranks inside those bins
+};
+
+// Pass 1: 256-bin histogram of (u8 value) or (u16 value >> 8).
+// Pass 2 (u16 only, second=true): low-byte histograms of the two selected bins.
+template <int BPP, bool SECOND>
+__global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images, Shape s, int rows_per_cta,
+                                              uint32_t* __restrict__ hist, const SelState* __restrict__ sel) {
+  constexpr int NH = SECOND ? 2 : 1;
+  __shared__ uint32_t sh[8][NH * 256];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 8 * NH * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  int sel_lo = -1, sel_hi = -1;
+  if (SECOND) { sel_lo = sel[b].bin_lo; sel_hi = sel[b].bin_hi; }
+  __syncthreads();
+  const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
+  const int y0 = blockIdx.x * rows_per_cta;
+  const int y1 = min(s.H, y0 + rows_per_cta);
+  const int row_bytes = s.W * BPP;
+  const int nvec = (row_bytes + 15) >> 4;
+  for (int y = y0; y < y1; ++y) {
+    const uint4* row = reinterpret_cast<const uint4*>(img + (int64_t)y * s.pitch);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      uint4 q = __ldg(row + v);
+      uint32_t wds[4] = {q.x, q.y, q.z, q.w};
+      const int base = v * 16;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (BPP == 1) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (base + 4 * k + j < row_bytes) atomicAdd(&sh[warp][(wds[k] >> (8 * j)) & 255u], 1u);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (base + 4 * k + 2 * j < row_bytes) {
+              uint32_t val = (wds[k] >> (16 * j)) & 0xffffu;
+              uint32_t top = val >> 8;
+              if (!SECOND) {
+                atomicAdd(&sh[warp][top], 1u);
+              } else {
+                if ((int)top == sel_lo) atomicAdd(&sh[warp][val & 255u], 1u);
+                if ((int)top == sel_hi) atomicAdd(&sh[warp][256 + (val & 255u)], 1u);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NH * 256; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += sh[w][i];
+    if (c) atomicAdd(&hist[(int64_t)b * (NH * 256) + i], c);
+  }
+}
+
+// Smallest bin whose cumulative count exceeds `rank`; returns the rank left inside it.
+__device__ __forceinline__ int select_bin(const uint32_t* h, int64_t rank, int64_t* rem) {
+  int64_t cum = 0;
+  for (int v = 0; v < 256; ++v) {
+    int64_t c = h[v];
+    if (cum + c > rank) { *rem = rank - cum; return v; }
+    cum += c;
+  }
+  *rem = 0;
+  return 255;
+}
+
+__device__ __forceinline__ void finish(ImgPar* p, int lo, int hi) {
+  p->lo = lo;
+  p->hi = hi;
+  p->degen = (hi == lo) ? 1 : 0;
+  p->inv = (hi == lo) ? 0.0f : 1.0f / (float)(hi - lo);
+}
+
+// One thread per image: scan the 256-bin histogram(s).
+template <int BPP>
+__global__ void k_select1(const uint32_t* __restrict__ hist1, RankPar r, SelState* __restrict__ sel,
+                          ImgPar* __restrict__ par, int batch) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const uint32_t* h = hist1 + (int64_t)b * 256;
+  int64_t rl, rh;
+  int bl = select_bin(h, r.rank_lo, &rl);
+  int bh = select_bin(h, r.rank_hi, &rh);
+  if (BPP == 1) {
+    finish(&par[b], bl, bh);
+  } else {
+    sel[b].bin_lo = bl; sel[b].bin_hi = bh; sel[b].rem_lo = rl; sel[b].rem_hi = rh;
+  }
+}
+
+__global__ void k_select2(const uint32_t* __restrict__ hist2, const SelState* __restrict__ sel,
+                          ImgPar* __restrict__ par, int batch) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const uint32_t* h = hist2 + (int64_t)b * 512;
+  int64_t dummy;
+  int lo = (sel[b].bin_lo << 8) | select_bin(h, sel[b].rem_lo, &dummy);
+  int hi = (sel[b].bin_hi << 8) | select_bin(h + 256, sel[b].rem_hi, &dummy);
+  finish(&par[b], lo, hi);
+}
+
+}  // namespace mhfd

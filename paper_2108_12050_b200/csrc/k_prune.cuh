@@ -1,0 +1,254 @@
+// k_prune.cuh — blob-overlap pruning, focus score and ordered output (rows a9, a10).
+//
+// Not in the paper: the north star's "blob-overlap pruning" (reading R12).  A blob of
+// DoG plane s has radius r_s = sqrt(2) t_s; the overlap fraction of two blobs is the
+// lens area of their disks over the area of the smaller disk.  Semantics = greedy in
+// priority order (scale descending, then raster ascending): a blob is kept iff no kept,
+// higher-priority blob overlaps it by more than `overlap`.
+//
+// Parallel equivalent (exact, not an approximation): every blob starts UNDECIDED; in a
+// round, an undecided blob becomes REMOVED if some higher-priority overlapping blob is
+// KEPT, KEPT if all of them are REMOVED, and stays UNDECIDED otherwise.  Each decision
+// is final and equals the sequential one (induction on priority), and the highest-
+// priority undecided blob always decides, so the rounds terminate (<= 10
+// rounds on EM tiles).  One cooperative launch runs all rounds for the whole batch,
+// separated by grid-wide barriers; candidates are looked up through a per-row index
+// of the raster-sorted candidate list.
+//
+// Score: DOF = |C| after pruning.  The kept list is emitted in
+// (y, x, scale) order by a chunked scan (no atomics decide positions).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace mhfd {
+
+namespace cg = cooperative_groups;
+
+constexpr uint8_t kUndecided = 0, kKept = 1, kRemoved = 2;
+constexpr int kChunk = 256;
+
+struct PruneArgs {
+  int B, W, H;
+  int64_t cap;              // candidate capacity per image
+  const mhfd_blob* cand;    // B x cap, raster order
+  const int32_t* ncand;     // exact candidate counts
+  double overlap;
+  int prune;                // overlap < 1
+  double radmax;
+  double rad[kMaxLevels];   // sqrt(2) * t_s
+  uint8_t* st;              // B x cap
+  int32_t* rowstart;        // B x (H + 1)
+  int64_t* img_off;         // B + 1: prefix of effective candidate counts
+  int64_t* chunk_off;       // B + 1: prefix of chunk counts
+  int32_t* chunk_cnt;       // kept per chunk
+  int32_t* chunk_pos;       // exclusive kept offsets per chunk (within the image)
+  int32_t* counters;        // 4 ints: undecided counters (3) + round count
+  mhfd_blob* blobs;         // nullable: B x blob_cap output
+  int32_t blob_cap;
+  int32_t* counts;          // nullable
+  double* scores;           // nullable
+  int32_t* flags;           // nullable
+};
+
+__device__ __forceinline__ double lens_fraction(double d, double r1, double r2) {
+  const double rmin = fmin(r1, r2);
+  if (d >= r1 + r2) return 0.0;
+  if (d <= fabs(r1 - r2)) return 1.0;
+  double a1 = (d * d + r1 * r1 - r2 * r2) / (2.0 * d * r1);
+  double a2 = (d * d + r2 * r2 - r1 * r1) / (2.0 * d * r2);
+  a1 = fmin(1.0, fmax(-1.0, a1));
+  a2 = fmin(1.0, fmax(-1.0, a2));
+  double k = (-d + r1 + r2) * (d + r1 - r2) * (d - r1 + r2) * (d + r1 + r2);
+  k = fmax(k, 0.0);
+  const double area = r1 * r1 * acos(a1) + r2 * r2 * acos(a2) - 0.5 * sqrt(k);
+  return area / (3.14159265358979323846 * rmin * rmin);
+}
+
+__device__ __forceinline__ int image_of(const int64_t* off, int B, int64_t g) {
+  int lo = 0, hi = B;  // largest b with off[b] <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
+  const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+  const uint8_t* st = a.st + (int64_t)b * a.cap;
+  const int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
+  const mhfd_blob me = C[k];
+  const double r = a.rad[me.scale];
+  const int Dm = (int)ceil(r + a.radmax);
+  bool blocked = false;
+  const int ylo = max(0, me.y - Dm), yhi = min(a.H - 1, me.y + Dm);
+  for (int yy = ylo; yy <= yhi; ++yy) {
+    int lo = rs[yy];
+    const int hi = rs[yy + 1];
+    if (lo >= hi) continue;
+    int h2 = hi;  // lower_bound on x >= me.x - Dm
+    const int xmin = me.x - Dm;
+    while (lo < h2) {
+      const int mid = (lo + h2) >> 1;
+      if (C[mid].x < xmin) lo = mid + 1; else h2 = mid;
+    }
+    for (int q = lo; q < hi; ++q) {
+      const mhfd_blob o = C[q];
+      if (o.x > me.x + Dm) break;
+      if (q == k) continue;
+      const bool higher = o.scale > me.scale ||
+                          (o.scale == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
+      if (!higher) continue;
+      const double dx = (double)(o.x - me.x), dy = (double)(o.y - me.y);
+      if (lens_fraction(sqrt(dx * dx + dy * dy), r, a.rad[o.scale]) > a.overlap) {
+        const uint8_t s = __ldcg(st + q);
+        if (s == kKept) return kRemoved;
+        if (s == kUndecided) blocked = true;
+      }
+    }
+  }
+  return blocked ? kUndecided : kKept;
+}
+
+__global__ void __launch_bounds__(256) k_prune(PruneArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+  __shared__ int32_t red[8];
+  __shared__ int32_t wpre[8];
+
+  // phase 0: per-image prefixes (one thread; B is small)
+  if (gtid == 0) {
+    int64_t o = 0, c = 0;
+    for (int b = 0; b < a.B; ++b) {
+      a.img_off[b] = o;
+      a.chunk_off[b] = c;
+      const int64_t n = min((int64_t)a.ncand[b], a.cap);
+      o += n;
+      c += (n + kChunk - 1) / kChunk;
+    }
+    a.img_off[a.B] = o;
+    a.chunk_off[a.B] = c;
+    a.counters[0] = a.counters[1] = a.counters[2] = 0;
+    a.counters[3] = 0;
+  }
+  grid.sync();
+  const int64_t total = a.img_off[a.B];
+  const int64_t nchunks = a.chunk_off[a.B];
+
+  // phase 1: row index (lower bound of each row in the raster-sorted list), init states
+  for (int64_t g = gtid; g < (int64_t)a.B * (a.H + 1); g += gsize) {
+    const int b = (int)(g / (a.H + 1));
+    const int y = (int)(g - (int64_t)b * (a.H + 1));
+    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (C[mid].y < y) lo = mid + 1; else hi = mid;
+    }
+    a.rowstart[g] = (int32_t)lo;
+  }
+  for (int64_t g = gtid; g < total; g += gsize) {
+    const int b = image_of(a.img_off, a.B, g);
+    a.st[(int64_t)b * a.cap + (g - a.img_off[b])] = a.prune ? kUndecided : kKept;
+  }
+  grid.sync();
+
+  // phase 2: decision rounds
+  if (a.prune) {
+    for (int round = 0;; ++round) {
+      if (gtid == 0) a.counters[(round + 1) % 3] = 0;
+      int undecided = 0;
+      for (int64_t g = gtid; g < total; g += gsize) {
+        const int b = image_of(a.img_off, a.B, g);
+        const int64_t k = g - a.img_off[b];
+        uint8_t* sp = a.st + (int64_t)b * a.cap + k;
+        if (__ldcg(sp) != kUndecided) continue;
+        const uint8_t d = decide(a, b, k);
+        if (d != kUndecided) __stcg(sp, d); else ++undecided;
+      }
+      if (undecided) atomicAdd(&a.counters[round % 3], undecided);
+      grid.sync();
+      const int left = *((volatile int32_t*)&a.counters[round % 3]);
+      if (gtid == 0) a.counters[3] = round + 1;
+      if (left == 0) break;
+    }
+  }
+  grid.sync();
+
+  // phase 3: kept count per chunk of 256 candidates
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int b = image_of(a.chunk_off, a.B, c);
+    const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
+    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const bool kept = k < n && __ldcg(a.st + (int64_t)b * a.cap + k) == kKept;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, kept));
+    if (lane == 0) red[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      a.chunk_cnt[c] = s;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+
+  // phase 4: per-image exclusive scan over chunks (one warp per image)
+  {
+    const int64_t gw = gtid >> 5, nw = gsize >> 5;
+    for (int64_t b = gw; b < a.B; b += nw) {
+      int64_t run = 0;
+      for (int64_t c0 = a.chunk_off[b]; c0 < a.chunk_off[b + 1]; c0 += 32) {
+        const int64_t c = c0 + lane;
+        const int v = c < a.chunk_off[b + 1] ? __ldcg(a.chunk_cnt + c) : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (c < a.chunk_off[b + 1]) a.chunk_pos[c] = (int32_t)(run + x - v);
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) {
+        const int32_t nc = a.ncand[b];
+        const int64_t count = a.prune ? run : (int64_t)nc;   // overlap = 1: every candidate kept
+        int32_t f = (nc > a.cap) ? 1 : 0;
+        if (a.blobs && count > a.blob_cap) f |= 2;
+        if (a.counts) a.counts[b] = (int32_t)count;
+        if (a.scores) a.scores[b] = (double)count;
+        if (a.flags) a.flags[b] = f;
+      }
+    }
+  }
+  if (!a.blobs) return;
+  grid.sync();
+
+  // phase 5: write kept blobs in (y, x, scale) order
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int b = image_of(a.chunk_off, a.B, c);
+    const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
+    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const bool kept = k < n && __ldcg(a.st + (int64_t)b * a.cap + k) == kKept;
+    const uint32_t m = __ballot_sync(0xffffffffu, kept);
+    if (lane == 0) red[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int w = 0; w < 8; ++w) { wpre[w] = s; s += red[w]; }
+    }
+    __syncthreads();
+    if (kept) {
+      const int64_t pos = (int64_t)__ldcg(a.chunk_pos + c) + wpre[warp] + __popc(m & ((1u << lane) - 1u));
+      if (pos < a.blob_cap) a.blobs[(int64_t)b * a.blob_cap + pos] = a.cand[(int64_t)b * a.cap + k];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mhfd

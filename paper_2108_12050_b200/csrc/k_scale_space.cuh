@@ -1,0 +1,415 @@
+// k_scale_space.cuh — stretch-on-load prepass and the hot kernel: separable Gaussian
+// blur at all n+1 scales, Eq. 2 DoG and the Eq. 3 inner argmax over scale, fused (hot-
+// path rows a2-a6).  The response stack never touches HBM: per pixel only v = max_i DoG
+// (f32) and its first argmax (u8) are written (or, in 26-NMS / dump mode, the n planes).
+//
+//  PAPER.md:257        I' = clamp((I-lo)/(hi-lo), 0, 1)   (centred by -1/2; the DoG is
+//                      unchanged because every level's taps sum to 1)      [k_normalize]
+//  PAPER.md:136-141    L(.,.,t_i) = G(t_i) * I', sigma = t_i, periodic boundary
+//                      (readings R1, R7); taps sampled, renormalised, |d| <= ceil(5 t_i)
+//                      (reading R6)
+//  PAPER.md:171        DoG_i = t_i (L_{i+1} - L_i)
+//  PAPER.md:240-244    v = max_i DoG_i, i^ = first argmax (reading R10)
+//
+// Layout: one CTA = one image x one strip of 32 columns x one band of
+// BH = 8*RPT rows; 256 threads, 2 CTAs per SM.  Levels are processed one after another.
+//   row pass   : chunks of 32 rows x (32+2R+pad) columns of the normalised f32 image are
+//                brought into shared memory by TMA (one 2-D cp.async.bulk.tensor box per
+//                chunk; chunks that wrap around the image edge use one 1-D cp.async.bulk
+//                per row, split at the edge), in a 3-stage mbarrier pipeline so the copies
+//                of chunks k+1, k+2 overlap the FMAs of chunk k.  Lane =
+//                row; each thread convolves 4 consecutive columns with 128-bit LDS (row
+//                pitch = 4 x odd words -> conflict-free), writing (BH+2R+p) x 32 filtered
+//                rows to `hbuf`.
+//   column pass: lane = column, each thread convolves RPT consecutive rows (8 at a time)
+//                from `hbuf`, then updates DoG / running max / argmax held in registers.
+// Taps are prefixed with p = (-R) mod 4 zeros so every window starts 16-byte aligned; the
+// same prefixed table serves both passes (hbuf row 0 = band row -R-p).  The tap table is
+// copied from the kernel parameters into shared memory once per CTA and read with
+// broadcast 128-bit loads (4 weights per instruction).
+#pragma once
+#include "common.cuh"
+
+namespace mhfd {
+
+constexpr int kChunkRows = 32;
+constexpr int kStages = 3;         // stage buffers in the copy pipeline
+constexpr int kHP = kStripW + 1;   // hbuf pitch (odd: conflict-free row-pass stores)
+
+// stage pitch: 4*q floats with q odd (conflict-free LDS.128 with lane = row), holding
+// 32 + 2R + p columns plus the window overrun of the padded tap loop
+__host__ __device__ inline int stage_pitch(int rmax) {
+  int q = (2 * rmax + 47 + 3) / 4;   // >= 32+2R+p+3 staged columns and the 2R+p+43 window reach
+  if ((q & 1) == 0) ++q;
+  return 4 * q;
+}
+__host__ __device__ inline int hbuf_rows(int rmax, int BH) { return BH + 2 * rmax + 3 + 16; }
+// hbuf floats, rounded to 32 so the tap table and mbarriers after it stay 128-byte aligned
+__host__ __device__ inline int hbuf_floats(int rmax, int BH) { return (hbuf_rows(rmax, BH) * kHP + 31) & ~31; }
+__host__ __device__ inline int wtab_floats(int ntaps_total) { return (ntaps_total + 31) & ~31; }
+// layout: [stage: kStages x 32 x SP][hbuf][weights][mbarriers]
+__host__ __device__ inline size_t scale_space_smem(int rmax, int BH, int ntaps_total) {
+  return sizeof(float) * ((size_t)kStages * kChunkRows * stage_pitch(rmax) + 64 + (size_t)hbuf_floats(rmax, BH) +
+                          wtab_floats(ntaps_total)) +
+         8 * kStages;
+}
+// 2-D TMA boxes hold SP <= 256 columns
+__host__ __device__ inline bool tma_boxes(int rmax) { return stage_pitch(rmax) <= 256; }
+// the bulk-copy staging path needs every row segment to wrap at most once, at a
+// 16-byte boundary
+__host__ __device__ inline bool fast_staging(int W, int rmax) { return (W % 4) == 0 && W >= kStripW + 2 * rmax + 16; }
+
+__device__ __forceinline__ int wrap_idx(int a, int n) {
+  while (a < 0) a += n;
+  while (a >= n) a -= n;
+  return a;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_2d_g2s(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------------
+// k_normalize: u8/u16 -> centred f32 I' - 1/2, row-major W floats per row (a2).
+template <int BPP>
+__global__ void __launch_bounds__(256) k_normalize(const uint8_t* __restrict__ images, Shape s,
+                                                   const ImgPar* __restrict__ par, float* __restrict__ out) {
+  const int b = blockIdx.y;
+  const ImgPar ip = par[b];
+  const float lo = (float)ip.lo, inv = ip.inv;
+  const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
+  float* o = out + (int64_t)b * s.H * s.W;
+  const int64_t total = (int64_t)s.H * s.W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / s.W), x = (int)(i - (int64_t)y * s.W);
+    const float p = (float)load_px(img, s.pitch, BPP, y, x);
+    o[i] = fminf(fmaxf((p - lo) * inv, 0.f), 1.f) - 0.5f;
+  }
+}
+
+// vectorised variant: 16 input bytes per thread-iteration; needs W % 16 == 0 (u8) or
+// W % 8 == 0 (u16)
+template <int BPP>
+__global__ void __launch_bounds__(256) k_normalize_vec(const uint8_t* __restrict__ images, Shape s,
+                                                       const ImgPar* __restrict__ par, float* __restrict__ out) {
+  constexpr int PX = 16 / BPP;   // pixels per 16-byte vector
+  const int b = blockIdx.y;
+  const ImgPar ip = par[b];
+  const float lo = (float)ip.lo, inv = ip.inv;
+  const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
+  float* o = out + (int64_t)b * s.H * s.W;
+  const int vpr = s.W / PX;  // vectors per row
+  const int64_t total = (int64_t)s.H * vpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / vpr), v = (int)(i - (int64_t)y * vpr);
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(img + (int64_t)y * s.pitch) + v);
+    const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
+    float f[PX];
+#pragma unroll
+    for (int k = 0; k < PX; ++k) {
+      const uint32_t p = BPP == 1 ? (wds[k >> 2] >> (8 * (k & 3))) & 0xffu : (wds[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+      f[k] = fminf(fmaxf(((float)p - lo) * inv, 0.f), 1.f) - 0.5f;
+    }
+    float4* dst = reinterpret_cast<float4*>(o + (int64_t)y * s.W + (int64_t)v * PX);
+#pragma unroll
+    for (int k = 0; k < PX / 4; ++k) dst[k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// acc[o] += sum_{jj<4} w[jj] * x[o+jj], o = 0..3, window x = a ++ b
+__device__ __forceinline__ void tap4(float (&acc)[4], const float4& a, const float4& b, const float* w) {
+  const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const float wj = w[jj];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) acc[o] = fmaf(wj, x[o + jj], acc[o]);
+  }
+}
+
+// row pass: out[o] = sum_{t<ntap} w[t] * src[o+t], o = 0..3; src 16-byte aligned, ntap % 8 == 0
+__device__ __forceinline__ void conv4_row(float (&acc)[4], const float* __restrict__ src, const float* __restrict__ w,
+                                          int ntap) {
+#pragma unroll
+  for (int o = 0; o < 4; ++o) acc[o] = 0.f;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4 a = s4[0], b;
+  for (int j = 0; j < ntap; j += 8) {
+    b = s4[(j >> 2) + 1];
+    tap4(acc, a, b, w + j);
+    a = s4[(j >> 2) + 2];
+    tap4(acc, b, a, w + j + 4);
+  }
+}
+
+// acc[o] += sum_{jj<8} w[jj] * x[o+jj], o = 0..7, window x = a[0..7] ++ b[0..6]
+__device__ __forceinline__ void tap8(float (&acc)[8], const float (&a)[8], const float (&b)[8], const float* w) {
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const float wj = w[jj];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const int k = o + jj;
+      acc[o] = fmaf(wj, k < 8 ? a[k] : b[k - 8], acc[o]);
+    }
+  }
+}
+
+// column pass: out[o] = sum_{t<ntap} w[t] * src[(o+t)*stride], o = 0..7, ntap % 8 == 0
+__device__ __forceinline__ void conv8_col(float (&acc)[8], const float* __restrict__ src, int stride,
+                                          const float* __restrict__ w, int ntap) {
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = 0.f;
+  float xa[8], xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) xa[k] = src[k * stride];
+  int j0 = 0;
+  for (; j0 + 16 <= ntap; j0 += 16) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xb[k] = src[(j0 + 8 + k) * stride];
+    tap8(acc, xa, xb, w + j0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xa[k] = src[(j0 + 16 + k) * stride];
+    tap8(acc, xb, xa, w + j0 + 8);
+  }
+  if (j0 < ntap) {  // ntap % 16 == 8: one more group
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xb[k] = src[(j0 + 8 + k) * stride];
+    tap8(acc, xa, xb, w + j0);
+  }
+}
+
+// Stage rows [r0, r0 + nrow) of a level's row-pass input (image rows Y0-R-p+r, columns
+// x0-R-p .. x0+32+R+3) into `dst0` (kChunkRows x SP floats).  FAST: warp 0 issues one
+// bulk copy per row (two where the row wraps at the image edge) completing on `bar`;
+// otherwise every thread copies with plain loads (caller synchronises).
+template <bool FAST>
+__device__ __forceinline__ void stage_rows(float* dst0, uint64_t* bar, const float* __restrict__ img,
+                                           const void* tmap, int b, int W, int H, int x0, int Y0, int R, int p,
+                                           int r0, int nrow, int SP, int warp, int lane) {
+  const int xs = x0 - R - p;                  // first staged column (multiple of 4)
+  const int ncol = (kStripW + 2 * R + p + 3) & ~3;
+  const int yf = Y0 - R - p + r0;             // first image row of the chunk
+  if (FAST && tmap != nullptr && xs >= 0 && xs + ncol <= W && yf >= 0 && yf + nrow <= H) {
+    // interior chunk: one 2-D box of 32 rows x SP columns (rows/columns past the needed
+    // ones are harmless: they meet zero taps or are not stored)
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(bar, (uint32_t)(kChunkRows * SP * 4));
+      tma_2d_g2s(dst0, tmap, xs, b * H + yf, bar);
+    }
+  } else if (FAST) {
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nrow * ncol * 4));
+      __syncwarp();
+      if (lane < nrow) {
+        const int y = wrap_idx(Y0 - R - p + r0 + lane, H);
+        const float* row = img + (int64_t)y * W;
+        float* dst = dst0 + lane * SP;
+        if (xs < 0) {
+          bulk_g2s(dst, row + (W + xs), (uint32_t)(-xs * 4), bar);
+          bulk_g2s(dst - xs, row, (uint32_t)((ncol + xs) * 4), bar);
+        } else if (xs + ncol > W) {
+          bulk_g2s(dst, row + xs, (uint32_t)((W - xs) * 4), bar);
+          bulk_g2s(dst + (W - xs), row, (uint32_t)((xs + ncol - W) * 4), bar);
+        } else {
+          bulk_g2s(dst, row + xs, (uint32_t)(ncol * 4), bar);
+        }
+      }
+    }
+  } else {
+    for (int k = warp; k < nrow; k += 8) {
+      const int y = wrap_idx(Y0 - R - p + r0 + k, H);
+      const float* row = img + (int64_t)y * W;
+      for (int cc = lane; cc < ncol; cc += 32) dst0[k * SP + cc] = row[wrap_idx(xs + cc, W)];
+    }
+  }
+}
+
+template <int RPT, bool WRITE_V, bool WRITE_DOG, bool FAST>
+__global__ void __launch_bounds__(kThreads, 2)
+k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict__ par,
+              const __grid_constant__ LevelTable tab, const __grid_constant__ CUtensorMap tmap, int use_tmap,
+              float* __restrict__ v_out,
+              uint8_t* __restrict__ idx_out, float* __restrict__ dog_out) {
+  constexpr int BH = 8 * RPT;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw);
+  const int rmax = tab.rmax;
+  const int SP = stage_pitch(rmax);
+  float* stage = smem;                                         // kStages x kChunkRows x SP
+  float* hbuf = smem + kStages * kChunkRows * SP + 64;         // hbuf_rows x kHP
+  float* wsm = hbuf + hbuf_floats(rmax, BH);                   // tap table
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + wtab_floats(tab.ntaps_total));
+
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * kStripW;
+  const int Y0 = blockIdx.y * BH;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const float* img = fimg + (int64_t)b * s.H * s.W;
+  const int64_t plane = (int64_t)s.H * s.W;
+
+  if (par[b].degen) {  // hi == lo: I' == 0, every DoG plane is exactly 0
+    const int x = x0 + lane;
+    for (int r = 0; r < RPT; ++r) {
+      const int y = Y0 + warp * RPT + r;
+      if (x < s.W && y < s.H) {
+        const int64_t p = (int64_t)y * s.W + x;
+        if (WRITE_V) { v_out[(int64_t)b * plane + p] = 0.f; idx_out[(int64_t)b * plane + p] = 0; }
+        if (WRITE_DOG)
+          for (int i = 0; i + 1 < tab.nlev; ++i) dog_out[((int64_t)b * (tab.nlev - 1) + i) * plane + p] = 0.f;
+      }
+    }
+    return;
+  }
+
+  // zero stage and hbuf once: entries past a level's valid columns / rows are read only
+  // against zero (padding) taps and must stay finite
+  const int nzero = kStages * kChunkRows * SP + 64 + hbuf_floats(rmax, BH);
+  for (int i = threadIdx.x; i < nzero; i += kThreads) smem[i] = 0.f;
+  for (int i = threadIdx.x; i < tab.ntaps_total; i += kThreads) wsm[i] = tab.w[i];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const void* tm = use_tmap ? (const void*)&tmap : nullptr;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  float lprev[RPT], vbest[RPT];
+  uint32_t ibest[RPT / 4];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) { lprev[r] = 0.f; vbest[r] = -INFINITY; }
+#pragma unroll
+  for (int r = 0; r < RPT / 4; ++r) ibest[r] = 0u;
+
+  const int nlev = tab.nlev;
+  uint32_t phases = 0u;   // bit k: parity of mbarrier k
+  // (lev, r0) of the items one and two ahead of the current one
+  auto rows_of = [BH](int R, int p) { return BH + 2 * R + p; };
+  int l1 = 0, q1 = 0, l2 = 0, q2 = 0;
+  {  // prologue: stage items 0 and 1
+    stage_rows<FAST>(stage, &bars[0], img, tm, b, s.W, s.H, x0, Y0, tab.R[0], tab.pre[0], 0,
+                     min(kChunkRows, rows_of(tab.R[0], tab.pre[0])), SP, warp, lane);
+    l1 = 0; q1 = kChunkRows;
+    if (q1 >= rows_of(tab.R[0], tab.pre[0])) { l1 = 1; q1 = 0; }
+    if (l1 < nlev) {
+      const int R1 = tab.R[l1], p1 = tab.pre[l1];
+      stage_rows<FAST>(stage + kChunkRows * SP, &bars[1], img, tm, b, s.W, s.H, x0, Y0, R1, p1, q1,
+                       min(kChunkRows, rows_of(R1, p1) - q1), SP, warp, lane);
+    }
+  }
+  int item = 0;           // (level, chunk) items rotate through the kStages buffers
+  int buf = 0;
+
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int ntap = tab.ntap[lev];
+    const float* w = wsm + tab.woff[lev];
+    const int nrow = rows_of(tab.R[lev], tab.pre[lev]);   // hbuf rows: band rows -R-p .. BH+R-1
+
+    // ---------------- row pass (chunks of 32 rows) ----------------
+    for (int r0 = 0; r0 < nrow; r0 += kChunkRows, ++item) {
+      {  // prefetch item + 2 into the buffer freed by item - 1
+        l2 = l1; q2 = q1 + kChunkRows;
+        if (l2 < nlev && q2 >= rows_of(tab.R[l2], tab.pre[l2])) { ++l2; q2 = 0; }
+        if (l1 < nlev && l2 < nlev) {
+          const int R2 = tab.R[l2], p2 = tab.pre[l2];
+          const int b2 = buf == 0 ? 2 : buf - 1;
+          stage_rows<FAST>(stage + b2 * kChunkRows * SP, &bars[b2], img, tm, b, s.W, s.H, x0, Y0, R2, p2, q2,
+                           min(kChunkRows, rows_of(R2, p2) - q2), SP, warp, lane);
+        }
+        l1 = l2; q1 = q2;
+      }
+      if (FAST) {
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+      } else {
+        __syncthreads();
+      }
+      const float* src = stage + buf * kChunkRows * SP + lane * SP + 4 * warp;
+      float acc[4];
+      conv4_row(acc, src, w, ntap);
+      if (r0 + lane < nrow) {
+        float* h = hbuf + (r0 + lane) * kHP + 4 * warp;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) h[o] = acc[o];
+      }
+      buf = buf == 2 ? 0 : buf + 1;
+      __syncthreads();   // stage[item % 3] is free for the copy issued in the next iteration
+    }
+
+    // ---------------- column pass + DoG + running argmax ----------------
+    const float tprev = lev > 0 ? tab.tdog[lev - 1] : 0.f;
+#pragma unroll
+    for (int q = 0; q < RPT / 8; ++q) {
+      const int rb = warp * RPT + q * 8;      // first band row of this group
+      float acc[8];
+      conv8_col(acc, hbuf + rb * kHP + lane, kHP, w, ntap);
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int r = q * 8 + o;
+        const float L = acc[o];
+        if (lev > 0) {
+          const float D = tprev * (L - lprev[r]);
+          if (D > vbest[r]) {
+            vbest[r] = D;
+            const int sh = (r & 3) * 8;
+            ibest[r >> 2] = (ibest[r >> 2] & ~(0xffu << sh)) | ((uint32_t)(lev - 1) << sh);
+          }
+          if (WRITE_DOG) {
+            const int x = x0 + lane, y = Y0 + rb + o;
+            if (x < s.W && y < s.H)
+              dog_out[((int64_t)b * (tab.nlev - 1) + (lev - 1)) * plane + (int64_t)y * s.W + x] = D;
+          }
+        }
+        lprev[r] = L;
+      }
+    }
+    __syncthreads();  // hbuf is rewritten by the next level
+  }
+
+  if (WRITE_V) {
+    const int x = x0 + lane;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int y = Y0 + warp * RPT + r;
+      if (x < s.W && y < s.H) {
+        const int64_t p = (int64_t)b * plane + (int64_t)y * s.W + x;
+        v_out[p] = vbest[r];
+        idx_out[p] = (uint8_t)((ibest[r >> 2] >> ((r & 3) * 8)) & 0xffu);
+      }
+    }
+  }
+}
+
+}  // namespace mhfd

@@ -1,0 +1,674 @@
+// mhfd.cu — C-ABI (include/mhfd.h) and host orchestration of the MHFD CUDA path.
+//
+// Host side: validate arguments, build the scale grid and f32 tap tables from f64
+// (PAPER.md:134-137, 166-168), carve the caller's workspace, and enqueue the launch
+// sequence on the caller's stream without any host synchronisation:
+//
+//   k_hist / k_select (u8: 1 pass, u16: 2 passes)   percentiles, row a1
+//   k_scale_space                                   stretch+blur+DoG+argmax, rows a2-a6
+//   k_nms_count -> k_seg_scan -> k_nms_write        NMS+threshold+compaction, rows a7-a8
+//   k_prune (cooperative, one launch)               pruning + score + ordered list, a9-a10
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "k_nms.cuh"
+#include "k_percentile.cuh"
+#include "k_prune.cuh"
+#include "k_scale_space.cuh"
+
+using namespace mhfd;
+
+struct mhfd_ctx {
+  mhfd_params p;
+  LevelTable* tab;   // host copy, passed by value to k_scale_space
+  int n;             // DoG planes
+  double dt;
+  double t[kMaxLevels];
+  double rad[kMaxLevels];
+  double radmax;
+  int64_t cap;       // candidates per image
+  int prune_grid;    // cooperative grid size for k_prune
+  int sms;
+  // bench instrumentation (mhfd_timing_*): 5 events per recorded call
+  cudaEvent_t* tev;
+  int tmax, tcount;
+  // e2e host path (mhfd_focus_score_host): copy stream + double-buffer events
+  cudaStream_t copy_stream;
+  cudaEvent_t ev_ready[2], ev_free[2];
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+mhfd_status fail(mhfd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+mhfd_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(MHFD_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, imgoff, chunkoff,
+      chunkcnt, chunkpos, counters, scores, counts, total;
+};
+
+int nseg_of(const mhfd_ctx* c) {
+  const int64_t plane = (int64_t)c->p.width * c->p.height;
+  return (int)((plane + kSeg - 1) / kSeg);
+}
+
+Layout layout(const mhfd_ctx* c, int B) {
+  Layout L{};
+  const int64_t plane = (int64_t)c->p.width * c->p.height;
+  const int64_t nseg = nseg_of(c);
+  const int64_t nchunk = (c->cap + kChunk - 1) / kChunk;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
+  L.par = take(sizeof(ImgPar) * B);
+  L.sel = take(sizeof(SelState) * B);
+  L.hist1 = take(sizeof(uint32_t) * 256 * B);
+  L.hist2 = take(sizeof(uint32_t) * 512 * B);
+  L.fimg = take(sizeof(float) * plane * B);
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  L.v = take(paper ? sizeof(float) * plane * B : 0);
+  L.idx = take(paper ? plane * B : 0);
+  L.dog = take(paper ? 0 : sizeof(float) * plane * c->n * B);
+  L.segcnt = take(sizeof(int32_t) * nseg * B);
+  L.segoff = take(sizeof(int32_t) * nseg * B);
+  L.ncand = take(sizeof(int32_t) * B);
+  L.cand = take(sizeof(mhfd_blob) * c->cap * B);
+  L.st = take(c->cap * B);
+  L.rowstart = take(sizeof(int32_t) * (c->p.height + 1) * (size_t)B);
+  L.imgoff = take(sizeof(int64_t) * (B + 1));
+  L.chunkoff = take(sizeof(int64_t) * (B + 1));
+  L.chunkcnt = take(sizeof(int32_t) * nchunk * B);
+  L.chunkpos = take(sizeof(int32_t) * nchunk * B);
+  L.counters = take(sizeof(int32_t) * 8);
+  L.scores = take(sizeof(double) * B);
+  L.counts = take(sizeof(int32_t) * B);
+  L.total = o;
+  return L;
+}
+
+mhfd_status check_call(const mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch, int64_t pitch,
+                       const void* ws, size_t ws_bytes) {
+  if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!d_images) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_images is NULL");
+  if (dtype != MHFD_U8 && dtype != MHFD_U16) return fail(MHFD_ERR_INVALID_ARGUMENT, "dtype %d", dtype);
+  if (batch < 1) return fail(MHFD_ERR_SHAPE, "batch %d < 1", batch);
+  const int bpp = dtype == MHFD_U8 ? 1 : 2;
+  if (pitch < (int64_t)c->p.width * bpp || pitch % 16 != 0)
+    return fail(MHFD_ERR_SHAPE, "pitch_bytes %lld: need >= width*bpp and a multiple of 16", (long long)pitch);
+  if (((uintptr_t)d_images) % 16 != 0) return fail(MHFD_ERR_SHAPE, "d_images not 16-byte aligned");
+  if (!ws) return fail(MHFD_ERR_WORKSPACE, "workspace is NULL");
+  if (((uintptr_t)ws) % 256 != 0) return fail(MHFD_ERR_WORKSPACE, "workspace not 256-byte aligned");
+  const size_t need = layout(c, batch).total;
+  if (ws_bytes < need) return fail(MHFD_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != c->p.device)
+    return fail(MHFD_ERR_DEVICE, "current device %d != context device %d", dev, c->p.device);
+  return MHFD_OK;
+}
+
+#define LAUNCH_CHECK(where)                                  \
+  do {                                                       \
+    cudaError_t e_ = cudaGetLastError();                     \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where);      \
+    ++launches;                                              \
+  } while (0)
+
+// Everything up to the candidate list.  dog_dump (nullable) receives the DoG planes.
+cudaEvent_t* next_timing(mhfd_ctx* c) {
+  if (!c->tev || c->tcount >= c->tmax) return nullptr;
+  return c->tev + 5 * (c->tcount++);
+}
+
+#define MARK(k)                                                     \
+  do {                                                              \
+    if (ev) {                                                       \
+      cudaError_t em_ = cudaEventRecord(ev[k], st);                 \
+      if (em_ != cudaSuccess) return cuda_fail(em_, "event record"); \
+    }                                                               \
+  } while (0)
+
+mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t B, int64_t pitch, char* ws,
+                      const Layout& L, float* dog_dump, cudaStream_t st, int& launches, cudaEvent_t* ev) {
+  MARK(0);
+  const int W = c->p.width, H = c->p.height;
+  const int bpp = dtype == MHFD_U8 ? 1 : 2;
+  const Shape s{W, H, pitch, bpp};
+  const uint8_t* img = static_cast<const uint8_t*>(d_images);
+  ImgPar* par = reinterpret_cast<ImgPar*>(ws + L.par);
+  SelState* sel = reinterpret_cast<SelState*>(ws + L.sel);
+  uint32_t* h1 = reinterpret_cast<uint32_t*>(ws + L.hist1);
+  uint32_t* h2 = reinterpret_cast<uint32_t*>(ws + L.hist2);
+
+  // ---- a1: percentiles
+  const int64_t N = (int64_t)W * H;
+  RankPar rp;
+  rp.npx = N;
+  rp.rank_lo = std::min<int64_t>((int64_t)std::floor((double)c->p.sat_low * (double)N), N - 1);
+  rp.rank_hi = N - 1 - std::min<int64_t>((int64_t)std::floor((double)c->p.sat_high * (double)N), N - 1);
+  cudaError_t e = cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 256 * B, st);
+  if (e == cudaSuccess && bpp == 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset hist");
+  int rows_per_cta = std::max(1, (int)((int64_t)H * B / (c->sms * 8)));
+  rows_per_cta = std::min(rows_per_cta, 64);
+  dim3 hg((H + rows_per_cta - 1) / rows_per_cta, B);
+  if (bpp == 1) {
+    k_hist<1, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
+    LAUNCH_CHECK("k_hist");
+    k_select1<1><<<(B + 127) / 128, 128, 0, st>>>(h1, rp, sel, par, B);
+    LAUNCH_CHECK("k_select1");
+  } else {
+    k_hist<2, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
+    LAUNCH_CHECK("k_hist");
+    k_select1<2><<<(B + 127) / 128, 128, 0, st>>>(h1, rp, sel, par, B);
+    LAUNCH_CHECK("k_select1");
+    k_hist<2, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    LAUNCH_CHECK("k_hist2");
+    k_select2<<<(B + 127) / 128, 128, 0, st>>>(h2, sel, par, B);
+    LAUNCH_CHECK("k_select2");
+  }
+
+  MARK(1);
+  // ---- a2: stretch on load -> centred f32 image
+  float* fimg = reinterpret_cast<float*>(ws + L.fimg);
+  {
+    const int64_t plane = (int64_t)W * H;
+    const bool vec = (bpp == 1) ? (W % 16 == 0) : (W % 8 == 0);
+    const int64_t work = vec ? plane / (16 / bpp) : plane;
+    dim3 gn((unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)c->sms * 8), B);
+    if (vec) {
+      if (bpp == 1) k_normalize_vec<1><<<gn, 256, 0, st>>>(img, s, par, fimg);
+      else k_normalize_vec<2><<<gn, 256, 0, st>>>(img, s, par, fimg);
+    } else {
+      if (bpp == 1) k_normalize<1><<<gn, 256, 0, st>>>(img, s, par, fimg);
+      else k_normalize<2><<<gn, 256, 0, st>>>(img, s, par, fimg);
+    }
+    LAUNCH_CHECK("k_normalize");
+  }
+  // ---- a3-a6: fused blur + DoG + argmax
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  float* v = reinterpret_cast<float*>(ws + L.v);
+  uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
+  float* dog = dog_dump ? dog_dump : reinterpret_cast<float*>(ws + L.dog);
+  const bool write_dog = dog_dump != nullptr || !paper;
+  const int strips = (W + kStripW - 1) / kStripW;
+  // band height: 256 rows when that still gives >= 4 waves of 2 CTAs/SM, else 128
+  const int64_t ctas256 = (int64_t)strips * ((H + 255) / 256) * B;
+  const int RPT = (ctas256 >= (int64_t)c->sms * 2 * 4) ? 32 : 16;
+  const int BH = 8 * RPT;
+  const size_t smem = scale_space_smem(c->tab->rmax, BH, c->tab->ntaps_total);
+  const bool fast = fast_staging(W, c->tab->rmax);
+  // 2-D TMA descriptor of the normalised batch viewed as a (B*H) x W f32 matrix
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  int use_tmap = 0;
+  if (fast && tma_boxes(c->tab->rmax)) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (encode) {
+      const cuuint64_t gdim[2] = {(cuuint64_t)W, (cuuint64_t)H * (cuuint64_t)B};
+      const cuuint64_t gstride[1] = {(cuuint64_t)W * 4};
+      const cuuint32_t box[2] = {(cuuint32_t)stage_pitch(c->tab->rmax), (cuuint32_t)kChunkRows};
+      const cuuint32_t estr[2] = {1, 1};
+      CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, fimg, gdim, gstride, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      use_tmap = (r == CUDA_SUCCESS) ? 1 : 0;
+    }
+  }
+  dim3 g3(strips, (H + BH - 1) / BH, B);
+  const Shape sf{W, H, (int64_t)W * 4, 4};
+  auto launch_ss = [&](auto kern) -> cudaError_t {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return ea;
+    kern<<<g3, kThreads, smem, st>>>(fimg, sf, par, *c->tab, tmap, use_tmap, v, idx, dog);
+    return cudaGetLastError();
+  };
+#define SS_VARIANTS(RPTV, FASTV)                                                              \
+  (paper && write_dog) ? launch_ss(k_scale_space<RPTV, true, true, FASTV>)                    \
+  : paper              ? launch_ss(k_scale_space<RPTV, true, false, FASTV>)                   \
+                       : launch_ss(k_scale_space<RPTV, false, true, FASTV>)
+  cudaError_t es;
+  if (RPT == 32) es = fast ? (SS_VARIANTS(32, true)) : (SS_VARIANTS(32, false));
+  else es = fast ? (SS_VARIANTS(16, true)) : (SS_VARIANTS(16, false));
+#undef SS_VARIANTS
+  if (es != cudaSuccess) return cuda_fail(es, "k_scale_space");
+  ++launches;
+  MARK(2);
+
+  // ---- a7-a8: NMS + threshold + ordered compaction
+  NmsArgs na{W, H, c->n, c->p.threshold, c->p.strict, v, idx, dog};
+  const int nseg = nseg_of(c);
+  int32_t* segcnt = reinterpret_cast<int32_t*>(ws + L.segcnt);
+  int32_t* segoff = reinterpret_cast<int32_t*>(ws + L.segoff);
+  int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
+  mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
+  dim3 gn((nseg + 7) / 8, B);
+  if (paper) {
+    k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
+  } else {
+    k_nms_count<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segcnt);
+  }
+  LAUNCH_CHECK("k_nms_count");
+  k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
+  LAUNCH_CHECK("k_seg_scan");
+  if (paper) {
+    k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
+  } else {
+    k_nms_write<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
+  }
+  LAUNCH_CHECK("k_nms_write");
+  MARK(3);
+  return MHFD_OK;
+}
+
+mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_blob* blobs, int32_t blob_cap,
+                      int32_t* counts, double* scores, int32_t* flags, cudaStream_t st, int& launches,
+                      cudaEvent_t* ev) {
+  PruneArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.B = B;
+  pa.W = c->p.width;
+  pa.H = c->p.height;
+  pa.cap = c->cap;
+  pa.cand = reinterpret_cast<const mhfd_blob*>(ws + L.cand);
+  pa.ncand = reinterpret_cast<const int32_t*>(ws + L.ncand);
+  pa.overlap = c->p.overlap;
+  pa.prune = c->p.overlap < 1.0f ? 1 : 0;
+  pa.radmax = c->radmax;
+  for (int s = 0; s < c->n; ++s) pa.rad[s] = c->rad[s];
+  pa.st = reinterpret_cast<uint8_t*>(ws + L.st);
+  pa.rowstart = reinterpret_cast<int32_t*>(ws + L.rowstart);
+  pa.img_off = reinterpret_cast<int64_t*>(ws + L.imgoff);
+  pa.chunk_off = reinterpret_cast<int64_t*>(ws + L.chunkoff);
+  pa.chunk_cnt = reinterpret_cast<int32_t*>(ws + L.chunkcnt);
+  pa.chunk_pos = reinterpret_cast<int32_t*>(ws + L.chunkpos);
+  pa.counters = reinterpret_cast<int32_t*>(ws + L.counters);
+  pa.blobs = blobs;
+  pa.blob_cap = blob_cap;
+  pa.counts = counts;
+  pa.scores = scores;
+  pa.flags = flags;
+  void* args[] = {&pa};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)k_prune, dim3(c->prune_grid), dim3(256), args, 0, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_prune (cooperative)");
+  ++launches;
+  MARK(4);
+  return MHFD_OK;
+}
+
+__global__ void k_copy_lohi(const ImgPar* par, int32_t* lohi, int B) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) { lohi[2 * b] = par[b].lo; lohi[2 * b + 1] = par[b].hi; }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t mhfd_abi_version(void) { return MHFD_ABI_VERSION; }
+int32_t mhfd_last_launch_count(void) { return g_launches; }
+const char* mhfd_last_error(void) { return g_err.c_str(); }
+
+const char* mhfd_status_string(mhfd_status s) {
+  switch (s) {
+    case MHFD_OK: return "MHFD_OK";
+    case MHFD_ERR_INVALID_ARGUMENT: return "MHFD_ERR_INVALID_ARGUMENT";
+    case MHFD_ERR_SHAPE: return "MHFD_ERR_SHAPE";
+    case MHFD_ERR_CAPACITY: return "MHFD_ERR_CAPACITY";
+    case MHFD_ERR_WORKSPACE: return "MHFD_ERR_WORKSPACE";
+    case MHFD_ERR_CUDA: return "MHFD_ERR_CUDA";
+    case MHFD_ERR_DEVICE: return "MHFD_ERR_DEVICE";
+  }
+  return "MHFD_ERR_UNKNOWN";
+}
+
+void mhfd_params_default(mhfd_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof(*p));
+  p->struct_size = sizeof(mhfd_params);
+  p->min_sigma = 1.0f;
+  p->max_sigma = 10.0f;
+  p->num_scales = 10;
+  p->threshold = 0.09f;  // 0.1 * dt for the paper-like grid (reading R11)
+  p->overlap = 0.5f;
+  p->sat_low = 0.00175f;
+  p->sat_high = 0.00175f;
+  p->nms = MHFD_NMS_PAPER;
+  p->strict = 0;
+  p->device = 0;
+  p->max_candidates = 0;
+}
+
+mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
+  g_err.clear();
+  if (!p || !out) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (p->struct_size < sizeof(mhfd_params)) return fail(MHFD_ERR_INVALID_ARGUMENT, "struct_size %u", p->struct_size);
+  if (!(std::isfinite(p->min_sigma) && p->min_sigma > 0.f))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "min_sigma must be > 0 (NonPositiveScale)");
+  if (!(std::isfinite(p->max_sigma) && p->max_sigma > p->min_sigma))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "max_sigma must be > min_sigma");
+  if (p->num_scales < 1 || p->num_scales > kMaxLevels - 2)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "num_scales %d not in [1, %d] (InsufficientLevels)", p->num_scales,
+                kMaxLevels - 2);
+  if (!(std::isfinite(p->threshold) && p->threshold >= 0.f))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "threshold must be finite and >= 0");
+  if (!(p->overlap >= 0.f && p->overlap <= 1.f)) return fail(MHFD_ERR_INVALID_ARGUMENT, "overlap not in [0,1]");
+  if (!(p->sat_low >= 0.f && p->sat_low < 0.5f && p->sat_high >= 0.f && p->sat_high < 0.5f))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "sat_low/sat_high not in [0, 0.5)");
+  if (p->nms != MHFD_NMS_PAPER && p->nms != MHFD_NMS_26) return fail(MHFD_ERR_INVALID_ARGUMENT, "nms %d", p->nms);
+  if (p->strict != 0 && p->strict != 1) return fail(MHFD_ERR_INVALID_ARGUMENT, "strict %d", p->strict);
+  if (p->max_candidates < 0) return fail(MHFD_ERR_INVALID_ARGUMENT, "max_candidates < 0");
+  const int n = p->num_scales;
+  // scale grid in f64
+  double t[kMaxLevels];
+  const double dt = ((double)p->max_sigma - (double)p->min_sigma) / n;
+  int R[kMaxLevels];
+  int rmax = 0;
+  for (int i = 0; i <= n; ++i) {
+    t[i] = (double)p->min_sigma + i * dt;
+    R[i] = (int)std::ceil(5.0 * t[i]);
+    rmax = std::max(rmax, R[i]);
+  }
+  if (rmax > kMaxRadius) return fail(MHFD_ERR_INVALID_ARGUMENT, "ceil(5*max_sigma) = %d > %d", rmax, kMaxRadius);
+  if (p->width < 2 * rmax + 1 || p->height < 2 * rmax + 1 || p->width > 65535 || p->height > 65535)
+    return fail(MHFD_ERR_SHAPE, "width/height %dx%d: need 2*ceil(5*max_sigma)+1 = %d <= W,H <= 65535", p->width,
+                p->height, 2 * rmax + 1);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(MHFD_ERR_DEVICE, "no CUDA device");
+  }
+  if (p->device < 0 || p->device >= ndev) return fail(MHFD_ERR_DEVICE, "device %d of %d", p->device, ndev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, p->device) != cudaSuccess) return fail(MHFD_ERR_DEVICE, "device properties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(MHFD_ERR_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a (B200)", p->device,
+                prop.major, prop.minor);
+
+  mhfd_ctx* c = new (std::nothrow) mhfd_ctx;
+  if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "out of host memory");
+  memset(c, 0, sizeof(*c));
+  c->tab = new (std::nothrow) LevelTable;
+  if (!c->tab) { delete c; return fail(MHFD_ERR_INVALID_ARGUMENT, "out of host memory"); }
+  memset(c->tab, 0, sizeof(LevelTable));
+  c->p = *p;
+  c->p.struct_size = sizeof(mhfd_params);
+  c->n = n;
+  c->dt = dt;
+  c->sms = prop.multiProcessorCount;
+  LevelTable& T = *c->tab;
+  T.nlev = n + 1;
+  T.rmax = rmax;
+  int off = 0;
+  for (int i = 0; i <= n; ++i) {
+    const int pre = (4 - R[i] % 4) % 4;
+    const int ntap = ((pre + 2 * R[i] + 1) + kTapUnroll - 1) / kTapUnroll * kTapUnroll;
+    if (off + ntap > kMaxTaps) {
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_INVALID_ARGUMENT, "tap table exceeds %d floats", kMaxTaps);
+    }
+    // sampled Gaussian exp(-d^2/2t^2) (sigma = t), renormalised in f64, rounded once
+    double sum = 0.0;
+    for (int d = -R[i]; d <= R[i]; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
+    for (int d = -R[i]; d <= R[i]; ++d)
+      T.w[off + pre + d + R[i]] = (float)(std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum);
+    T.R[i] = R[i];
+    T.pre[i] = pre;
+    T.ntap[i] = ntap;
+    T.woff[i] = off;
+    T.tdog[i] = (float)t[i];
+    off += ntap;
+    c->t[i] = t[i];
+  }
+  T.ntaps_total = off;
+  c->radmax = 0.0;
+  for (int s = 0; s < n; ++s) {
+    c->rad[s] = std::sqrt(2.0) * t[s];
+    c->radmax = std::max(c->radmax, c->rad[s]);
+  }
+  const int64_t half = (int64_t)((p->width + 1) / 2) * ((p->height + 1) / 2);
+  c->cap = p->max_candidates > 0 ? p->max_candidates : (p->nms == MHFD_NMS_PAPER ? half : half * n);
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_prune, 256, 0) != cudaSuccess || bps < 1) {
+    mhfd_destroy(c);
+    return fail(MHFD_ERR_CUDA, "occupancy query for k_prune failed");
+  }
+  c->prune_grid = bps * c->sms;
+  *out = c;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_timing_enable(mhfd_ctx* c, int32_t max_calls) {
+  if (!c || max_calls < 0) return fail(MHFD_ERR_INVALID_ARGUMENT, "bad argument");
+  if (c->tev) {
+    for (int i = 0; i < 5 * c->tmax; ++i) cudaEventDestroy(c->tev[i]);
+    delete[] c->tev;
+    c->tev = nullptr;
+  }
+  c->tmax = c->tcount = 0;
+  if (max_calls == 0) return MHFD_OK;
+  c->tev = new (std::nothrow) cudaEvent_t[5 * (size_t)max_calls];
+  if (!c->tev) return fail(MHFD_ERR_INVALID_ARGUMENT, "out of host memory");
+  for (int i = 0; i < 5 * max_calls; ++i) {
+    cudaError_t e = cudaEventCreate(&c->tev[i]);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaEventDestroy(c->tev[j]);
+      delete[] c->tev;
+      c->tev = nullptr;
+      return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  c->tmax = max_calls;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_timing_read(mhfd_ctx* c, float* ms, int32_t* ncalls) {
+  if (!c || !ms || !ncalls) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
+  *ncalls = 0;
+  for (int k = 0; k < c->tcount; ++k) {
+    cudaEvent_t* ev = c->tev + 5 * k;
+    cudaError_t e = cudaEventSynchronize(ev[4]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    for (int st = 0; st < 4; ++st) {
+      e = cudaEventElapsedTime(&ms[4 * k + st], ev[st], ev[st + 1]);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+    }
+  }
+  *ncalls = c->tcount;
+  return MHFD_OK;
+}
+
+void mhfd_destroy(mhfd_ctx* c) {
+  if (!c) return;
+  if (c->tev) {
+    for (int i = 0; i < 5 * c->tmax; ++i) cudaEventDestroy(c->tev[i]);
+    delete[] c->tev;
+  }
+  if (c->copy_stream) {
+    cudaStreamDestroy(c->copy_stream);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
+  }
+  delete c->tab;
+  delete c;
+}
+
+mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dtype, int32_t batch,
+                                  int64_t pitch_bytes, void* d_staging, size_t staging_bytes, void* d_workspace,
+                                  size_t workspace_bytes, double* h_scores, int32_t* h_counts, void* stream) {
+  g_err.clear();
+  if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!h_images || !h_scores || !d_staging) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (batch < 1) return fail(MHFD_ERR_SHAPE, "batch %d < 1", batch);
+  const size_t img_bytes = (size_t)c->p.height * (size_t)pitch_bytes;
+  const int chunk = (int)std::min<size_t>(staging_bytes / (2 * img_bytes), (size_t)batch);
+  if (chunk < 1) return fail(MHFD_ERR_WORKSPACE, "staging holds < 1 image per half");
+  if (((uintptr_t)d_staging) % 256 != 0) return fail(MHFD_ERR_WORKSPACE, "staging not 256-byte aligned");
+  mhfd_status s = check_call(c, d_staging, dtype, chunk, pitch_bytes, d_workspace, workspace_bytes);
+  if (s != MHFD_OK) return s;
+  cudaError_t e = cudaSuccess;
+  if (!c->copy_stream) {
+    e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&c->ev_ready[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "host-path stream/events");
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  const Layout L = layout(c, chunk);
+  double* d_sc = reinterpret_cast<double*>(ws + L.scores);
+  int32_t* d_ct = reinterpret_cast<int32_t*>(ws + L.counts);
+  // the copy stream must not overwrite staging the caller's stream may still read
+  e = cudaEventRecord(c->ev_free[0], st);
+  if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[1], st);
+  if (e != cudaSuccess) return cuda_fail(e, "event record");
+  int launches = 0;
+  for (int b0 = 0, k = 0; b0 < batch; b0 += chunk, ++k) {
+    const int nb = std::min(chunk, batch - b0);
+    const int h = k & 1;
+    char* dst = static_cast<char*>(d_staging) + (size_t)h * chunk * img_bytes;
+    e = cudaStreamWaitEvent(c->copy_stream, c->ev_free[h], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dst, static_cast<const char*>(h_images) + (size_t)b0 * img_bytes, (size_t)nb * img_bytes,
+                          cudaMemcpyHostToDevice, c->copy_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_ready[h], c->copy_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c->ev_ready[h], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "host-path copy");
+    cudaEvent_t* ev = next_timing(c);
+    s = run_front(c, dst, dtype, nb, pitch_bytes, ws, L, nullptr, st, launches, ev);
+    if (s != MHFD_OK) return s;
+    s = run_prune(c, nb, ws, L, nullptr, 0, d_ct, d_sc, nullptr, st, launches, ev);
+    if (s != MHFD_OK) return s;
+    e = cudaEventRecord(c->ev_free[h], st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_scores + b0, d_sc, sizeof(double) * nb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && h_counts)
+      e = cudaMemcpyAsync(h_counts + b0, d_ct, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "host-path readback");
+  }
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out) {
+  if (!c || !out) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = c->p;
+  out->max_candidates = (int32_t)c->cap;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_workspace_bytes(const mhfd_ctx* c, int32_t batch, size_t* bytes) {
+  if (!c || !bytes) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (batch < 1) return fail(MHFD_ERR_SHAPE, "batch %d < 1", batch);
+  *bytes = layout(c, batch).total;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_detect_batch(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch, int64_t pitch_bytes,
+                              void* d_workspace, size_t workspace_bytes, mhfd_blob* d_blobs, int32_t blob_capacity,
+                              int32_t* d_counts, int32_t* d_flags, void* stream) {
+  g_err.clear();
+  mhfd_status s = check_call(c, d_images, dtype, batch, pitch_bytes, d_workspace, workspace_bytes);
+  if (s != MHFD_OK) return s;
+  if (blob_capacity < 0) return fail(MHFD_ERR_CAPACITY, "blob_capacity < 0");
+  if (!d_counts) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_counts is NULL");
+  if (!d_blobs && blob_capacity > 0) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_blobs is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  const Layout L = layout(c, batch);
+  int launches = 0;
+  cudaEvent_t* ev = next_timing(c);
+  s = run_front(c, d_images, dtype, batch, pitch_bytes, ws, L, nullptr, st, launches, ev);
+  if (s != MHFD_OK) return s;
+  s = run_prune(c, batch, ws, L, d_blobs ? d_blobs : nullptr, blob_capacity, d_counts, nullptr, d_flags, st,
+                launches, ev);
+  if (s != MHFD_OK) return s;
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_focus_score(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch, int64_t pitch_bytes,
+                             void* d_workspace, size_t workspace_bytes, double* d_scores, int32_t* d_counts,
+                             void* stream) {
+  g_err.clear();
+  mhfd_status s = check_call(c, d_images, dtype, batch, pitch_bytes, d_workspace, workspace_bytes);
+  if (s != MHFD_OK) return s;
+  if (!d_scores) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_scores is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  const Layout L = layout(c, batch);
+  int launches = 0;
+  cudaEvent_t* ev = next_timing(c);
+  s = run_front(c, d_images, dtype, batch, pitch_bytes, ws, L, nullptr, st, launches, ev);
+  if (s != MHFD_OK) return s;
+  s = run_prune(c, batch, ws, L, nullptr, 0, d_counts, d_scores, nullptr, st, launches, ev);
+  if (s != MHFD_OK) return s;
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_debug_dump(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t batch, int64_t pitch_bytes,
+                            void* d_workspace, size_t workspace_bytes, int32_t* d_lohi, float* d_dog, float* d_v,
+                            uint8_t* d_idx, mhfd_blob* d_cands, int32_t* d_ncand, void* stream) {
+  g_err.clear();
+  mhfd_status s = check_call(c, d_images, dtype, batch, pitch_bytes, d_workspace, workspace_bytes);
+  if (s != MHFD_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  const Layout L = layout(c, batch);
+  int launches = 0;
+  s = run_front(c, d_images, dtype, batch, pitch_bytes, ws, L, d_dog, st, launches, nullptr);
+  if (s != MHFD_OK) return s;
+  const int64_t plane = (int64_t)c->p.width * c->p.height;
+  cudaError_t e = cudaSuccess;
+  if (d_lohi) {
+    k_copy_lohi<<<(batch + 127) / 128, 128, 0, st>>>(reinterpret_cast<const ImgPar*>(ws + L.par), d_lohi, batch);
+    e = cudaGetLastError();
+    ++launches;
+  }
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  if (e == cudaSuccess && d_v && paper)
+    e = cudaMemcpyAsync(d_v, ws + L.v, sizeof(float) * plane * batch, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && d_idx && paper)
+    e = cudaMemcpyAsync(d_idx, ws + L.idx, plane * batch, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && d_cands)
+    e = cudaMemcpyAsync(d_cands, ws + L.cand, sizeof(mhfd_blob) * c->cap * batch, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && d_ncand)
+    e = cudaMemcpyAsync(d_ncand, ws + L.ncand, sizeof(int32_t) * batch, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "debug copies");
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+"""CUDA path vs oracle, element by element, through the C ABI.
+
+Sizes: C1 (256^2, sigma 1-5, n 5) and C2 (1024^2, sigma 1-10, n 10) in full;
+ragged shapes, u16, the minimum image size, degenerate images and every ABI option;
+C3/C4-size images (4096^2, the launch configuration bench.py times) on sampled
+pixels the oracle evaluates one by one, plus properties.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import parity as P
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # the gpu marker is deselected on CPU runs
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2108_12050_b200 as mhfd  # noqa: E402
+
+C1 = dict(min_sigma=1.0, max_sigma=5.0, num_scales=5)
+C3 = dict(min_sigma=1.0, max_sigma=10.0, num_scales=10)
+
+
+def _tau(cfg):
+    return 0.1 * (cfg["max_sigma"] - cfg["min_sigma"]) / cfg["num_scales"]
+
+
+def _to_t(img):
+    t = torch.from_numpy(np.ascontiguousarray(img))
+    return t
+
+
+def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None):
+    """Full comparison on one image: percentiles, DoG stack, v/argmax, candidates,
+    pruned blobs, counts and score."""
+    H, W = img.shape
+    tau = _tau(cfg) if tau is None else tau
+    n = cfg["num_scales"]
+    det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, **cfg)
+    dump = det.debug_dump(_to_t(img))
+    ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True)
+    # a1: percentiles, exact integers
+    lo, hi = dump["lohi"][0].tolist()
+    assert (lo, hi) == (ref["lo"], ref["hi"])
+    # a2-a5: responses within 1e-4 of the peak
+    D = ref["D"]
+    Pk = float(D.max())
+    eps = P.REL_EPS * max(Pk, 1e-30)
+    Dg = dump["dog"][0].cpu().numpy().astype(np.float64)
+    err = float(np.abs(Dg - D).max())
+    assert err <= eps, f"max |DoG_gpu - DoG_oracle| = {err:.3e} > eps = {eps:.3e} (P = {Pk:.4f})"
+    # a6: inner argmax
+    tie = P.scale_tie(D, eps)
+    if nms == "paper":
+        vg = dump["v"][0].cpu().numpy().astype(np.float64)
+        assert float(np.abs(vg - ref["v"]).max()) <= eps
+        ig = dump["idx"][0].cpu().numpy()
+        assert np.array_equal(ig[~tie], ref["idx"][~tie])
+        amb = P.ambiguous_paper(ref["v"], tau, eps)
+        amb_xy = {(int(x), int(y)) for y, x in zip(*np.nonzero(amb))}
+        ora_c = P.oracle_rows(oracle.nms_paper(D, tau, strict))
+    else:
+        amb = P.ambiguous_26(D, tau, eps)
+        amb_xy = {(int(x), int(y), int(i)) for i, y, x in zip(*np.nonzero(amb))}
+        ora_c = P.oracle_rows(oracle.nms_26(D, tau, strict))
+    tie_xy = {(int(x), int(y)) for y, x in zip(*np.nonzero(tie))}
+    # a7-a8: candidates (ordered list)
+    nc = int(dump["ncand"][0])
+    gpu_c = P.gpu_rows(dump["cands"][0], min(nc, det.max_candidates))
+    assert gpu_c == sorted(gpu_c, key=lambda r: (r[1], r[0], r[2])), "candidate list not in (y, x, scale) order"
+    summ = P.compare_candidates(gpu_c, ora_c, amb_xy, tie_xy, eps, nms)
+    # a9-a10: pruned blobs, counts, score
+    blobs, cnt, flags = det.detect(_to_t(img))
+    scores = det.focus_score(_to_t(img))
+    torch.cuda.synchronize()
+    count = int(cnt[0])
+    assert int(flags[0]) == 0
+    assert float(scores[0]) == float(count)
+    gpu_k = P.gpu_rows(blobs[0], count)
+    assert gpu_k == sorted(gpu_k, key=lambda r: (r[1], r[0], r[2]))
+    ora_k = P.oracle_rows(ref["blobs"])
+    amb_pts = [(x, y) for (x, y, *_) in ([(k[0], k[1]) for k in amb_xy])]
+    rad = P.radii(cfg["min_sigma"], cfg["max_sigma"], n)
+    P.compare_pruned(gpu_k, ora_k, amb_pts, max(rad), rad, nms)
+    P.assert_score(count, ref["count"])
+    summ.update(count_gpu=count, count_oracle=ref["count"], dog_err_rel=err / max(Pk, 1e-30))
+    return summ
+
+
+@pytest.fixture(scope="module")
+def c1_img():
+    return synth.em_tile_np(256, 256, 1000, dose=300.0, bits=8)
+
+
+@pytest.mark.parametrize("nms", ["paper", "26"])
+@pytest.mark.parametrize("overlap", [0.5, 1.0, 0.0])
+def test_c1_full_parity(c1_img, nms, overlap):
+    s = _full_parity(c1_img, C1, nms=nms, overlap=overlap)
+    assert s["n_oracle"] > 100
+
+
+@pytest.mark.parametrize("strict", [True])
+def test_c1_strict(c1_img, strict):
+    _full_parity(c1_img, C1, strict=strict)
+
+
+@pytest.mark.parametrize("defocus", [0.0, 2.0])
+@pytest.mark.parametrize("bits", [8, 16])
+def test_c2_pair_parity(defocus, bits):
+    img = synth.em_tile_np(1024, 1024, 1000, defocus=defocus, dose=300.0, bits=bits)
+    _full_parity(img, C3)
+
+
+def test_c2_sharp_beats_defocused():
+    imgs = np.stack([synth.em_tile_np(1024, 1024, 1000, defocus=s, dose=300.0) for s in (0.0, 2.0)])
+    det = mhfd.Detector(1024, 1024, threshold=0.09, **C3)
+    sc = det.focus_score(torch.from_numpy(imgs)).cpu().tolist()
+    assert sc[0] > sc[1] > 0
+
+
+@pytest.mark.parametrize("shape,bits", [((257, 300), 8), ((300, 257), 16), ((51, 51), 8), ((77, 130), 16)])
+def test_ragged_and_minimum_shapes(shape, bits):
+    H, W = shape
+    img = synth.em_tile_np(H, W, 42, dose=300.0, bits=bits)
+    _full_parity(img, C1)
+
+
+def test_degenerate_and_constant():
+    img = synth.constant_image(128, 96, 200)
+    det = mhfd.Detector(96, 128, threshold=0.08, **C1)
+    blobs, cnt, flags = det.detect(_to_t(img))
+    assert int(cnt[0]) == 0
+    d = det.debug_dump(_to_t(img))
+    assert d["lohi"][0].tolist() == [200, 200]
+    assert float(d["dog"].abs().max()) == 0.0
+
+
+def test_batch_invariance_and_determinism():
+    imgs = np.stack([synth.em_tile_np(256, 320, 1000 + b, dose=300.0) for b in range(5)])
+    imgs[3] = 77  # a degenerate image inside the batch
+    det = mhfd.Detector(320, 256, threshold=0.08, **C1)
+    b_all, c_all, _ = det.detect(torch.from_numpy(imgs))
+    b_again, c_again, _ = det.detect(torch.from_numpy(imgs))
+    assert torch.equal(c_all, c_again)
+    for b in range(5):
+        k = int(c_all[b])
+        assert torch.equal(b_all[b, :k], b_again[b, :k])
+    for b in range(5):
+        b1, c1, _ = det.detect(torch.from_numpy(imgs[b:b + 1]))
+        assert int(c1[0]) == int(c_all[b])
+        k = int(c1[0])
+        assert torch.equal(b1[0, :k], b_all[b, :k])
+    assert int(c_all[3]) == 0
+
+
+def test_capacity_truncation_and_flags(c1_img):
+    det = mhfd.Detector(256, 256, threshold=0.08, **C1)
+    full, cnt, fl = det.detect(_to_t(c1_img))
+    k = int(cnt[0])
+    small, cnt2, fl2 = det.detect(_to_t(c1_img), blob_capacity=17)
+    assert int(cnt2[0]) == k and int(fl2[0]) == 2 and int(fl[0]) == 0
+    assert torch.equal(small[0, :17], full[0, :17])
+    det2 = mhfd.Detector(256, 256, threshold=0.08, max_candidates=50, **C1)
+    _, cnt3, fl3 = det2.detect(_to_t(c1_img))
+    assert int(fl3[0]) & 1
+
+
+def test_isolated_disk_gpu():
+    img = synth.disk_image(112, 112, 56.5, 56.5, 6.0, contrast=0.6, bits=16)
+    det = mhfd.Detector(112, 112, threshold=0.09, **C3)
+    blobs, cnt, _ = det.detect(_to_t(img))
+    rows = P.gpu_rows(blobs[0], int(cnt[0]))
+    ref = oracle.detect(img, 1.0, 10.0, 10, 0.09, 0.5)
+    assert [(r[0], r[1], r[2]) for r in rows] == [(56, 56, int(ref["blobs"][0]["scale"]))]
+
+
+def test_abi_errors_on_gpu():
+    det = mhfd.Detector(256, 256, **C1)
+    bad = torch.zeros((1, 255, 256), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        det.focus_score(bad)
+    with pytest.raises(mhfd.MHFDError):
+        mhfd.Detector(40, 40, **C1)   # smaller than 2*ceil(5*max_sigma)+1
+
+
+# ------------------------------------------------------------------ full size (4096^2)
+@pytest.fixture(scope="module")
+def c3_batch():
+    # generated on the GPU (fast); the oracle gets the same bytes
+    imgs = [synth.em_tile(4096, 4096, 1000 + b, defocus=0.5 * b, dose=300.0, device="cuda") for b in range(3)]
+    return torch.stack(imgs)
+
+
+def test_c3_sampled_pixels_and_properties(c3_batch):
+    """Bench launch configuration (4096^2, sigma 1-10, n 10): sampled responses vs the
+    oracle's per-pixel 2-D definition, Eq. 3 decisions at those pixels, properties."""
+    B = c3_batch.shape[0]
+    det = mhfd.Detector(4096, 4096, threshold=0.09, **C3)
+    dump = det.debug_dump(c3_batch, dog=False, cands=True)
+    blobs, cnt, flags = det.detect(c3_batch)
+    scores = det.focus_score(c3_batch)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    for b in range(B):
+        img = c3_batch[b].cpu().numpy()
+        lo, hi = oracle.percentiles(img)
+        assert dump["lohi"][b].tolist() == [lo, hi]
+        f = oracle.stretch(img, lo, hi)
+        v = dump["v"][b].cpu().numpy()
+        idx = dump["idx"][b].cpu().numpy()
+        pts = [(int(y), int(x)) for y, x in rng.integers(0, 4096, size=(12, 2))]
+        pts += [(0, 0), (4095, 4095), (0, 4095), (2048, 31), (2048, 32)]
+        peak = 0.0
+        vals = {}
+        for (y, x) in pts:
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    yy, xx = (y + dy) % 4096, (x + dx) % 4096
+                    if (yy, xx) not in vals:
+                        vals[(yy, xx)] = oracle.dog_at(f, 1.0, 10.0, 10, yy, xx)
+                        peak = max(peak, float(vals[(yy, xx)].max()))
+        eps = P.REL_EPS * max(peak, 0.05)
+        for (yy, xx), Dv in vals.items():
+            assert abs(float(v[yy, xx]) - Dv.max()) <= eps
+            s = np.sort(Dv)
+            if s[-1] - s[-2] > eps:
+                assert int(idx[yy, xx]) == int(np.argmax(Dv))
+        # Eq. 3 decision at the sampled interior pixels
+        cand_set = {(r[0], r[1]) for r in P.gpu_rows(dump["cands"][b], min(int(dump["ncand"][b]), det.max_candidates))}
+        for (y, x) in pts:
+            if not (1 <= y < 4095 and 1 <= x < 4095):
+                continue
+            c = vals[(y, x)].max()
+            m = max(vals[((y + dy) % 4096, (x + dx) % 4096)].max() for dy in (-1, 0, 1) for dx in (-1, 0, 1)
+                    if dy or dx)
+            if abs(c - m) > eps and abs(c - 0.09) > eps:
+                assert ((x, y) in cand_set) == (c >= m and c > 0.09)
+        # properties of the outputs
+        k = int(cnt[b])
+        assert float(scores[b]) == float(k) and int(flags[b]) == 0 and k > 0
+        rows = P.gpu_rows(blobs[b], k)
+        assert rows == sorted(rows, key=lambda r: (r[1], r[0], r[2]))
+        assert all(r[3] > 0.09 for r in rows)
+    sc = scores.cpu().tolist()
+    assert sc[0] > sc[1] > sc[2], sc   # defocus 0, 0.5, 1.0 px
