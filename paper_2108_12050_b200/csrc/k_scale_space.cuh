@@ -47,10 +47,10 @@ __host__ __device__ inline int hbuf_rows(int rmax, int BH) { return BH + 2 * rma
 // hbuf floats, rounded to 32 so the tap table and mbarriers after it stay 128-byte aligned
 __host__ __device__ inline int hbuf_floats(int rmax, int BH) { return (hbuf_rows(rmax, BH) * kHP + 31) & ~31; }
 __host__ __device__ inline int wtab_floats(int ntaps_total) { return (ntaps_total + 31) & ~31; }
-// layout: [stage: kStages x 32 x SP][hbuf][weights][mbarriers]
+// layout: [stage: kStages x 32 x SP][hbuf][weights wA][weights wB][mbarriers]
 __host__ __device__ inline size_t scale_space_smem(int rmax, int BH, int ntaps_total) {
   return sizeof(float) * ((size_t)kStages * kChunkRows * stage_pitch(rmax) + 64 + (size_t)hbuf_floats(rmax, BH) +
-                          wtab_floats(ntaps_total)) +
+                          2 * wtab_floats(ntaps_total)) +
          8 * kStages;
 }
 // 2-D TMA boxes hold SP <= 256 columns
@@ -146,67 +146,102 @@ __global__ void __launch_bounds__(256) k_normalize_vec(const uint8_t* __restrict
 }
 
 // ---------------------------------------------------------------------------------
-// acc[o] += sum_{jj<4} w[jj] * x[o+jj], o = 0..3, window x = a ++ b
-__device__ __forceinline__ void tap4(float (&acc)[4], const float4& a, const float4& b, const float* w) {
-  const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const float wj = w[jj];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) acc[o] = fmaf(wj, x[o + jj], acc[o]);
-  }
-}
+// Packed FFMA2 convolutions.  A 1-D convolution out[o] = sum_t w[t] x[o+t] is computed
+// with tap pairs: FFMA2 multiplies an input pair (x[2m], x[2m+1]) by a weight pair and
+// accumulates into (acc.x, acc.y), out[o] = acc.x + acc.y.  Even outputs use the pairs
+// (w[2k], w[2k+1]) (table wA = w), odd outputs the pairs (w[2k-1], w[2k]) (table wB[i] =
+// w[i-1]); both then meet 2-aligned input pairs, so every operand is an aligned register
+// pair and no shuffling is needed.  Odd outputs need one extra pair k = ntap/2 whose
+// second weight w[ntap] is the zero padding after each level's taps.
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
 
-// row pass: out[o] = sum_{t<ntap} w[t] * src[o+t], o = 0..3; src 16-byte aligned, ntap % 8 == 0
-__device__ __forceinline__ void conv4_row(float (&acc)[4], const float* __restrict__ src, const float* __restrict__ w,
-                                          int ntap) {
+// row pass: out[o] = sum_{t<ntap} w[t] src[o+t], o = 0..3; src 16-byte aligned, ntap % 8 == 0
+__device__ __forceinline__ void conv4_row(float (&out)[4], const float* __restrict__ src, const float* __restrict__ wA,
+                                          const float* __restrict__ wB, int ntap) {
+  float2 acc[4];
 #pragma unroll
-  for (int o = 0; o < 4; ++o) acc[o] = 0.f;
+  for (int o = 0; o < 4; ++o) acc[o] = make_float2(0.f, 0.f);
   const float4* s4 = reinterpret_cast<const float4*>(src);
-  float4 a = s4[0], b;
+  const float4* a4 = reinterpret_cast<const float4*>(wA);
+  const float4* b4 = reinterpret_cast<const float4*>(wB);
+  float4 xa = s4[0];
   for (int j = 0; j < ntap; j += 8) {
-    b = s4[(j >> 2) + 1];
-    tap4(acc, a, b, w + j);
-    a = s4[(j >> 2) + 2];
-    tap4(acc, b, a, w + j + 4);
+    const int q = j >> 2;
+    const float4 xb = s4[q + 1], xc = s4[q + 2];
+    const float4 A0 = a4[q], A1 = a4[q + 1], B0 = b4[q], B1 = b4[q + 1];
+    const float2 P[5] = {lo2(xa), hi2(xa), lo2(xb), hi2(xb), lo2(xc)};
+    const float2 WA[4] = {lo2(A0), hi2(A0), lo2(A1), hi2(A1)};
+    const float2 WB[4] = {lo2(B0), hi2(B0), lo2(B1), hi2(B1)};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      acc[0] = __ffma2_rn(P[kk], WA[kk], acc[0]);
+      acc[1] = __ffma2_rn(P[kk], WB[kk], acc[1]);
+      acc[2] = __ffma2_rn(P[kk + 1], WA[kk], acc[2]);
+      acc[3] = __ffma2_rn(P[kk + 1], WB[kk], acc[3]);
+    }
+    xa = xc;
   }
+  {  // odd outputs: tap pair (ntap-1, ntap)
+    const float2 wb = reinterpret_cast<const float2*>(wB)[ntap >> 1];
+    acc[1] = __ffma2_rn(lo2(xa), wb, acc[1]);
+    acc[3] = __ffma2_rn(hi2(xa), wb, acc[3]);
+  }
+#pragma unroll
+  for (int o = 0; o < 4; ++o) out[o] = acc[o].x + acc[o].y;
 }
 
-// acc[o] += sum_{jj<8} w[jj] * x[o+jj], o = 0..7, window x = a[0..7] ++ b[0..6]
-__device__ __forceinline__ void tap8(float (&acc)[8], const float (&a)[8], const float (&b)[8], const float* w) {
+// acc[2q], acc[2q+1] += pair (q + kk) x (wA, wB) pair kk, for the 8 outputs of the column pass
+__device__ __forceinline__ void col_group(float2 (&acc)[8], const float2 (&Pa)[4], const float2 (&Pb)[4],
+                                          const float* __restrict__ wA, const float* __restrict__ wB) {
 #pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    const float wj = w[jj];
+  for (int kk = 0; kk < 4; ++kk) {
+    const float2 wa = reinterpret_cast<const float2*>(wA)[kk];
+    const float2 wb = reinterpret_cast<const float2*>(wB)[kk];
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      const int k = o + jj;
-      acc[o] = fmaf(wj, k < 8 ? a[k] : b[k - 8], acc[o]);
+    for (int q = 0; q < 4; ++q) {
+      const int m = q + kk;
+      const float2 x = m < 4 ? Pa[m] : Pb[m - 4];
+      acc[2 * q] = __ffma2_rn(x, wa, acc[2 * q]);
+      acc[2 * q + 1] = __ffma2_rn(x, wb, acc[2 * q + 1]);
     }
   }
 }
 
-// column pass: out[o] = sum_{t<ntap} w[t] * src[(o+t)*stride], o = 0..7, ntap % 8 == 0
-__device__ __forceinline__ void conv8_col(float (&acc)[8], const float* __restrict__ src, int stride,
-                                          const float* __restrict__ w, int ntap) {
+__device__ __forceinline__ void load_pairs(float2 (&P)[4], const float* __restrict__ src, int stride, int m0) {
 #pragma unroll
-  for (int o = 0; o < 8; ++o) acc[o] = 0.f;
-  float xa[8], xb[8];
+  for (int k = 0; k < 4; ++k)
+    P[k] = make_float2(src[(2 * (m0 + k)) * stride], src[(2 * (m0 + k) + 1) * stride]);
+}
+
+// column pass: out[o] = sum_{t<ntap} w[t] src[(o+t)*stride], o = 0..7, ntap % 8 == 0
+__device__ __forceinline__ void conv8_col(float (&out)[8], const float* __restrict__ src, int stride,
+                                          const float* __restrict__ wA, const float* __restrict__ wB, int ntap) {
+  float2 acc[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) xa[k] = src[k * stride];
-  int j0 = 0;
-  for (; j0 + 16 <= ntap; j0 += 16) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) xb[k] = src[(j0 + 8 + k) * stride];
-    tap8(acc, xa, xb, w + j0);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) xa[k] = src[(j0 + 16 + k) * stride];
-    tap8(acc, xb, xa, w + j0 + 8);
+  for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.f, 0.f);
+  float2 Pa[4], Pb[4];
+  load_pairs(Pa, src, stride, 0);
+  int j = 0;
+  for (; j + 16 <= ntap; j += 16) {
+    load_pairs(Pb, src, stride, (j >> 1) + 4);
+    col_group(acc, Pa, Pb, wA + j, wB + j);
+    load_pairs(Pa, src, stride, (j >> 1) + 8);
+    col_group(acc, Pb, Pa, wA + j + 8, wB + j + 8);
   }
-  if (j0 < ntap) {  // ntap % 16 == 8: one more group
+  if (j < ntap) {  // ntap % 16 == 8
+    load_pairs(Pb, src, stride, (j >> 1) + 4);
+    col_group(acc, Pa, Pb, wA + j, wB + j);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) xb[k] = src[(j0 + 8 + k) * stride];
-    tap8(acc, xa, xb, w + j0);
+    for (int k = 0; k < 4; ++k) Pa[k] = Pb[k];
   }
+  {  // odd outputs: tap pair (ntap-1, ntap), input pairs ntap/2 + q (now in Pa)
+    const float2 wb = reinterpret_cast<const float2*>(wB)[ntap >> 1];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[2 * q + 1] = __ffma2_rn(Pa[q], wb, acc[2 * q + 1]);
+  }
+#pragma unroll
+  for (int o = 0; o < 8; ++o) out[o] = acc[o].x + acc[o].y;
 }
 
 // Stage rows [r0, r0 + nrow) of a level's row-pass input (image rows Y0-R-p+r, columns
@@ -269,7 +304,8 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
   float* stage = smem;                                         // kStages x kChunkRows x SP
   float* hbuf = smem + kStages * kChunkRows * SP + 64;         // hbuf_rows x kHP
   float* wsm = hbuf + hbuf_floats(rmax, BH);                   // tap table
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + wtab_floats(tab.ntaps_total));
+  float* wsmB = wsm + wtab_floats(tab.ntaps_total);            // shifted tap table w[i-1]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wsmB + wtab_floats(tab.ntaps_total));
 
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * kStripW;
@@ -298,6 +334,9 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
   const int nzero = kStages * kChunkRows * SP + 64 + hbuf_floats(rmax, BH);
   for (int i = threadIdx.x; i < nzero; i += kThreads) smem[i] = 0.f;
   for (int i = threadIdx.x; i < tab.ntaps_total; i += kThreads) wsm[i] = tab.w[i];
+  for (int l = 0; l < tab.nlev; ++l)  // wB = each level's taps shifted right by one (zero in front)
+    for (int i = threadIdx.x; i < tab.ntap[l] + 8; i += kThreads)
+      wsmB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -335,6 +374,7 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
   for (int lev = 0; lev < nlev; ++lev) {
     const int ntap = tab.ntap[lev];
     const float* w = wsm + tab.woff[lev];
+    const float* wB = wsmB + tab.woff[lev];
     const int nrow = rows_of(tab.R[lev], tab.pre[lev]);   // hbuf rows: band rows -R-p .. BH+R-1
 
     // ---------------- row pass (chunks of 32 rows) ----------------
@@ -358,7 +398,7 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
       }
       const float* src = stage + buf * kChunkRows * SP + lane * SP + 4 * warp;
       float acc[4];
-      conv4_row(acc, src, w, ntap);
+      conv4_row(acc, src, w, wB, ntap);
       if (r0 + lane < nrow) {
         float* h = hbuf + (r0 + lane) * kHP + 4 * warp;
 #pragma unroll
@@ -374,7 +414,7 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
     for (int q = 0; q < RPT / 8; ++q) {
       const int rb = warp * RPT + q * 8;      // first band row of this group
       float acc[8];
-      conv8_col(acc, hbuf + rb * kHP + lane, kHP, w, ntap);
+      conv8_col(acc, hbuf + rb * kHP + lane, kHP, w, wB, ntap);
 #pragma unroll
       for (int o = 0; o < 8; ++o) {
         const int r = q * 8 + o;

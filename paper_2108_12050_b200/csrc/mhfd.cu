@@ -433,7 +433,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   for (int i = 0; i <= n; ++i) {
     const int pre = (4 - R[i] % 4) % 4;
     const int ntap = ((pre + 2 * R[i] + 1) + kTapUnroll - 1) / kTapUnroll * kTapUnroll;
-    if (off + ntap > kMaxTaps) {
+    if (off + ntap + 8 > kMaxTaps) {
       mhfd_destroy(c);
       return fail(MHFD_ERR_INVALID_ARGUMENT, "tap table exceeds %d floats", kMaxTaps);
     }
@@ -447,7 +447,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     T.ntap[i] = ntap;
     T.woff[i] = off;
     T.tdog[i] = (float)t[i];
-    off += ntap;
+    off += ntap + 8;   // >= 1 zero after the taps (the FFMA2 odd-output pair reads w[ntap])
     c->t[i] = t[i];
   }
   T.ntaps_total = off;
