@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -23,6 +24,7 @@
 #include "k_percentile.cuh"
 #include "k_prune.cuh"
 #include "k_scale_space.cuh"
+#include "k_band.cuh"
 
 using namespace mhfd;
 
@@ -37,6 +39,7 @@ struct mhfd_ctx {
   int64_t cap;       // candidates per image
   int prune_grid;    // cooperative grid size for k_prune
   int sms;
+  int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
   cudaEvent_t* tev;
   int tmax, tcount;
@@ -137,6 +140,27 @@ mhfd_status check_call(const mhfd_ctx* c, const void* d_images, int32_t dtype, i
   } while (0)
 
 // Everything up to the candidate list.  dog_dump (nullable) receives the DoG planes.
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+bool encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t cols, uint64_t rows,
+               uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)row_bytes};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaEvent_t* next_timing(mhfd_ctx* c) {
   if (!c->tev || c->tcount >= c->tmax) return nullptr;
   return c->tev + 5 * (c->tcount++);
@@ -149,6 +173,35 @@ cudaEvent_t* next_timing(mhfd_ctx* c) {
       if (em_ != cudaSuccess) return cuda_fail(em_, "event record"); \
     }                                                               \
   } while (0)
+
+mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L, float* v, uint8_t* idx,
+                    float* dog, cudaStream_t st, int& launches, cudaEvent_t* ev) {
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  // ---- a7-a8: NMS + threshold + ordered compaction
+  NmsArgs na{W, H, c->n, c->p.threshold, c->p.strict, v, idx, dog};
+  const int nseg = nseg_of(c);
+  int32_t* segcnt = reinterpret_cast<int32_t*>(ws + L.segcnt);
+  int32_t* segoff = reinterpret_cast<int32_t*>(ws + L.segoff);
+  int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
+  mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
+  dim3 gn((nseg + 7) / 8, B);
+  if (paper) {
+    k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
+  } else {
+    k_nms_count<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segcnt);
+  }
+  LAUNCH_CHECK("k_nms_count");
+  k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
+  LAUNCH_CHECK("k_seg_scan");
+  if (paper) {
+    k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
+  } else {
+    k_nms_write<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
+  }
+  LAUNCH_CHECK("k_nms_write");
+  MARK(3);
+  return MHFD_OK;
+}
 
 mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t B, int64_t pitch, char* ws,
                       const Layout& L, float* dog_dump, cudaStream_t st, int& launches, cudaEvent_t* ev) {
@@ -191,6 +244,26 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   }
 
   MARK(1);
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  float* v = reinterpret_cast<float*>(ws + L.v);
+  uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
+  // ---- a2-a6 on u8 images: band schedule (raw band staged once per CTA, no f32 prepass)
+  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
+      band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
+    const size_t smem = band_smem(c->tab->rmax, c->tab->ntaps_total);
+    cudaError_t ea = cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return cuda_fail(ea, "k_band attribute");
+    dim3 gb((W + kStripW - 1) / kStripW, (H + kBandBH - 1) / kBandBH, B);
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    const int use_tm = (pitch % 16 == 0) &&
+                       encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W, (uint64_t)H * B, (uint64_t)pitch,
+                                 (uint32_t)band_raw_w(c->tab->rmax), (uint32_t)kBandBoxRows);
+    k_band<<<gb, kBandThreads, smem, st>>>(img, s, par, *c->tab, tm, use_tm, v, idx);
+    LAUNCH_CHECK("k_band");
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
+  }
   // ---- a2: stretch on load -> centred f32 image
   float* fimg = reinterpret_cast<float*>(ws + L.fimg);
   {
@@ -208,9 +281,6 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     LAUNCH_CHECK("k_normalize");
   }
   // ---- a3-a6: fused blur + DoG + argmax
-  const bool paper = c->p.nms == MHFD_NMS_PAPER;
-  float* v = reinterpret_cast<float*>(ws + L.v);
-  uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
   float* dog = dog_dump ? dog_dump : reinterpret_cast<float*>(ws + L.dog);
   const bool write_dog = dog_dump != nullptr || !paper;
   const int strips = (W + kStripW - 1) / kStripW;
@@ -224,26 +294,9 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   int use_tmap = 0;
-  if (fast && tma_boxes(c->tab->rmax)) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-      cudaDriverEntryPointQueryResult q;
-      void* fn = nullptr;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-          q == cudaDriverEntryPointSuccess)
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    if (encode) {
-      const cuuint64_t gdim[2] = {(cuuint64_t)W, (cuuint64_t)H * (cuuint64_t)B};
-      const cuuint64_t gstride[1] = {(cuuint64_t)W * 4};
-      const cuuint32_t box[2] = {(cuuint32_t)stage_pitch(c->tab->rmax), (cuuint32_t)kChunkRows};
-      const cuuint32_t estr[2] = {1, 1};
-      CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, fimg, gdim, gstride, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      use_tmap = (r == CUDA_SUCCESS) ? 1 : 0;
-    }
-  }
+  if (fast && tma_boxes(c->tab->rmax))
+    use_tmap = encode_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, fimg, (uint64_t)W, (uint64_t)H * B, (uint64_t)W * 4,
+                         (uint32_t)stage_pitch(c->tab->rmax), (uint32_t)kChunkRows) ? 1 : 0;
   dim3 g3(strips, (H + BH - 1) / BH, B);
   const Shape sf{W, H, (int64_t)W * 4, 4};
   auto launch_ss = [&](auto kern) -> cudaError_t {
@@ -264,30 +317,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   ++launches;
   MARK(2);
 
-  // ---- a7-a8: NMS + threshold + ordered compaction
-  NmsArgs na{W, H, c->n, c->p.threshold, c->p.strict, v, idx, dog};
-  const int nseg = nseg_of(c);
-  int32_t* segcnt = reinterpret_cast<int32_t*>(ws + L.segcnt);
-  int32_t* segoff = reinterpret_cast<int32_t*>(ws + L.segoff);
-  int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
-  mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
-  dim3 gn((nseg + 7) / 8, B);
-  if (paper) {
-    k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
-  } else {
-    k_nms_count<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segcnt);
-  }
-  LAUNCH_CHECK("k_nms_count");
-  k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
-  LAUNCH_CHECK("k_seg_scan");
-  if (paper) {
-    k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
-  } else {
-    k_nms_write<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
-  }
-  LAUNCH_CHECK("k_nms_write");
-  MARK(3);
-  return MHFD_OK;
+  return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
 }
 
 mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_blob* blobs, int32_t blob_cap,
@@ -426,6 +456,10 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   c->n = n;
   c->dt = dt;
   c->sms = prop.multiProcessorCount;
+  {
+    const char* nb = getenv("MHFD_NO_BAND");
+    c->band_enabled = !(nb && nb[0] == '1');
+  }
   LevelTable& T = *c->tab;
   T.nlev = n + 1;
   T.rmax = rmax;
