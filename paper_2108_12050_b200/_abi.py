@@ -6,6 +6,7 @@ is no fallback: if ``libmhfd.so`` cannot be built or loaded, this raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 from . import _build
@@ -45,7 +46,8 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.build()
+        # MHFD_LIB: load an explicitly built variant (performance experiments only)
+        path = os.environ.get("MHFD_LIB") or _build.build()
         lib = ctypes.CDLL(path)
         P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
         sig = {

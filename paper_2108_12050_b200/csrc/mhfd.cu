@@ -253,13 +253,14 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     const size_t smem = band_smem(c->tab->rmax, c->tab->ntaps_total);
     cudaError_t ea = cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_band attribute");
-    dim3 gb((W + kStripW - 1) / kStripW, (H + kBandBH - 1) / kBandBH, B);
+    const int64_t ntiles = (int64_t)((W + kStripW - 1) / kStripW) * ((H + kBandBH - 1) / kBandBH) * B;
+    dim3 gb((unsigned)std::min<int64_t>(ntiles, c->sms));   // persistent: one CTA per SM
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     const int use_tm = (pitch % 16 == 0) &&
                        encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W, (uint64_t)H * B, (uint64_t)pitch,
                                  (uint32_t)band_raw_w(c->tab->rmax), (uint32_t)kBandBoxRows);
-    k_band<<<gb, kBandThreads, smem, st>>>(img, s, par, *c->tab, tm, use_tm, v, idx);
+    k_band<<<gb, kBandThreads, smem, st>>>(img, s, par, *c->tab, tm, use_tm, v, idx, B);
     LAUNCH_CHECK("k_band");
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
