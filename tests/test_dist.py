@@ -1,0 +1,73 @@
+"""Multi-process host logic of the image-sharded path, world_size 2 over gloo (CPU).
+
+Each rank scores its contiguous shard of a batch with the oracle (standing in for the
+per-GPU kernels, which need a B200), gathers (count, score) with the same
+`paper_2108_12050_b200.dist.gather_results` the bench uses over NCCL, and checks that
+the gathered vector equals the single-process result (GPU-count invariance,
+SPEC.md:339 analog) and that the shards partition the batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2108_12050_b200.dist import gather_results, shard
+
+
+def test_shard_partitions():
+    for n in (0, 1, 7, 64, 513):
+        for w in (1, 2, 3, 8):
+            parts = [shard(n, w, r) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [e - s for s, e in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, imgs, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    s, e = shard(len(imgs), world, rank)
+    counts = torch.tensor([oracle.detect(im, 1.0, 5.0, 5, 0.08, 0.5)["count"] for im in imgs[s:e]], dtype=torch.int32)
+    scores = counts.to(torch.float64)
+    g = gather_results(counts, scores)
+    if rank == 0:
+        q.put(g.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_world2_matches_single_process():
+    import oracle
+    import synth
+    imgs = [synth.em_tile_np(64, 64, 1000 + b, dose=300.0) for b in range(4)]
+    ref = np.array([oracle.detect(im, 1.0, 5.0, 5, 0.08, 0.5)["count"] for im in imgs], np.float64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, imgs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    g = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert g.shape == (2, 2, 2)
+    np.testing.assert_array_equal(g.reshape(-1, 2)[:, 0], ref)
+    np.testing.assert_array_equal(g.reshape(-1, 2)[:, 1], ref)
