@@ -39,7 +39,9 @@ struct PruneArgs {
   double radmax;
   double rad[kMaxLevels];   // sqrt(2) * t_s
   uint8_t* st;              // B x cap
-  int32_t* rowstart;        // B x (H + 1)
+  int32_t* rowstart;        // B x (H + 1): first candidate of each row
+  int32_t* rbi;             // B x H x (nbx + 1): first candidate of row y with x >= 32 k
+  int nbx;                  // ceil(W / 32)
   int64_t* img_off;         // B + 1: prefix of effective candidate counts
   int64_t* chunk_off;       // B + 1: prefix of chunk counts
   int32_t* chunk_cnt;       // kept per chunk
@@ -78,25 +80,20 @@ __device__ __forceinline__ int image_of(const int64_t* off, int B, int64_t g) {
 __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
   const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
   const uint8_t* st = a.st + (int64_t)b * a.cap;
-  const int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
   const mhfd_blob me = C[k];
   const double r = a.rad[me.scale];
   const int Dm = (int)ceil(r + a.radmax);
   bool blocked = false;
   const int ylo = max(0, me.y - Dm), yhi = min(a.H - 1, me.y + Dm);
+  const int kb0 = max(0, me.x - Dm) >> 5, kb1 = min(a.nbx, ((me.x + Dm) >> 5) + 1);
+  const int32_t* ri = a.rbi + (int64_t)b * a.H * (a.nbx + 1);
   for (int yy = ylo; yy <= yhi; ++yy) {
-    int lo = rs[yy];
-    const int hi = rs[yy + 1];
-    if (lo >= hi) continue;
-    int h2 = hi;  // lower_bound on x >= me.x - Dm
-    const int xmin = me.x - Dm;
-    while (lo < h2) {
-      const int mid = (lo + h2) >> 1;
-      if (C[mid].x < xmin) lo = mid + 1; else h2 = mid;
-    }
+    const int32_t* rrow = ri + (int64_t)yy * (a.nbx + 1);
+    const int lo = __ldcg(rrow + kb0), hi = __ldcg(rrow + kb1);
     for (int q = lo; q < hi; ++q) {
       const mhfd_blob o = C[q];
       if (o.x > me.x + Dm) break;
+      if (o.x < me.x - Dm) continue;
       if (q == k) continue;
       const bool higher = o.scale > me.scale ||
                           (o.scale == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
@@ -154,6 +151,25 @@ __global__ void __launch_bounds__(256) k_prune(PruneArgs a) {
   for (int64_t g = gtid; g < total; g += gsize) {
     const int b = image_of(a.img_off, a.B, g);
     a.st[(int64_t)b * a.cap + (g - a.img_off[b])] = a.prune ? kUndecided : kKept;
+  }
+  grid.sync();
+  // row-block index: first candidate of row y with x >= 32 k, k = 0 .. nbx
+  if (a.prune) {
+    const int64_t per_img = (int64_t)a.H * (a.nbx + 1);
+    for (int64_t g = gtid; g < (int64_t)a.B * per_img; g += gsize) {
+      const int b = (int)(g / per_img);
+      const int64_t rem = g - (int64_t)b * per_img;
+      const int y = (int)(rem / (a.nbx + 1));
+      const int kb = (int)(rem - (int64_t)y * (a.nbx + 1));
+      const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+      int lo = a.rowstart[(int64_t)b * (a.H + 1) + y], hi = a.rowstart[(int64_t)b * (a.H + 1) + y + 1];
+      const int xk = 32 * kb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (C[mid].x < xk) lo = mid + 1; else hi = mid;
+      }
+      a.rbi[g] = lo;
+    }
   }
   grid.sync();
 

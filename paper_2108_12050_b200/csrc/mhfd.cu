@@ -70,7 +70,7 @@ mhfd_status cuda_fail(cudaError_t e, const char* where) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, imgoff, chunkoff,
+  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
       chunkcnt, chunkpos, counters, scores, counts, total;
 };
 
@@ -101,6 +101,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.cand = take(sizeof(mhfd_blob) * c->cap * B);
   L.st = take(c->cap * B);
   L.rowstart = take(sizeof(int32_t) * (c->p.height + 1) * (size_t)B);
+  L.rbi = take(sizeof(int32_t) * (size_t)c->p.height * ((c->p.width + 31) / 32 + 1) * (size_t)B);
   L.imgoff = take(sizeof(int64_t) * (B + 1));
   L.chunkoff = take(sizeof(int64_t) * (B + 1));
   L.chunkcnt = take(sizeof(int32_t) * nchunk * B);
@@ -185,7 +186,10 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
   mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
   dim3 gn((nseg + 7) / 8, B);
-  if (paper) {
+  const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
+  if (rows_fast) {
+    k_nms_rows<false><<<gn, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0);
+  } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
   } else {
     k_nms_count<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segcnt);
@@ -193,7 +197,9 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   LAUNCH_CHECK("k_nms_count");
   k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
   LAUNCH_CHECK("k_seg_scan");
-  if (paper) {
+  if (rows_fast) {
+    k_nms_rows<true><<<gn, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap);
+  } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {
     k_nms_write<MHFD_NMS_26><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
@@ -338,6 +344,8 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   for (int s = 0; s < c->n; ++s) pa.rad[s] = c->rad[s];
   pa.st = reinterpret_cast<uint8_t*>(ws + L.st);
   pa.rowstart = reinterpret_cast<int32_t*>(ws + L.rowstart);
+  pa.rbi = reinterpret_cast<int32_t*>(ws + L.rbi);
+  pa.nbx = (c->p.width + 31) / 32;
   pa.img_off = reinterpret_cast<int64_t*>(ws + L.imgoff);
   pa.chunk_off = reinterpret_cast<int64_t*>(ws + L.chunkoff);
   pa.chunk_cnt = reinterpret_cast<int32_t*>(ws + L.chunkcnt);
