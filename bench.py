@@ -146,7 +146,7 @@ def oracle_band(img: np.ndarray, rows: int) -> tuple[float, dict]:
     return dt, {"candidates": int(len(cand)), "kept": int(keep.sum())}
 
 
-def cpu_baseline(img: np.ndarray, rows: int = 256) -> dict:
+def cpu_baseline(img: np.ndarray, rows: int = 2048) -> dict:
     import oracle
     oracle.set_threads(os.cpu_count() or 1)
     dt, info = oracle_band(img, rows)

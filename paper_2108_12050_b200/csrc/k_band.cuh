@@ -151,6 +151,66 @@ __device__ __forceinline__ void row_item(const uint32_t* __restrict__ src, const
                     acc[4 * v4 + 2].x + acc[4 * v4 + 2].y, acc[4 * v4 + 3].x + acc[4 * v4 + 3].y);
 }
 
+// Column pass + DoG + running max/argmax for the 8 rows x 2 columns a thread owns:
+// src = hbuf row (8 rg) column 2 cp; L' = sum_t w[t] hbuf[o + t]; DoG of the previous
+// level = tinv (L' - lprev) (tinv = t_{lev-1} * inv, Eq. 2 on the re-centred input).
+template <int HP>
+__device__ __forceinline__ void col_pass(const float* __restrict__ src, const float* __restrict__ wa, int ntap,
+                                         int lev, float tinv, float (&lprev)[16], float (&vbest)[16],
+                                         uint32_t (&ibest)[4]) {
+  float2 acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.f, 0.f);
+  float2 Xa[8], Xb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + k * HP);
+  auto group = [&](const float2 (&Xl)[8], const float2 (&Xh)[8], int jj) {
+    const float4 W0 = reinterpret_cast<const float4*>(wa + jj)[0];
+    const float4 W1 = reinterpret_cast<const float4*>(wa + jj)[1];
+    const float w8[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float2 wt = make_float2(w8[t], w8[t]);
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int m = o + t;
+        acc[o] = __ffma2_rn(m < 8 ? Xl[m] : Xh[m - 8], wt, acc[o]);
+      }
+    }
+  };
+  int j = 0;
+  for (; j + 16 <= ntap; j += 16) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * HP);
+    group(Xa, Xb, j);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + (j + 16 + k) * HP);
+    group(Xb, Xa, j + 8);
+  }
+  if (j < ntap) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * HP);
+    group(Xa, Xb, j);
+  }
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int k = 2 * o + c;
+      const float L = c ? acc[o].y : acc[o].x;
+      if (lev > 0) {
+        const float D = tinv * (L - lprev[k]);
+        if (D > vbest[k]) {
+          vbest[k] = D;
+          const int sh = (k & 3) * 8;
+          ibest[k >> 2] = (ibest[k >> 2] & ~(0xffu << sh)) | ((uint32_t)(lev - 1) << sh);
+        }
+      }
+      lprev[k] = L;
+    }
+  }
+}
+
 struct BandTile {
   int b, x0, Y0;
 };
@@ -346,62 +406,8 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
 
         // ---------------- column pass + DoG + running argmax ----------------
 #ifndef MHFD_EXP_SKIP_COL
-        {
-          const float* src = hbuf + (8 * rg) * kBandHP + 2 * cp;
-          float2 acc[8];
-#pragma unroll
-          for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.f, 0.f);
-          float2 Xa[8], Xb[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + k * kBandHP);
-          auto group = [&](const float2 (&Xl)[8], const float2 (&Xh)[8], int jj) {
-            const float4 W0 = reinterpret_cast<const float4*>(wa + jj)[0];
-            const float4 W1 = reinterpret_cast<const float4*>(wa + jj)[1];
-            const float w8[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const float2 wt = make_float2(w8[t], w8[t]);
-#pragma unroll
-              for (int o = 0; o < 8; ++o) {
-                const int m = o + t;
-                acc[o] = __ffma2_rn(m < 8 ? Xl[m] : Xh[m - 8], wt, acc[o]);
-              }
-            }
-          };
-          int j = 0;
-          for (; j + 16 <= ntap; j += 16) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * kBandHP);
-            group(Xa, Xb, j);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + (j + 16 + k) * kBandHP);
-            group(Xb, Xa, j + 8);
-          }
-          if (j < ntap) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * kBandHP);
-            group(Xa, Xb, j);
-          }
-          // DoG_{lev-1} = t_{lev-1} (L_lev - L_{lev-1}) with L = inv L' + const (Eq. 2)
-          const float tinv = lev > 0 ? tab.tdog[lev - 1] * inv : 0.f;
-#pragma unroll
-          for (int o = 0; o < 8; ++o) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const int k = 2 * o + c;
-              const float L = c ? acc[o].y : acc[o].x;
-              if (lev > 0) {
-                const float D = tinv * (L - lprev[k]);
-                if (D > vbest[k]) {
-                  vbest[k] = D;
-                  const int sh = (k & 3) * 8;
-                  ibest[k >> 2] = (ibest[k >> 2] & ~(0xffu << sh)) | ((uint32_t)(lev - 1) << sh);
-                }
-              }
-              lprev[k] = L;
-            }
-          }
-        }
+        col_pass<kBandHP>(hbuf + (8 * rg) * kBandHP + 2 * cp, wa, ntap, lev, lev > 0 ? tab.tdog[lev - 1] * inv : 0.f,
+                          lprev, vbest, ibest);
 #endif
         __syncthreads();  // hbuf is rewritten by the next level
       }

@@ -25,6 +25,7 @@
 #include "k_prune.cuh"
 #include "k_scale_space.cuh"
 #include "k_band.cuh"
+#include "k_band2.cuh"
 
 using namespace mhfd;
 
@@ -40,6 +41,7 @@ struct mhfd_ctx {
   int prune_grid;    // cooperative grid size for k_prune
   int sms;
   int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
+  int band_kind;     // 1 = k_band (1 CTA/SM, persistent), 2 = k_band2 (2 CTAs/SM); MHFD_SCHEDULE=band|band2
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
   cudaEvent_t* tev;
   int tmax, tcount;
@@ -49,6 +51,8 @@ struct mhfd_ctx {
 };
 
 namespace {
+
+constexpr size_t kSmemLimit = 227 * 1024;   // opt-in dynamic shared memory per CTA on sm_100
 
 thread_local std::string g_err;
 thread_local int32_t g_launches = 0;
@@ -253,6 +257,18 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   float* v = reinterpret_cast<float*>(ws + L.v);
   uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
+  // ---- a2-a6 on u8 images, two-CTA band schedule
+  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
+      band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
+    const size_t smem = band2_smem(c->tab->rmax, c->tab->ntaps_total);
+    cudaError_t ea = cudaFuncSetAttribute(k_band2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return cuda_fail(ea, "k_band2 attribute");
+    dim3 gb((W + kStripW - 1) / kStripW, (H + kBand2BH - 1) / kBand2BH, B);
+    k_band2<<<gb, kBand2Threads, smem, st>>>(img, s, par, *c->tab, v, idx);
+    LAUNCH_CHECK("k_band2");
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
+  }
   // ---- a2-a6 on u8 images: band schedule (raw band staged once per CTA, no f32 prepass)
   if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
       band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
@@ -293,7 +309,8 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   const int strips = (W + kStripW - 1) / kStripW;
   // band height: 256 rows when that still gives >= 4 waves of 2 CTAs/SM, else 128
   const int64_t ctas256 = (int64_t)strips * ((H + 255) / 256) * B;
-  const int RPT = (ctas256 >= (int64_t)c->sms * 2 * 4) ? 32 : 16;
+  const bool fits256 = scale_space_smem(c->tab->rmax, 256, c->tab->ntaps_total) <= kSmemLimit;
+  const int RPT = (fits256 && ctas256 >= (int64_t)c->sms * 2 * 4) ? 32 : 16;
   const int BH = 8 * RPT;
   const size_t smem = scale_space_smem(c->tab->rmax, BH, c->tab->ntaps_total);
   const bool fast = fast_staging(W, c->tab->rmax);
@@ -468,6 +485,8 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   {
     const char* nb = getenv("MHFD_NO_BAND");
     c->band_enabled = !(nb && nb[0] == '1');
+    const char* sch = getenv("MHFD_SCHEDULE");
+    c->band_kind = (sch && strcmp(sch, "band2") == 0) ? 2 : 1;
   }
   LevelTable& T = *c->tab;
   T.nlev = n + 1;
@@ -507,6 +526,11 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     return fail(MHFD_ERR_CUDA, "occupancy query for k_prune failed");
   }
   c->prune_grid = bps * c->sms;
+  if (scale_space_smem(rmax, 128, T.ntaps_total) > kSmemLimit) {
+    mhfd_destroy(c);
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "ceil(5*max_sigma) = %d: the generic schedule's shared memory exceeds the "
+                "sm_100 limit", rmax);
+  }
   *out = c;
   return MHFD_OK;
 }

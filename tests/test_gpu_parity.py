@@ -248,3 +248,38 @@ def test_c3_sampled_pixels_and_properties(c3_batch):
         assert all(r[3] > 0.09 for r in rows)
     sc = scores.cpu().tolist()
     assert sc[0] > sc[1] > sc[2], sc   # defocus 0, 0.5, 1.0 px
+
+
+# ------------------------------------------------------------------ C5: 8192^2 u16, sigma 1-30, 20 scales
+def test_c5_large_radius_sampled():
+    """Large-kernel-radius stress (config C5): R up to 150 takes the generic schedule;
+    sampled pixels vs the oracle's 2-D definition, argmax, properties."""
+    img = synth.em_tile(8192, 8192, 7, defocus=0.0, dose=300.0, bits=16, device="cuda")
+    img16 = img.to(torch.int32).cpu().numpy().astype(np.uint16)
+    t16 = torch.from_numpy(img16)
+    C5 = dict(min_sigma=1.0, max_sigma=30.0, num_scales=20)
+    det = mhfd.Detector(8192, 8192, threshold=0.145, **C5)
+    dump = det.debug_dump(t16, dog=False, cands=False)
+    scores, cnt = det.focus_score(t16, counts=True)
+    torch.cuda.synchronize()
+    lo, hi = oracle.percentiles(img16)
+    assert dump["lohi"][0].tolist() == [lo, hi]
+    f = oracle.stretch(img16, lo, hi)
+    v = dump["v"][0].cpu().numpy()
+    idx = dump["idx"][0].cpu().numpy()
+    rng = np.random.default_rng(11)
+    pts = [(int(y), int(x)) for y, x in rng.integers(0, 8192, size=(24, 2))] + [(0, 0), (8191, 8191), (4096, 127)]
+    vals = {p: oracle.dog_at(f, 1.0, 30.0, 20, p[0], p[1]) for p in pts}
+    peak = max(float(d.max()) for d in vals.values())
+    eps = P.REL_EPS * max(peak, 0.1)
+    for (y, x), Dv in vals.items():
+        assert abs(float(v[y, x]) - Dv.max()) <= eps, ((y, x), float(v[y, x]), Dv.max(), eps)
+        s = np.sort(Dv)
+        if s[-1] - s[-2] > eps:
+            assert int(idx[y, x]) == int(np.argmax(Dv))
+    assert int(cnt[0]) > 0 and float(scores[0]) == float(int(cnt[0]))
+
+
+def test_c2_26_mode_parity():
+    img = synth.em_tile_np(1024, 1024, 1000, defocus=0.0, dose=300.0, bits=8)
+    _full_parity(img, C3, nms="26")
