@@ -55,7 +55,7 @@ __host__ __device__ inline size_t band_rawp_bytes(int rmax) {
 }
 __host__ __device__ inline size_t band_smem(int rmax, int ntaps_total) {
   return band_land_bytes(rmax) + band_rawp_bytes(rmax) +
-         sizeof(float) * ((size_t)band_hrows(rmax) * kBandHP + 2 * (size_t)wtab_floats(ntaps_total)) + 16;
+         sizeof(float) * ((size_t)band_hrows(rmax) * kBandHP + 3 * (size_t)wtab_floats(ntaps_total)) + 16;
 }
 __host__ __device__ inline bool band_ok(int W, int H, int rmax, int ntaps_total) {
   return band_smem(rmax, ntaps_total) <= 224 * 1024 && W >= band_raw_w(rmax) && H >= band_raw_rows(rmax);
@@ -152,10 +152,12 @@ __device__ __forceinline__ void row_item(const uint32_t* __restrict__ src, const
 }
 
 // Column pass + DoG + running max/argmax for the 8 rows x 2 columns a thread owns:
-// src = hbuf row (8 rg) column 2 cp; L' = sum_t w[t] hbuf[o + t]; DoG of the previous
-// level = tinv (L' - lprev) (tinv = t_{lev-1} * inv, Eq. 2 on the re-centred input).
+// src = hbuf row (8 rg + p) column 2 cp (the first real tap row), L' = sum_{t<n} wc[t]
+// src[o + t] with n = 2R+1 unpadded taps (wc = the level's taps without the row-pass
+// prefix); DoG of the previous level = tinv (L' - lprev) (tinv = t_{lev-1} inv, Eq. 2 on
+// the re-centred input).
 template <int HP>
-__device__ __forceinline__ void col_pass(const float* __restrict__ src, const float* __restrict__ wa, int ntap,
+__device__ __forceinline__ void col_pass(const float* __restrict__ src, const float* __restrict__ wc, int n,
                                          int lev, float tinv, float (&lprev)[16], float (&vbest)[16],
                                          uint32_t (&ibest)[4]) {
   float2 acc[8];
@@ -164,33 +166,40 @@ __device__ __forceinline__ void col_pass(const float* __restrict__ src, const fl
   float2 Xa[8], Xb[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + k * HP);
-  auto group = [&](const float2 (&Xl)[8], const float2 (&Xh)[8], int jj) {
-    const float4 W0 = reinterpret_cast<const float4*>(wa + jj)[0];
-    const float4 W1 = reinterpret_cast<const float4*>(wa + jj)[1];
+  auto group = [&](const float2 (&Xl)[8], const float2 (&Xh)[8], int jj, int cnt) {
+    const float4 W0 = reinterpret_cast<const float4*>(wc + jj)[0];
+    const float4 W1 = reinterpret_cast<const float4*>(wc + jj)[1];
     const float w8[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const float2 wt = make_float2(w8[t], w8[t]);
+      if (t < cnt) {
+        const float2 wt = make_float2(w8[t], w8[t]);
 #pragma unroll
-      for (int o = 0; o < 8; ++o) {
-        const int m = o + t;
-        acc[o] = __ffma2_rn(m < 8 ? Xl[m] : Xh[m - 8], wt, acc[o]);
+        for (int o = 0; o < 8; ++o) {
+          const int m = o + t;
+          acc[o] = __ffma2_rn(m < 8 ? Xl[m] : Xh[m - 8], wt, acc[o]);
+        }
       }
     }
   };
   int j = 0;
-  for (; j + 16 <= ntap; j += 16) {
+  for (; j + 16 <= n; j += 16) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * HP);
-    group(Xa, Xb, j);
+    group(Xa, Xb, j, 8);
 #pragma unroll
     for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + (j + 16 + k) * HP);
-    group(Xb, Xa, j + 8);
+    group(Xb, Xa, j + 8, 8);
   }
-  if (j < ntap) {
+  if (j < n) {   // 1 .. 15 remaining taps
 #pragma unroll
     for (int k = 0; k < 8; ++k) Xb[k] = *reinterpret_cast<const float2*>(src + (j + 8 + k) * HP);
-    group(Xa, Xb, j);
+    group(Xa, Xb, j, min(8, n - j));
+    if (j + 8 < n) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Xa[k] = *reinterpret_cast<const float2*>(src + (j + 16 + k) * HP);
+      group(Xb, Xa, j + 8, n - j - 8);
+    }
   }
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
@@ -286,7 +295,8 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
   float* hbuf = reinterpret_cast<float*>(rawp + band_rawp_bytes(rmax));   // hrows x 36
   float* wA = hbuf + band_hrows(rmax) * kBandHP;
   float* wB = wA + wtab_floats(tab.ntaps_total);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wB + wtab_floats(tab.ntaps_total));
+  float* wC = wB + wtab_floats(tab.ntaps_total);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wC + wtab_floats(tab.ntaps_total));
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -301,7 +311,10 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
   for (int i = kBandBH * kBandHP + tid; i < band_hrows(rmax) * kBandHP; i += kBandThreads) hbuf[i] = 0.f;
   for (int i = tid; i < tab.ntaps_total; i += kBandThreads) wA[i] = tab.w[i];
   for (int l = 0; l < tab.nlev; ++l)
-    for (int i = tid; i < tab.ntap[l] + 8; i += kBandThreads) wB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
+    for (int i = tid; i < tab.ntap[l] + 8; i += kBandThreads) {
+      wB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
+      wC[tab.woff[l] + i] = i < 2 * tab.R[l] + 1 ? tab.w[tab.woff[l] + tab.pre[l] + i] : 0.f;
+    }
   for (int i = tid; i < RWP / 4; i += kBandThreads)   // row past the band: x = 0 (meets zero taps)
     reinterpret_cast<uint32_t*>(rawp + (size_t)NRB * RWP)[i] = 0x80808080u;
   if (tid == 0) {
@@ -406,8 +419,8 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
 
         // ---------------- column pass + DoG + running argmax ----------------
 #ifndef MHFD_EXP_SKIP_COL
-        col_pass<kBandHP>(hbuf + (8 * rg) * kBandHP + 2 * cp, wa, ntap, lev, lev > 0 ? tab.tdog[lev - 1] * inv : 0.f,
-                          lprev, vbest, ibest);
+        col_pass<kBandHP>(hbuf + (8 * rg + p) * kBandHP + 2 * cp, wC + tab.woff[lev], 2 * R + 1, lev,
+                          lev > 0 ? tab.tdog[lev - 1] * inv : 0.f, lprev, vbest, ibest);
 #endif
         __syncthreads();  // hbuf is rewritten by the next level
       }

@@ -24,7 +24,7 @@ __host__ __device__ inline size_t band2_rawp_bytes(int rmax) {
 }
 __host__ __device__ inline size_t band2_smem(int rmax, int ntaps_total) {
   return band2_rawp_bytes(rmax) +
-         sizeof(float) * ((size_t)band2_hrows(rmax) * kBandHP + 2 * (size_t)wtab_floats(ntaps_total));
+         sizeof(float) * ((size_t)band2_hrows(rmax) * kBandHP + 3 * (size_t)wtab_floats(ntaps_total));
 }
 __host__ __device__ inline bool band2_ok(int W, int H, int rmax, int ntaps_total) {
   return band2_smem(rmax, ntaps_total) <= 110 * 1024 && W >= band_raw_w(rmax) && H >= band2_raw_rows(rmax) &&
@@ -34,7 +34,7 @@ __host__ __device__ inline bool band2_ok(int W, int H, int rmax, int ntaps_total
 __global__ void __launch_bounds__(kBand2Threads, 2)
 k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par,
         const __grid_constant__ LevelTable tab, float* __restrict__ v_out, uint8_t* __restrict__ idx_out) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int rmax = tab.rmax;
   const int RM = band_rm(rmax);
   const int RW = band_raw_w(rmax);
@@ -44,6 +44,7 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
   float* hbuf = reinterpret_cast<float*>(rawp + band2_rawp_bytes(rmax));     // hrows x 36
   float* wA = hbuf + band2_hrows(rmax) * kBandHP;
   float* wB = wA + wtab_floats(tab.ntaps_total);
+  float* wC = wB + wtab_floats(tab.ntaps_total);
 
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * kStripW;
@@ -105,7 +106,10 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
   for (int i = kBand2BH * kBandHP + tid; i < band2_hrows(rmax) * kBandHP; i += kBand2Threads) hbuf[i] = 0.f;
   for (int i = tid; i < tab.ntaps_total; i += kBand2Threads) wA[i] = tab.w[i];
   for (int l = 0; l < tab.nlev; ++l)
-    for (int i = tid; i < tab.ntap[l] + 8; i += kBand2Threads) wB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
+    for (int i = tid; i < tab.ntap[l] + 8; i += kBand2Threads) {
+      wB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
+      wC[tab.woff[l] + i] = i < 2 * tab.R[l] + 1 ? tab.w[tab.woff[l] + tab.pre[l] + i] : 0.f;
+    }
   __syncthreads();
 
   const float inv = ip.inv;
@@ -140,8 +144,8 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
       }
     }
     __syncthreads();  // hbuf complete
-    col_pass<kBandHP>(hbuf + (8 * rg) * kBandHP + 2 * cp, wa, ntap, lev, lev > 0 ? tab.tdog[lev - 1] * inv : 0.f,
-                      lprev, vbest, ibest);
+    col_pass<kBandHP>(hbuf + (8 * rg + p) * kBandHP + 2 * cp, wC + tab.woff[lev], 2 * R + 1, lev,
+                      lev > 0 ? tab.tdog[lev - 1] * inv : 0.f, lprev, vbest, ibest);
     __syncthreads();  // hbuf is rewritten by the next level
   }
 

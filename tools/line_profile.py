@@ -46,9 +46,13 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 iA, iE, iW = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+STALLS = ["stall_math", "stall_wait", "stall_not_selected", "stall_selected", "stall_short_sb", "stall_barrier",
+          "stall_long_sb", "stall_dispatch", "stall_mio", "stall_branch_resolving"]
+iS = {k: hdr.index(k) for k in STALLS if k in hdr}
 data = [r for r in rows[2:] if len(r) > iW and r[iA].startswith("0x")]
 base = int(data[0][iA], 16)
 agg_s, agg_e = collections.Counter(), collections.Counter()
+agg_r = collections.defaultdict(collections.Counter)
 tot = 0
 for r in data:
     off = int(r[iA], 16) - base
@@ -57,6 +61,8 @@ for r in data:
     e = int(r[iE]) if r[iE].isdigit() else 0
     agg_s[key] += w
     agg_e[key] += e
+    for k, i in iS.items():
+        agg_r[key][k] += int(r[i]) if r[i].isdigit() else 0
     tot += w
 src_cache = {}
 print(f"total samples {tot}")
@@ -67,4 +73,5 @@ for key, w in agg_s.most_common(30):
         if os.path.exists(cand):
             src_cache.setdefault(cand, open(cand).read().split("\n"))
             text = src_cache[cand][line - 1].strip()[:80] if 0 < line <= len(src_cache[cand]) else ""
-    print(f"{w / max(tot, 1) * 100:5.1f}%  {agg_e[key]:>12d}  {fn}:{line}  {text}")
+    br = " ".join(f"{k[6:10]}={v * 100 // max(w, 1)}" for k, v in agg_r[key].most_common(4) if v)
+    print(f"{w / max(tot, 1) * 100:5.1f}%  {agg_e[key]:>12d}  {fn}:{line}  {text[:56]:56s} [{br}]")
