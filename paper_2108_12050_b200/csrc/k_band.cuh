@@ -6,9 +6,9 @@
 //   CTA = one image x one strip of 32 columns x one band of BH = 256 rows, 512 threads.
 //   prologue : the raw u8 band with its halo ((256+2Rmax+3) x (32+2*ceil16(Rmax+3)) bytes,
 //              ~60 KB at sigma <= 10) comes from HBM ONCE, by TMA (image-edge CTAs: plain
-//              loads with periodic wrap).  Each byte is then saturated to [lo, hi] and
-//              re-centred, x = clamp(p, lo, hi) - mid, stored as x + 128 in a copy with a
-//              conflict-free row pitch.  The stretch I' - 1/2 = (x + mid - lo) inv - 1/2 is
+//              loads with periodic wrap).  Each byte is then saturated to [lo, hi] (VIMNMX on
+//              u16 pairs) into a copy with a conflict-free row pitch; the row pass
+//              re-centres it, x = p' - mid, in its exact u8 -> f32 conversion.  The stretch I' - 1/2 = (x + mid - lo) inv - 1/2 is
 //              affine in x and the blur kernels sum to one, so every level is blurred on x
 //              and the DoG is t_i inv (L'_{i+1} - L'_i)  (exact for unit-sum kernels).
 //   per level: row pass — lane = row, 16 consecutive output columns per thread, input
@@ -41,7 +41,7 @@ __host__ __device__ inline int band_raw_rows(int rmax) { return kBandBH + 2 * rm
 __host__ __device__ inline int band_land_rows(int rmax) {
   return (band_raw_rows(rmax) + kBandBoxRows - 1) / kBandBoxRows * kBandBoxRows;
 }
-// re-centred copy: row pitch 4 x odd bytes (conflict-free 4-byte loads with lane = row),
+// saturated copy: row pitch 4 x odd bytes (conflict-free 4-byte loads with lane = row),
 // wide enough for the row-pass window overrun
 __host__ __device__ inline int band_rwp(int rmax) {
   int q = (band_raw_w(rmax) + 16 + 3) / 4;
@@ -61,17 +61,24 @@ __host__ __device__ inline bool band_ok(int W, int H, int rmax, int ntaps_total)
   return band_smem(rmax, ntaps_total) <= 224 * 1024 && W >= band_raw_w(rmax) && H >= band_raw_rows(rmax);
 }
 
-// two exact floats x - 128 for the bytes of w picked by the two PRMT selectors in sel
-// (2^23 + u built by PRMT, 2^23 + 128 subtracted by one FADD2)
-__device__ __forceinline__ float2 byte_pair(uint32_t w, uint32_t sel_lo, uint32_t sel_hi) {
+// Exact floats x = p' - mid for two bytes p' of w (PRMT builds 2^23 + p', one FADD2
+// subtracts nc = 2^23 + mid; every value is an integer below 2^24, so nothing rounds).
+__device__ __forceinline__ float2 byte_pair(uint32_t w, uint32_t sel_lo, uint32_t sel_hi, float2 nc) {
   const uint32_t a = __byte_perm(w, 0x4B000000u, sel_lo);
   const uint32_t b = __byte_perm(w, 0x4B000000u, sel_hi);
-  return __fadd2_rn(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(-8388736.f, -8388736.f));
+  return __fadd2_rn(make_float2(__uint_as_float(a), __uint_as_float(b)), nc);
 }
 // one 4-byte word -> pairs (x0, x1), (x2, x3)
-__device__ __forceinline__ void word_pairs(uint32_t w, float2& p0, float2& p1) {
-  p0 = byte_pair(w, 0x7540u, 0x7541u);
-  p1 = byte_pair(w, 0x7542u, 0x7543u);
+__device__ __forceinline__ void word_pairs(uint32_t w, float2& p0, float2& p1, float2 nc) {
+  p0 = byte_pair(w, 0x7540u, 0x7541u, nc);
+  p1 = byte_pair(w, 0x7542u, 0x7543u, nc);
+}
+// saturate the 4 bytes of w to [lo, hi] (two VIMNMX.U16x2 per half-word pair); lo4/hi4 =
+// the bounds replicated in both 16-bit halves
+__device__ __forceinline__ uint32_t clamp_bytes(uint32_t w, uint32_t lo2, uint32_t hi2) {
+  const uint32_t e = __vminu2(__vmaxu2(__byte_perm(w, 0u, 0x4240u), lo2), hi2);   // bytes 0, 2
+  const uint32_t o = __vminu2(__vmaxu2(__byte_perm(w, 0u, 0x4341u), lo2), hi2);   // bytes 1, 3
+  return __byte_perm(e, o, 0x6240u);
 }
 
 // Row pass over 8 taps for NQ output pairs (2*NQ consecutive outputs): the input pairs
@@ -96,9 +103,10 @@ __device__ __forceinline__ void row_group(float2 (&acc)[2 * NQ], const float2 (&
 }
 
 template <int NB>
-__device__ __forceinline__ void load_block(float2 (&Q)[NB][4], int blk, const uint32_t* __restrict__ src, int word) {
-  word_pairs(src[word], Q[blk][0], Q[blk][1]);
-  word_pairs(src[word + 1], Q[blk][2], Q[blk][3]);
+__device__ __forceinline__ void load_block(float2 (&Q)[NB][4], int blk, const uint32_t* __restrict__ src, int word,
+                                           float2 nc) {
+  word_pairs(src[word], Q[blk][0], Q[blk][1], nc);
+  word_pairs(src[word + 1], Q[blk][2], Q[blk][3], nc);
 }
 
 // One row-pass item: 2*NQ consecutive outputs of one row (src = its first input word),
@@ -106,20 +114,20 @@ __device__ __forceinline__ void load_block(float2 (&Q)[NB][4], int blk, const ui
 template <int NQ>
 __device__ __forceinline__ void row_item(const uint32_t* __restrict__ src, const float* __restrict__ wa,
                                          const float* __restrict__ wb, int ntap, float* __restrict__ hdst,
-                                         bool store) {
+                                         bool store, float2 nc) {
   constexpr int NB = NQ / 4 + 1;
   float2 acc[2 * NQ];
 #pragma unroll
   for (int o = 0; o < 2 * NQ; ++o) acc[o] = make_float2(0.f, 0.f);
   float2 Q[NB][4];
 #pragma unroll
-  for (int bb = 0; bb + 1 < NB; ++bb) load_block(Q, bb, src, 2 * bb);
+  for (int bb = 0; bb + 1 < NB; ++bb) load_block(Q, bb, src, 2 * bb, nc);
   const int ng = ntap >> 3;   // groups of 8 taps; group gi uses blocks gi .. gi+NB-1 (mod NB)
   int gi = 0;
   for (; gi + NB <= ng; gi += NB) {
 #pragma unroll
     for (int u = 0; u < NB; ++u) {
-      load_block(Q, (u + NB - 1) % NB, src, 2 * (gi + u + NB - 1));
+      load_block(Q, (u + NB - 1) % NB, src, 2 * (gi + u + NB - 1), nc);
       row_group<NQ, NB>(acc, Q, u, wa + 8 * (gi + u), wb + 8 * (gi + u));
     }
   }
@@ -127,7 +135,7 @@ __device__ __forceinline__ void row_item(const uint32_t* __restrict__ src, const
 #pragma unroll
   for (int u = 0; u < NB - 1; ++u) {
     if (u < rem) {
-      load_block(Q, (u + NB - 1) % NB, src, 2 * (gi + u + NB - 1));
+      load_block(Q, (u + NB - 1) % NB, src, 2 * (gi + u + NB - 1), nc);
       row_group<NQ, NB>(acc, Q, u, wa + 8 * (gi + u), wb + 8 * (gi + u));
     }
   }
@@ -291,7 +299,7 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
   const int NRB = band_raw_rows(rmax);
   const int RWP = band_rwp(rmax);
   uint8_t* land = smem_raw;                                   // TMA landing: land_rows x RW
-  uint8_t* rawp = land + band_land_bytes(rmax);               // (NRB+1) x RWP, bytes x + 128
+  uint8_t* rawp = land + band_land_bytes(rmax);               // (NRB+1) x RWP, saturated bytes p'
   float* hbuf = reinterpret_cast<float*>(rawp + band_rawp_bytes(rmax));   // hrows x 36
   float* wA = hbuf + band_hrows(rmax) * kBandHP;
   float* wB = wA + wtab_floats(tab.ntaps_total);
@@ -316,7 +324,7 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
       wC[tab.woff[l] + i] = i < 2 * tab.R[l] + 1 ? tab.w[tab.woff[l] + tab.pre[l] + i] : 0.f;
     }
   for (int i = tid; i < RWP / 4; i += kBandThreads)   // row past the band: x = 0 (meets zero taps)
-    reinterpret_cast<uint32_t*>(rawp + (size_t)NRB * RWP)[i] = 0x80808080u;
+    reinterpret_cast<uint32_t*>(rawp + (size_t)NRB * RWP)[i] = 0u;
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -333,7 +341,7 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
   const int g = warp & 1;
 
   for (;;) {
-    // ---- the fetched band: wait, then saturate/re-centre into rawp (x + 128)
+    // ---- the fetched band: wait, then saturate into rawp (p' = clamp(p, lo, hi))
     if (mode) {
       mbar_wait(bar, phase);
       phase ^= 1u;
@@ -341,24 +349,16 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
     __syncthreads();
     const ImgPar ip = par[bt.b];
     const int lo = ip.lo, hi = ip.hi;
-    const int mid = lo + (hi - lo + 1) / 2;   // x in [-128, 127] since hi - lo <= 255
+    const int mid = lo + (hi - lo + 1) / 2;   // x = p' - mid in [-128, 127] since hi - lo <= 255
+    const uint32_t lo2 = (uint32_t)lo * 0x10001u, hi2 = (uint32_t)hi * 0x10001u;
+    const float2 nc = make_float2(-(8388608.f + (float)mid), -(8388608.f + (float)mid));
     {
       const int nw = RW / 4;
       for (int r = warp; r < NRB; r += 16) {
         const uint32_t* srow = reinterpret_cast<const uint32_t*>(land + (size_t)r * RW);
         uint32_t* drow = reinterpret_cast<uint32_t*>(rawp + (size_t)r * RWP);
         for (int c4 = lane; c4 < RWP / 4; c4 += 32) {
-          uint32_t o = 0x80808080u;   // past the band: x = 0
-          if (c4 < nw) {
-            const uint32_t wd = srow[c4];
-            o = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int pv = (int)((wd >> (8 * k)) & 255u);
-              o |= (uint32_t)(min(max(pv, lo), hi) - mid + 128) << (8 * k);
-            }
-          }
-          drow[c4] = o;
+          drow[c4] = c4 < nw ? clamp_bytes(srow[c4], lo2, hi2) : 0u;   // past the band: meets zero taps
         }
       }
     }
@@ -404,14 +404,14 @@ k_band(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ p
         {
           const uint8_t* rbase = rawp + (size_t)(rs + prow) * RWP + cs;
           row_item<8>(reinterpret_cast<const uint32_t*>(rbase + 16 * g), wa, wb, ntap,
-                      hbuf + prow * kBandHP + 16 * g, true);
+                      hbuf + prow * kBandHP + 16 * g, true, nc);
           const int n2 = nrow - 256;                       // 13 .. 2*rmax+3 rows
           const int items = ((n2 + 31) >> 5) * 4;          // 32 rows x 8 columns each
           for (int it = warp; it < items; it += 16) {
             const int r2 = 256 + 32 * (it >> 2) + lane;    // hbuf row
             const int c2 = 8 * (it & 3);
             row_item<4>(reinterpret_cast<const uint32_t*>(rawp + (size_t)(rs + r2) * RWP + cs + c2), wa, wb, ntap,
-                        hbuf + r2 * kBandHP + c2, r2 < nrow);
+                        hbuf + r2 * kBandHP + c2, r2 < nrow, nc);
           }
         }
 #endif

@@ -5,8 +5,8 @@
 // 8 rows x 2 columns per thread, column-pair FFMA2), but a CTA is 256 threads on a
 // 128-row band and needs ~84 KB of shared memory, so two CTAs share an SM and one CTA's
 // staging, barriers and DoG updates overlap the other's FMA stream.  The raw band is
-// staged by plain 4-byte loads straight into the re-centred layout (saturate to [lo, hi],
-// x = p' - mid, stored x + 128), no landing buffer.  The taller-halo cost
+// staged by plain 4-byte loads straight into the saturated layout (p' = clamp(p, lo, hi),
+// PAPER.md:257; the row pass re-centres x = p' - mid while converting), no landing buffer.  The taller-halo cost
 // (row pass on 128 + 2R + p rows per 128) is the price of the second CTA.
 #pragma once
 #include "common.cuh"
@@ -65,24 +65,23 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
     return;
   }
 
-  // ---- stage the band (rows Y0-rmax-3 .., columns x0-RM ..), saturated and re-centred
+  // ---- stage the band (rows Y0-rmax-3 .., columns x0-RM ..), saturated
   {
     const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
     const int yr = Y0 - rmax - 3, xr = x0 - RM;
     const bool xin = xr >= 0 && xr + RW <= s.W;
-    const int lo = ip.lo, hi = ip.hi;
-    const int mid = lo + (hi - lo + 1) / 2;   // x in [-128, 127] since hi - lo <= 255
+    const uint32_t lo2 = (uint32_t)ip.lo * 0x10001u, hi2 = (uint32_t)ip.hi * 0x10001u;
     const int nw = RW / 4, nwp = RWP / 4;
 #pragma unroll 4
     for (int r = warp; r <= NRB; r += 8) {
       uint32_t* drow = reinterpret_cast<uint32_t*>(rawp + (size_t)r * RWP);
-      if (r == NRB) {   // padding row: x = 0 (meets zero taps only)
-        for (int c4 = lane; c4 < nwp; c4 += 32) drow[c4] = 0x80808080u;
+      if (r == NRB) {   // padding row (meets zero taps only)
+        for (int c4 = lane; c4 < nwp; c4 += 32) drow[c4] = 0u;
         continue;
       }
       const uint8_t* row = img + (int64_t)wrap_idx(yr + r, s.H) * s.pitch;
       for (int c4 = lane; c4 < nwp; c4 += 32) {
-        uint32_t o = 0x80808080u;
+        uint32_t o = 0u;
         if (c4 < nw) {
           uint32_t wd;
           if (xin) {
@@ -92,12 +91,7 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
 #pragma unroll
             for (int k = 0; k < 4; ++k) wd |= (uint32_t)row[wrap_idx(xr + 4 * c4 + k, s.W)] << (8 * k);
           }
-          o = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int pv = (int)((wd >> (8 * k)) & 255u);
-            o |= (uint32_t)(min(max(pv, lo), hi) - mid + 128) << (8 * k);
-          }
+          o = clamp_bytes(wd, lo2, hi2);
         }
         drow[c4] = o;
       }
@@ -113,6 +107,8 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
   __syncthreads();
 
   const float inv = ip.inv;
+  const int mid = ip.lo + (ip.hi - ip.lo + 1) / 2;   // x = p' - mid in [-128, 127]
+  const float2 nc = make_float2(-(8388608.f + (float)mid), -(8388608.f + (float)mid));
   const int cp = lane & 15;                    // column pair
   const int rg = 2 * warp + (lane >> 4);       // row group 0..15 (8 rows each)
   const int prow = lane + 32 * (warp >> 1);    // row-pass row in a 128-row pass
@@ -134,13 +130,13 @@ k_band2(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ 
     // ---- row pass: rows 0..127 one 32x16 item per warp; the 2R+p remaining rows as
     //      32x16 items on warps 0 .. 2*ceil((2R+p)/32)-1
     row_item<8>(reinterpret_cast<const uint32_t*>(rawp + (size_t)(rs + prow) * RWP + cs + 16 * g), wa, wb, ntap,
-                hbuf + prow * kBandHP + 16 * g, true);
+                hbuf + prow * kBandHP + 16 * g, true, nc);
     {
       const int items = ((nrow - kBand2BH + 31) >> 5) * 2;
       if (warp < items) {
         const int r2 = kBand2BH + 32 * (warp >> 1) + lane;
         row_item<8>(reinterpret_cast<const uint32_t*>(rawp + (size_t)(rs + r2) * RWP + cs + 16 * g), wa, wb, ntap,
-                    hbuf + r2 * kBandHP + 16 * g, r2 < nrow);
+                    hbuf + r2 * kBandHP + 16 * g, r2 < nrow, nc);
       }
     }
     __syncthreads();  // hbuf complete
