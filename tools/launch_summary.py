@@ -11,12 +11,12 @@ iK, iV, iU = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
 agg = collections.defaultdict(list)
 for r in data:
-    name = r[iK].split("(")[0].replace("void ", "")
-    if not name.startswith("mhfd::"):
+    name = r[iK].split("(")[0].replace("void ", "").replace("mhfd::", "")
+    if not name.startswith("k_"):
         continue   # synthetic-input generation (torch) is outside the timed step
     agg[name].append(float(r[iV].replace(",", "")) * scale[r[iU]])
 tot = sum(sum(v) for v in agg.values())
-print(f"# {sys.argv[1]}: mhfd kernels only (cold-cache, serialised ncu timings; compare shares)")
+print(f"# {sys.argv[1]}: library kernels (k_*) only (cold-cache, serialised ncu timings; compare shares)")
 print(f"{'kernel':40s} {'launches':>8s} {'mean_ms':>10s} {'share':>7s}")
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     print(f"{k:40s} {len(v):8d} {sum(v) / len(v):10.4f} {sum(v) / tot * 100:6.1f}%")
