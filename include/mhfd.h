@@ -166,7 +166,8 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
 /* Per-stage device timing (bench instrumentation; not thread-safe).
  * mhfd_timing_enable(c, k) arms k records (k = 0 disables); each subsequent
  * mhfd_detect_batch / mhfd_focus_score call records CUDA events on its stream
- * around its 4 stages: [0] percentiles (a1), [1] k_scale_space (a2-a6),
+ * around its 4 stages: [0] percentiles (a1), [1] the fused blur kernel (a2-a6,
+ * the one mhfd_schedule_name names),
  * [2] NMS + compaction (a7-a8), [3] pruning + score (a9-a10).
  * mhfd_timing_read waits for the recorded events and writes ms[call*4 + stage]
  * for *ncalls (<= k) calls. */
@@ -187,6 +188,15 @@ mhfd_status mhfd_debug_dump(mhfd_ctx* c, const void* d_images, int32_t dtype, in
 
 /* Read back the parameters a context was built with (derived fields filled). */
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
+
+/* Name of the kernel that computes rows a2-a6 (stretch, blur, DoG, scale argmax)
+ * for images of `dtype` in mhfd_detect_batch / mhfd_focus_score on this context:
+ * "k_tc" (u8, Eq. 3 NMS, tensor-core banded blur; default when the staged tile
+ * fits), "k_band" / "k_band2" (u8, CUDA-core band schedules), "k_scale_space"
+ * (generic).  The environment variable MHFD_SCHEDULE=tc|band|band2|generic, read
+ * at mhfd_create, selects among the applicable ones.  Static string; "none" for
+ * a NULL context. */
+const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype);
 
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int32_t mhfd_last_launch_count(void);

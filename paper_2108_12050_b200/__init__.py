@@ -188,6 +188,11 @@ class Detector:
         _abi.check(self._lib.mhfd_timing_read(self._h, buf, ctypes.byref(n)))
         return [[buf[4 * k + j] for j in range(4)] for k in range(n.value)]
 
+    def schedule(self, dtype: str = "u8") -> str:
+        """Kernel that computes rows a2-a6 for `dtype` images (mhfd_schedule_name)."""
+        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16}[dtype]
+        return self._lib.mhfd_schedule_name(self._h, code).decode()
+
     @staticmethod
     def last_launch_count() -> int:
         return int(_abi.load().mhfd_last_launch_count())

@@ -5,7 +5,8 @@
 // sequence on the caller's stream without any host synchronisation:
 //
 //   k_hist / k_select (u8: 1 pass, u16: 2 passes)   percentiles, row a1
-//   k_scale_space                                   stretch+blur+DoG+argmax, rows a2-a6
+//   k_tc (u8, tensor cores) | k_band (u8, CUDA cores) | k_scale_space (generic)
+//                                                   stretch+blur+DoG+argmax, rows a2-a6
 //   k_nms_count -> k_seg_scan -> k_nms_write        NMS+threshold+compaction, rows a7-a8
 //   k_prune (cooperative, one launch)               pruning + score + ordered list, a9-a10
 #include <algorithm>
@@ -16,6 +17,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include <cudaTypedefs.h>
 
@@ -26,6 +28,7 @@
 #include "k_scale_space.cuh"
 #include "k_band.cuh"
 #include "k_band2.cuh"
+#include "k_tc.cuh"
 
 using namespace mhfd;
 
@@ -41,7 +44,9 @@ struct mhfd_ctx {
   int prune_grid;    // cooperative grid size for k_prune
   int sms;
   int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
-  int band_kind;     // 1 = k_band (1 CTA/SM, persistent), 2 = k_band2 (2 CTAs/SM); MHFD_SCHEDULE=band|band2
+  int band_kind;     // 3 = k_tc (default), 1 = k_band, 2 = k_band2; MHFD_SCHEDULE=tc|band|band2|generic
+  TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
+  uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
   cudaEvent_t* tev;
   int tmax, tcount;
@@ -257,6 +262,25 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   float* v = reinterpret_cast<float*>(ws + L.v);
   uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
+  // ---- a2-a6 on u8 images on the tensor cores (banded-Toeplitz blur)
+  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 3 && c->d_tctab &&
+      tc_ok(*c->tc, W, H)) {
+    const TcPlan& P = *c->tc;
+    const size_t smem = tc_smem(P);
+    cudaError_t ea = cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ea != cudaSuccess) return cuda_fail(ea, "k_tc attribute");
+    const int64_t ntiles = (int64_t)((W + kTcTile - 1) / kTcTile) * ((H + kTcTile - 1) / kTcTile) * B;
+    dim3 gb((unsigned)std::min<int64_t>(ntiles, c->sms));   // persistent: one CTA per SM
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
+                                                      (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
+                                                      (uint32_t)P.S);
+    k_tc<<<gb, kTcThreads, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B);
+    LAUNCH_CHECK("k_tc");
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
+  }
   // ---- a2-a6 on u8 images, two-CTA band schedule
   if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
       band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
@@ -486,7 +510,10 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     const char* nb = getenv("MHFD_NO_BAND");
     c->band_enabled = !(nb && nb[0] == '1');
     const char* sch = getenv("MHFD_SCHEDULE");
-    c->band_kind = (sch && strcmp(sch, "band2") == 0) ? 2 : 1;
+    c->band_kind = 3;
+    if (sch && strcmp(sch, "band2") == 0) c->band_kind = 2;
+    if (sch && strcmp(sch, "band") == 0) c->band_kind = 1;
+    if (sch && strcmp(sch, "generic") == 0) c->band_enabled = 0;
   }
   LevelTable& T = *c->tab;
   T.nlev = n + 1;
@@ -513,6 +540,29 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     c->t[i] = t[i];
   }
   T.ntaps_total = off;
+  // tensor-core plan and its Toeplitz tables (device copy owned by the context)
+  c->tc = new (std::nothrow) TcPlan;
+  if (c->tc && tc_plan_build(*c->tc, n + 1, R, t)) {
+    std::vector<std::vector<double>> wv(n + 1);
+    for (int i = 0; i <= n; ++i) {
+      double sum = 0.0;
+      for (int d = -R[i]; d <= R[i]; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
+      for (int d = -R[i]; d <= R[i]; ++d) wv[i].push_back(std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum);
+    }
+    std::vector<uint8_t> tabh((size_t)c->tc->tab_bytes);
+    tc_fill_tables(*c->tc, wv, tabh.data());
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(p->device) == cudaSuccess &&
+        cudaMalloc(&c->d_tctab, tabh.size()) == cudaSuccess &&
+        cudaMemcpy(c->d_tctab, tabh.data(), tabh.size(), cudaMemcpyHostToDevice) == cudaSuccess) {
+    } else {
+      if (c->d_tctab) cudaFree(c->d_tctab);
+      c->d_tctab = nullptr;
+      cudaGetLastError();
+    }
+    cudaSetDevice(prev);
+  }
   c->radmax = 0.0;
   for (int s = 0; s < n; ++s) {
     c->rad[s] = std::sqrt(2.0) * t[s];
@@ -585,6 +635,8 @@ void mhfd_destroy(mhfd_ctx* c) {
     cudaStreamDestroy(c->copy_stream);
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
   }
+  if (c->d_tctab) cudaFree(c->d_tctab);
+  delete c->tc;
   delete c->tab;
   delete c;
 }
@@ -646,6 +698,18 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
   }
   g_launches = launches;
   return MHFD_OK;
+}
+
+const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
+  if (!c) return "none";
+  const int W = c->p.width, H = c->p.height;
+  const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  if (dtype == MHFD_U8 && paper && c->band_enabled) {
+    if (c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
+    if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
+    if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
+  }
+  return "k_scale_space";
 }
 
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out) {

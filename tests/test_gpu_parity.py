@@ -74,6 +74,18 @@ def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None):
     gpu_c = P.gpu_rows(dump["cands"][0], min(nc, det.max_candidates))
     assert gpu_c == sorted(gpu_c, key=lambda r: (r[1], r[0], r[2])), "candidate list not in (y, x, scale) order"
     summ = P.compare_candidates(gpu_c, ora_c, amb_xy, tie_xy, eps, nms)
+    if nms == "paper" and img.dtype == np.uint8:
+        # the fused u8 schedule detect/focus_score run (k_tc when the tile fits, else
+        # k_band): v, argmax and candidates without the DoG dump
+        fused = det.debug_dump(_to_t(img), dog=False, cands=True)
+        vf = fused["v"][0].cpu().numpy().astype(np.float64)
+        assert float(np.abs(vf - ref["v"]).max()) <= eps, (det.schedule(), float(np.abs(vf - ref["v"]).max()), eps)
+        iff = fused["idx"][0].cpu().numpy()
+        assert np.array_equal(iff[~tie], ref["idx"][~tie]), det.schedule()
+        ncf = int(fused["ncand"][0])
+        gpu_cf = P.gpu_rows(fused["cands"][0], min(ncf, det.max_candidates))
+        P.compare_candidates(gpu_cf, ora_c, amb_xy, tie_xy, eps, nms)
+        summ["fused_v_err_rel"] = float(np.abs(vf - ref["v"]).max()) / max(Pk, 1e-30)
     # a9-a10: pruned blobs, counts, score
     blobs, cnt, flags = det.detect(_to_t(img))
     scores = det.focus_score(_to_t(img))
@@ -114,6 +126,14 @@ def test_c1_strict(c1_img, strict):
 def test_c2_pair_parity(defocus, bits):
     img = synth.em_tile_np(1024, 1024, 1000, defocus=defocus, dose=300.0, bits=bits)
     _full_parity(img, C3)
+
+
+def test_u8_schedule_is_tensor_core():
+    """The bench configuration (4096^2 u8, sigma 1-10, n 10) and C2 run the tcgen05 kernel."""
+    assert mhfd.Detector(4096, 4096, threshold=0.09, **C3).schedule("u8") == "k_tc"
+    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u8") == "k_tc"
+    assert mhfd.Detector(256, 256, threshold=0.08, **C1).schedule("u8") == "k_tc"
+    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u16") == "k_scale_space"
 
 
 def test_c2_sharp_beats_defocused():
