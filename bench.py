@@ -15,8 +15,8 @@ The 1.07 GB batch per GPU is larger than L2 (126 MB), so no L2 flush is needed.
 Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
 cudaDeviceSynchronize and CUDA events on the launching stream; max over ranks.
 Per-stage device times come from events the library records on the same stream
-(mhfd_timing_*), which gives the dominant kernel's (k_scale_space) duration for
-the roofline.  `e2e` repeats the measurement through mhfd_focus_score_host with the
+(mhfd_timing_*), which gives the dominant kernel's (mhfd_schedule_name) duration for
+the roofline (k_tc, the tcgen05 kernel, by default).  `e2e` repeats the measurement through mhfd_focus_score_host with the
 batch in pinned host memory (H2D copies and the D2H of scores inside the timed
 region).  `cpu_baseline` times the oracle (oracle/, f64, plain C) on rank 0 on a
 bounded sample (a band of rows of one tile).
@@ -190,6 +190,52 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def peaks() -> tuple[dict, str]:
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the fallback
+    of B200_PROFILING.md (6.65 TB/s, 1.59 PF burst / ~1.4 PF sustained)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "of measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "of fallback (B200_PROFILING.md)"
+
+
+def roofline_of(det, B: int, kern_ms: float, step_ms: float) -> dict:
+    """Roofline of the dominant kernel (DESIGN.md §6/§8).  k_tc is bound by the fp16
+    tensor pipe: achieved = the banded formulation's MMA flops per pixel
+    (mhfd_schedule_flops_per_pixel: 2 row-pass and 3 column-pass fp16 products per
+    level, K_i-wide Toeplitz windows) x pixels / launch time, against the sustained
+    cuBLAS bf16 peak (fp16 runs at the bf16 rate: 2.25 PF nominal for both) because the
+    kernel runs inside a long step.  The CUDA-core schedules are FP32-FMA bound.
+    `alu_equivalent` restates the same time against the direct separable blur's FMA
+    count on the FP32 pipe, i.e. how far the kernel is past the CUDA-core ceiling."""
+    pk, pk_note = peaks()
+    name = det.schedule("u8")
+    px = B * SIZE * SIZE
+    fpp = det.schedule_flops_per_pixel("u8")
+    achieved = fpp * px / (kern_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_{name}_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f)["dram_bytes_per_image"] * B
+    alg = alg_flops_per_px()
+    alu = {"alg_flops_per_px": alg, "achieved": alg * px / (kern_ms * 1e-3) / 1e12, "peak": ALU_PEAK_TFLOPS,
+           "unit": "TFLOP/s", "frac": alg * px / (kern_ms * 1e-3) / 1e12 / ALU_PEAK_TFLOPS,
+           "note": "direct separable blur at R_i = ceil(5 t_i) on the FP32 pipe: 148 SMs x 128 FFMA/clk x 2 x "
+                   "1.965 GHz (B200_PROFILING.md unit counts)"}
+    common = {"kernel": name, "traffic": traffic, "kernel_ms_per_launch": kern_ms, "share_of_step": kern_ms / step_ms,
+              "flops_per_px": fpp, "hbm_gbs": px * (1 + 5) / (kern_ms * 1e-3) / 1e9,
+              "hbm_note": f"{name} HBM bytes: 1 B/px read + 5 B/px (v f32 + argmax u8) written"}
+    if name == "k_tc":
+        peak = pk["bf16_tflops_sustained"]
+        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_note": f"fp16 dense tensor = bf16 rate; sustained cuBLAS bf16 {pk_note}",
+                **common, "alu_equivalent": alu}
+    return {"bound": "alu", "achieved": achieved, "peak": ALU_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / ALU_PEAK_TFLOPS, "peak_note": alu["note"], **common}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -263,26 +309,11 @@ def main() -> None:
     px_step = world * B * SIZE * SIZE
     value = px_step / (ms_max * 1e-3) / 1e6
 
-    # dominant kernel: k_scale_space (stage 1), averaged over the timed steps
+    # dominant kernel: the fused a2-a6 kernel (stage 1), averaged over the timed steps
     ss_ms = statistics.mean(s[1] for s in stages)
     stage_ms = {k: statistics.mean(s[i] for s in stages) for i, k in
-                enumerate(["percentiles_a1", "scale_space_a2_a6", "nms_compact_a7_a8", "prune_score_a9_a10"])}
-    flops = alg_flops_per_px() * B * SIZE * SIZE
-    achieved = flops / (ss_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_scale_space_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            t = json.load(f)
-        traffic = t["dram_bytes_per_image"] * B
-    roofline = {"bound": "alu", "kernel": "k_scale_space", "achieved": achieved, "peak": ALU_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / ALU_PEAK_TFLOPS, "traffic": traffic,
-                "alg_flops_per_px": alg_flops_per_px(), "kernel_ms_per_launch": ss_ms,
-                "share_of_step": ss_ms / ms,
-                "peak_note": "derived: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (B200_PROFILING.md); "
-                             "measured FFMA microbenchmark 72.2 TFLOP/s",
-                "hbm_gbs": (B * SIZE * SIZE * (1 + 5)) / (ss_ms * 1e-3) / 1e9,
-                "hbm_note": "k_scale_space HBM bytes: 1 B/px read + 5 B/px (v f32 + argmax u8) written"}
+                enumerate(["percentiles_a1", "blur_dog_argmax_a2_a6", "nms_compact_a7_a8", "prune_score_a9_a10"])}
+    roofline = roofline_of(det, B, ss_ms, ms)
 
     # e2e through the host-buffer C-ABI entry point
     e2e = None

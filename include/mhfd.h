@@ -198,6 +198,14 @@ mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
  * a NULL context. */
 const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype);
 
+/* Floating-point operations per output pixel that the kernel named by
+ * mhfd_schedule_name executes by construction (bench roofline): for "k_tc" the
+ * tensor-core MMA flops of the banded formulation (sum over levels of
+ * 2 x 2*128*K_i^2 + 3 x 2*128*128*K_i per 128 x 128 tile, K_i = the level's
+ * window); otherwise the direct separable blur, 2 x 2(2R_i+1) FMA
+ * per level plus 3 per DoG plane.  0 for a NULL context. */
+double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype);
+
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int32_t mhfd_last_launch_count(void);
 

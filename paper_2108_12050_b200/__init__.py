@@ -193,6 +193,11 @@ class Detector:
         code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16}[dtype]
         return self._lib.mhfd_schedule_name(self._h, code).decode()
 
+    def schedule_flops_per_pixel(self, dtype: str = "u8") -> float:
+        """Flops per pixel the schedule's a2-a6 kernel executes (bench roofline)."""
+        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16}[dtype]
+        return float(self._lib.mhfd_schedule_flops_per_pixel(self._h, code))
+
     @staticmethod
     def last_launch_count() -> int:
         return int(_abi.load().mhfd_last_launch_count())

@@ -21,7 +21,8 @@ MHFD_NMS_PAPER, MHFD_NMS_26 = 0, 1
 EXPORTS = ["mhfd_params_default", "mhfd_create", "mhfd_workspace_bytes", "mhfd_detect_batch",
            "mhfd_focus_score", "mhfd_debug_dump", "mhfd_get_params", "mhfd_last_launch_count",
            "mhfd_destroy", "mhfd_status_string", "mhfd_last_error", "mhfd_abi_version",
-           "mhfd_focus_score_host", "mhfd_timing_enable", "mhfd_timing_read", "mhfd_schedule_name"]
+           "mhfd_focus_score_host", "mhfd_timing_enable", "mhfd_timing_read", "mhfd_schedule_name",
+           "mhfd_schedule_flops_per_pixel"]
 
 
 class mhfd_params(ctypes.Structure):
@@ -67,6 +68,7 @@ def load() -> ctypes.CDLL:
             "mhfd_timing_enable": (i32, [P, i32]),
             "mhfd_timing_read": (i32, [P, P, ctypes.POINTER(i32)]),
             "mhfd_schedule_name": (ctypes.c_char_p, [P, i32]),
+            "mhfd_schedule_flops_per_pixel": (ctypes.c_double, [P, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

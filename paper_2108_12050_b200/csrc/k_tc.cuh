@@ -39,7 +39,7 @@ __host__ __device__ inline int tc_lw(const TcPlan& P) { return (P.S + tc_off(P) 
 __host__ __device__ inline size_t tc_b1_bytes(const TcPlan& P) { return (size_t)P.S * P.S * 2; }
 __host__ __device__ inline size_t tc_land_bytes(const TcPlan& P) { return (size_t)tc_lw(P) * P.S; }
 __host__ __device__ inline size_t tc_smem(const TcPlan& P) {
-  return tc_b1_bytes(P) + tc_land_bytes(P) + 2 * (size_t)P.max_level_bytes + 64;
+  return tc_b1_bytes(P) + tc_land_bytes(P) + 2 * (size_t)P.max_level_bytes + 128;
 }
 inline bool tc_ok(const TcPlan& P, int W, int H) {
   return P.S > 0 && tc_lw(P) <= 256 && tc_smem(P) <= 227 * 1024 && W >= tc_lw(P) && H >= P.S;
@@ -60,7 +60,8 @@ __device__ __forceinline__ TcTile tc_tile(int t, int tx, int ty) {
 // Fetch the raw window of tile tt into `land` (LW x S bytes, row pitch LW): columns
 // x0 - H0 - off .. +LW, rows y0 - H0 .. +S, periodic.  Mode as band_fetch: 2 = TMA box,
 // 1 = bulk copies per row, 0 = plain loads (complete on return).
-__device__ __forceinline__ int tc_fetch(const TcTile& tt, uint8_t* land, uint64_t* bar, const uint8_t* images,
+__device__ __forceinline__ void epi_sync();
+__device__ __forceinline__ int tc_fetch_epi(const TcTile& tt, uint8_t* land, uint64_t* bar, const uint8_t* images,
                                         const Shape& s, const CUtensorMap* tmap, int use_tmap, const TcPlan& P) {
   const int LW = tc_lw(P), S = P.S;
   const int xr = tt.x0 - P.H0 - tc_off(P), yr = tt.y0 - P.H0;
@@ -77,7 +78,7 @@ __device__ __forceinline__ int tc_fetch(const TcTile& tt, uint8_t* land, uint64_
   const uint8_t* img = images + (int64_t)tt.b * s.H * s.pitch;
   if (bulk) {
     if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)(S * LW));
-    __syncthreads();   // expect_tx registered before any copy completes
+    epi_sync();   // expect_tx registered before any copy completes
     const int xw = wrap_idx(xr, s.W);
     for (int r = tid; r < S; r += kTcThreads) {
       const uint8_t* row = img + (int64_t)wrap_idx(yr + r, s.H) * s.pitch;
@@ -99,223 +100,291 @@ __device__ __forceinline__ int tc_fetch(const TcTile& tt, uint8_t* land, uint64_
   return 0;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// raw window (land) -> B1: saturate to [lo, hi], centre on mid, exact fp16; chunk g of
+// 8 pixels lands at B1 + 16 g (canonical K-major: row group, column chunk, row)
+__device__ __forceinline__ void tc_stage_b1(const uint8_t* land, uint8_t* B1, int S, int LW, int OFF, int lo, int hi,
+                                            int mid) {
+  const uint32_t lo2 = (uint32_t)lo * 0x10001u, hi2 = (uint32_t)hi * 0x10001u;
+  const __half2 cm = __floats2half2_rn(1024.f + (float)mid, 1024.f + (float)mid);
+  const int nchunk = S * S / 8, kcs = S / 8;
+  for (int gch = threadIdx.x; gch < nchunk; gch += kTcThreads) {
+    const int cm8 = gch >> 3;
+    const int r = (cm8 / kcs) * 8 + (gch & 7), kc = cm8 % kcs;
+    const uint2 raw = *reinterpret_cast<const uint2*>(land + (size_t)r * LW + OFF + 8 * kc);
+    const uint32_t a = clamp_bytes(raw.x, lo2, hi2), bb = clamp_bytes(raw.y, lo2, hi2);
+    // 0x64pp = fp16 1024 + p exactly; subtracting 1024 + mid leaves the integer p - mid
+    const uint32_t p0 = __byte_perm(a, 0x64646464u, 0x4140u), p1 = __byte_perm(a, 0x64646464u, 0x4342u);
+    const uint32_t p2 = __byte_perm(bb, 0x64646464u, 0x4140u), p3 = __byte_perm(bb, 0x64646464u, 0x4342u);
+    __half2 x0 = __hsub2(*reinterpret_cast<const __half2*>(&p0), cm);
+    __half2 x1 = __hsub2(*reinterpret_cast<const __half2*>(&p1), cm);
+    __half2 x2 = __hsub2(*reinterpret_cast<const __half2*>(&p2), cm);
+    __half2 x3 = __hsub2(*reinterpret_cast<const __half2*>(&p3), cm);
+    uint4 o;
+    o.x = *reinterpret_cast<uint32_t*>(&x0);
+    o.y = *reinterpret_cast<uint32_t*>(&x1);
+    o.z = *reinterpret_cast<uint32_t*>(&x2);
+    o.w = *reinterpret_cast<uint32_t*>(&x3);
+    *reinterpret_cast<uint4*>(B1 + (size_t)gch * 16) = o;
+  }
+}
+
+// D1 chunk j (16 f32 columns of this thread's lane) -> hi fp16 at 16j, lo fp16 at 16j+8
+__device__ __forceinline__ void tc_split_chunk(uint32_t tq, int j) {
+  uint32_t r[16];
+  umma::ld16(tq + 16 * j, r);
+  umma::wait_ld();
+  uint32_t h8[8], l8[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float y0 = __uint_as_float(r[2 * u]) * (1.f / kTcWScale);
+    const float y1 = __uint_as_float(r[2 * u + 1]) * (1.f / kTcWScale);
+    const __half2 hh = __floats2half2_rn(y0, y1);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
+    h8[u] = *reinterpret_cast<const uint32_t*>(&hh);
+    l8[u] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  umma::st8(tq + 16 * j, h8);
+  umma::st8(tq + 16 * j + 8, l8);
+}
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }   // epilogue warps only
+
+
+// Roles: warps 0-15 = epilogue (TMEM lane quarter q = warp & 3, row group wg = warp >> 2):
+// staging, split, DoG; warp 16 = MMA issuer (one lane).
+// TMEM: D1 / A2 columns [0, 256); D2 double buffer [256, 384) and [384, 512) (level
+// parity), so the previous level's L stays in TMEM for the DoG.
+// Barriers (bars[]): 0 land (tx), 1 rowDone, 2 colDone (tcgen05.commit), 3-6 split groups
+// (16 warp arrivals), 7 staged (16), 8/9 table buffers (tx).  Barriers 1-2 complete once
+// per global level g (parity g & 1); 7 once per tile; split group k only on levels with
+// more than 4k chunks (its phase is tracked explicitly).
+//
+// Per level g:
+//   issuer : [tile start: wait staged] wait table g -> row pass (N = K_i, one MMA per
+//            split and K-step) -> commit rowDone; wait colDone(g-1) -> table g+1 prefetch;
+//            for each group of 4 chunks: wait split(grp) -> column K-steps of grp; commit colDone
+//   epilogue: [tile start: stage B1] wait colDone(g-1) -> DoG of level g-1 (D2 buffers);
+//            wait rowDone(g) -> per group: split own chunk -> arrive split(grp)
+// Hazards: row(g) writes D1 after col(g-1) read A2 (in-order tcgen05.mma); col(g) writes
+// D2[g&1] (= L_{g-2}) after every warp's DoG of g-1 (it precedes their split arrivals);
+// B1 is restaged after rowDone of the tile's last level (waited before its split).
+__global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
-     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, int batch) {
+     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, int batch, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int S = P.S, LW = tc_lw(P), OFF = tc_off(P);
   uint8_t* B1 = smem_raw;                                          // S x S fp16, canonical K-major
   uint8_t* land = B1 + tc_b1_bytes(P);                             // LW x S raw bytes
   uint8_t* tbuf = land + tc_land_bytes(P);                         // 2 x max_level_bytes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * (size_t)P.max_level_bytes);   // land, mma, tab0, tab1
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-  uint64_t* bar_land = bars;
-  uint64_t* bar_mma = bars + 1;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * (size_t)P.max_level_bytes);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+  // timeline probe (tools/tc_timeline.cu): CTA 0, first 64 levels, 16 stamps per level
+  unsigned long long* tr = (trace && blockIdx.x == 0) ? trace : nullptr;
+#define TC_STAMP(g, slot) \
+  do { if (tr && (g) < 64) tr[(g) * 16 + (slot)] = clock64(); } while (0)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, wg = warp >> 2;   // TMEM lane quarter, row group
   const int tx = (s.W + kTcTile - 1) / kTcTile, ty = (s.H + kTcTile - 1) / kTcTile;
   const int ntiles = tx * ty * batch;
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
-  const int my_tiles = (ntiles - 1 - t) / gridDim.x + 1;
+  const int t0 = blockIdx.x;
+  if (t0 >= ntiles) return;
+  const int my_tiles = (ntiles - 1 - t0) / gridDim.x + 1;
   const int G = my_tiles * P.nlev;   // levels this CTA processes
   const int SBO1 = (S / 8) * 128;
-  const int64_t plane = (int64_t)s.H * s.W;
 
-  if (tid == 0) {
-    for (int k = 0; k < 4; ++k) mbar_init(&bars[k], 1);
+  if (tid == kTcThreads) {
+    for (int k = 0; k < 10; ++k) mbar_init(&bars[k], (k >= 3 && k <= 7) ? 16 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  const uint32_t tmem = *tslot;            // D1 / A2: columns [0, 256); D2: [256, 384)
-  const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+  const uint32_t tmem = *tslot;
 
-  auto issue_table = [&](int g) {          // thread 0: level table of global level g
-    const int lev = g % P.nlev;
-    const int bytes = 2 * P.lev[lev].npairs * 256;
-    uint64_t* tb = &bars[2 + (g & 1)];
-    mbar_arrive_expect_tx(tb, (uint32_t)bytes);
-    bulk_g2s(tbuf + (size_t)(g & 1) * P.max_level_bytes, tabs + P.lev[lev].tab_off, (uint32_t)bytes, tb);
-  };
-  if (tid == 0) {
-    issue_table(0);
-    if (G > 1) issue_table(1);
-  }
-  TcTile tt = tc_tile(t, tx, ty);
-  int mode = tc_fetch(tt, land, bar_land, images, s, &tmap, use_tmap, P);
-  uint32_t land_phase = 0, mma_phase = 0;
-  int g = 0;
-
-  for (int it = 0;; ++it) {
-    // ---- staged raw window -> B1 (saturate, centre, fp16 exact)
-    if (mode) {
-      mbar_wait(bar_land, land_phase);
-      land_phase ^= 1u;
-    }
-    __syncthreads();
-    const ImgPar ip = par[tt.b];
-    const int lo = ip.lo, hi = ip.hi;
-    const int mid = lo + (hi - lo + 1) / 2;
-    {
-      const uint32_t lo2 = (uint32_t)lo * 0x10001u, hi2 = (uint32_t)hi * 0x10001u;
-      const __half2 cm = __floats2half2_rn(1024.f + (float)mid, 1024.f + (float)mid);
-      const int nchunk = S * S / 8;
-      for (int gch = tid; gch < nchunk; gch += kTcThreads) {
-        const int cm8 = gch >> 3;
-        const int r = (cm8 / (S / 8)) * 8 + (gch & 7), kc = cm8 % (S / 8);
-        const uint2 raw = *reinterpret_cast<const uint2*>(land + (size_t)r * LW + OFF + 8 * kc);
-        const uint32_t a = clamp_bytes(raw.x, lo2, hi2), bb = clamp_bytes(raw.y, lo2, hi2);
-        uint4 o;
-        const uint32_t p0 = __byte_perm(a, 0x64646464u, 0x4140u), p1 = __byte_perm(a, 0x64646464u, 0x4342u);
-        const uint32_t p2 = __byte_perm(bb, 0x64646464u, 0x4140u), p3 = __byte_perm(bb, 0x64646464u, 0x4342u);
-        __half2 x0 = __hsub2(*reinterpret_cast<const __half2*>(&p0), cm);
-        __half2 x1 = __hsub2(*reinterpret_cast<const __half2*>(&p1), cm);
-        __half2 x2 = __hsub2(*reinterpret_cast<const __half2*>(&p2), cm);
-        __half2 x3 = __hsub2(*reinterpret_cast<const __half2*>(&p3), cm);
-        o.x = *reinterpret_cast<uint32_t*>(&x0);
-        o.y = *reinterpret_cast<uint32_t*>(&x1);
-        o.z = *reinterpret_cast<uint32_t*>(&x2);
-        o.w = *reinterpret_cast<uint32_t*>(&x3);
-        *reinterpret_cast<uint4*>(B1 + (size_t)gch * 16) = o;
+  if (warp == kTcThreads / 32) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      auto issue_table = [&](int gg) {
+        const int lev = gg % P.nlev;
+        const int bytes = 2 * P.lev[lev].npairs * 256;
+        uint64_t* tb = &bars[8 + (gg & 1)];
+        mbar_arrive_expect_tx(tb, (uint32_t)bytes);
+        bulk_g2s(tbuf + (size_t)(gg & 1) * P.max_level_bytes, tabs + P.lev[lev].tab_off, (uint32_t)bytes, tb);
+      };
+      issue_table(0);
+      if (G > 1) issue_table(1);
+      int tile_i = 0;
+      uint32_t sph = 0;   // phase bits of the split barriers (group 3 is not used on every level)
+      for (int g = 0; g < G; ++g) {
+        const int lev = g % P.nlev;
+        TC_STAMP(g, 0);
+        if (lev == 0) mbar_wait(&bars[7], (uint32_t)(tile_i++ & 1));
+        mbar_wait(&bars[8 + (g & 1)], (uint32_t)((g >> 1) & 1));
+        umma::fence_after();
+        TC_STAMP(g, 1);
+        const TcLevel& L = P.lev[lev];
+        const int K = L.K, E1 = K / 8 - 2, nj = K / 16;
+        const uint32_t thi = umma::smem_addr(tbuf + (size_t)(g & 1) * P.max_level_bytes);
+        const uint32_t tlo = thi + L.npairs * 256;
+        const uint32_t b1 = umma::smem_addr(B1) + (L.c0 / 8) * SBO1 + (L.c0 / 8) * 128;
+        const uint32_t idr = umma::idesc_f16(128, K), idc = umma::idesc_f16(128, 128);
+        // K-step j: B1 window +256 B (start field +16), Toeplitz pairs -512 B (field -32)
+        const uint64_t dB = umma::desc_kmajor(b1, 128, SBO1);
+        const uint64_t dH = umma::desc_kmajor(thi + E1 * 256, 128, 256);
+        const uint64_t dL = umma::desc_kmajor(tlo + E1 * 256, 128, 256);
+        // row pass of level g.  No wait for the previous column pass: tcgen05.mma from one
+        // thread execute in issue order, so these writes of D1 follow its reads of A2.
+        for (int j = 0; j < nj; ++j) {
+          umma::mma_ss(tmem, dH - 32u * j, dB + 16u * j, idr, j > 0);
+          umma::mma_ss(tmem, dL - 32u * j, dB + 16u * j, idr, 1);
+        }
+        umma::commit(&bars[1]);
+        TC_STAMP(g, 2);
+        if (g > 0) {
+          mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));   // column pass g-1 done: table buffer free
+          if (g + 1 < G) issue_table(g + 1);
+        }
+        const uint32_t d2 = tmem + 256 + 128 * (g & 1);
+        for (int grp = 0; 4 * grp < nj; ++grp) {
+          mbar_wait(&bars[3 + grp], (sph >> grp) & 1u);
+          sph ^= 1u << grp;
+          umma::fence_after();
+          TC_STAMP(g, 3 + grp);
+          for (int j = 4 * grp; j < nj && j < 4 * grp + 4; ++j) {
+            umma::mma_ts(d2, tmem + 16 * j, dH - 32u * j, idc, j > 0);
+            umma::mma_ts(d2, tmem + 16 * j, dL - 32u * j, idc, 1);
+            umma::mma_ts(d2, tmem + 16 * j + 8, dH - 32u * j, idc, 1);
+          }
+        }
+        umma::commit(&bars[2]);
+        TC_STAMP(g, 7);
       }
     }
-    umma::fence_async_smem();
-    __syncthreads();   // B1 ready (async proxy), landing free
-    const int tn = t + gridDim.x;
-    TcTile tn_t;
-    int mode_n = 0;
-    if (tn < ntiles) {
-      tn_t = tc_tile(tn, tx, ty);
-      mode_n = tc_fetch(tn_t, land, bar_land, images, s, &tmap, use_tmap, P);
-    }
-
-    const float inv = ip.inv * (1.f / kTcWScale);
-    float lprev[32], vbest[32];
+    __syncwarp();
+  } else {
+    // ================= epilogue warps =================
+    const int q = warp & 3, wg = warp >> 2;
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+    const int64_t plane = (int64_t)s.H * s.W;
+    int t = t0;
+    TcTile tt = tc_tile(t, tx, ty);
+    int mode = tc_fetch_epi(tt, land, &bars[0], images, s, &tmap, use_tmap, P);
+    uint32_t land_phase = 0;
+    TcTile ot = tt;
+    float oinv = 0.f;
+    int odeg = 0;
+    float vbest[32];
     uint32_t ibest[8];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) { lprev[u] = 0.f; vbest[u] = -INFINITY; }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) ibest[u] = 0u;
 
-    // DoG epilogue of level `lev` (D2 holds L_lev): rows 32 wg .. +32 of column c = 32 q + lane
-    auto consume = [&](int lev) {
-      uint32_t r0[16], r1[16];
-      umma::ld16(tq + 256 + 32 * wg, r0);
-      umma::ld16(tq + 256 + 32 * wg + 16, r1);
-      umma::wait_ld();
-      const float tf = lev > 0 ? P.lev[lev - 1].tdog * inv : 0.f;
+    auto consume = [&](int gg) {   // DoG plane lev-1 from L_lev (D2[gg&1]) and L_{lev-1} (D2[(gg-1)&1])
+      const int lev = gg % P.nlev;
+      if (lev == 0) return;
+      const float tf = P.lev[lev - 1].tdog * oinv;
+      const uint32_t cur = tq + 256 + 128 * (gg & 1) + 32 * wg, prv = tq + 256 + 128 * ((gg - 1) & 1) + 32 * wg;
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const float L = __uint_as_float(u < 16 ? r0[u] : r1[u - 16]);
-        if (lev > 0) {
-          const float D = tf * (L - lprev[u]);
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        uint32_t a[16], b[16];
+        umma::ld16(cur + 16 * hlf, a);
+        umma::ld16(prv + 16 * hlf, b);
+        umma::wait_ld();
+#pragma unroll
+        for (int uu = 0; uu < 16; ++uu) {
+          const int u = 16 * hlf + uu;
+          const float D = tf * (__uint_as_float(a[uu]) - __uint_as_float(b[uu]));
           if (D > vbest[u]) {
             vbest[u] = D;
             const int sh = (u & 3) * 8;
             ibest[u >> 2] = (ibest[u >> 2] & ~(0xffu << sh)) | ((uint32_t)(lev - 1) << sh);
           }
         }
-        lprev[u] = L;
+      }
+    };
+    auto write_out = [&]() {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
+      const int x = ot.x0 + 32 * q + lane;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int y = ot.y0 + 32 * wg + u;
+        if (x < s.W && y < s.H) {
+          const int64_t pidx = (int64_t)ot.b * plane + (int64_t)y * s.W + x;
+          v_out[pidx] = odeg ? 0.f : vbest[u];
+          idx_out[pidx] = odeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+        }
       }
     };
 
-    for (int lev = 0; lev < P.nlev; ++lev, ++g) {
-      const TcLevel& L = P.lev[lev];
-      const int K = L.K;
-      const int npairs = L.npairs, E1 = K / 8 - 2;
-      const uint32_t thi = umma::smem_addr(tbuf + (size_t)(g & 1) * P.max_level_bytes);
-      const uint32_t tlo = thi + npairs * 256;
-      // ---- row pass (thread 0 issues)
-      if (tid == 0) {
-        mbar_wait(&bars[2 + (g & 1)], (uint32_t)((g >> 1) & 1));
-        umma::fence_after();
-        const uint32_t b1 = umma::smem_addr(B1) + (L.c0 / 8) * SBO1 + (L.c0 / 8) * 128;
-        const uint32_t id = umma::idesc_f16(128, K);
-        for (int j = 0; j < K / 16; ++j) {
-          const uint64_t bd = umma::desc_kmajor(b1 + 256 * j, 128, SBO1);
-          umma::mma_ss(tmem, umma::desc_kmajor(thi + (E1 - 2 * j) * 256, 128, 256), bd, id, j > 0);
-          umma::mma_ss(tmem, umma::desc_kmajor(tlo + (E1 - 2 * j) * 256, 128, 256), bd, id, 1);
+    if (tid != 0) tr = nullptr;
+    for (int g = 0; g < G; ++g) {
+      const int lev = g % P.nlev;
+      const uint32_t par_g = (uint32_t)(g & 1);
+      TC_STAMP(g, 8);
+      if (lev == 0) {
+        // ---- stage tile tt (rowDone of the previous tile's last level was waited below)
+        if (mode) {
+          mbar_wait(&bars[0], land_phase);
+          land_phase ^= 1u;
         }
-        umma::commit(bar_mma);
-      }
-      // ---- previous level's DoG epilogue overlaps the row pass
-      if (lev > 0) consume(lev - 1);
-      mbar_wait(bar_mma, mma_phase);
-      mma_phase ^= 1u;
-      umma::fence_after();
-      // ---- split D1 -> (hi, lo) fp16 in place: chunk j = 16 columns -> hi at 16j, lo at 16j+8
-      for (int j = wg; j < K / 16; j += 4) {
-        uint32_t r[16];
-        umma::ld16(tq + 16 * j, r);
-        umma::wait_ld();
-        uint32_t h8[8], l8[8];
+        epi_sync();
+        const ImgPar ip = par[tt.b];
+        tc_stage_b1(land, B1, S, LW, OFF, ip.lo, ip.hi, ip.lo + (ip.hi - ip.lo + 1) / 2);
+        umma::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&bars[7]);
+        epi_sync();   // landing zone free
+        const int tn = t + gridDim.x;
+        if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty), land, &bars[0], images, s, &tmap, use_tmap, P);
+        // ---- DoG of the previous tile's last level, then its output
+        if (g > 0) {
+          mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
+          umma::fence_after();
+          consume(g - 1);
+          write_out();
+        }
+        ot = tt;
+        oinv = ip.inv * (1.f / kTcWScale);
+        odeg = ip.degen;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float y0 = __uint_as_float(r[2 * u]) * (1.f / kTcWScale);
-          const float y1 = __uint_as_float(r[2 * u + 1]) * (1.f / kTcWScale);
-          const __half2 hh = __floats2half2_rn(y0, y1);
-          const float2 hf = __half22float2(hh);
-          const __half2 ll = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
-          h8[u] = *reinterpret_cast<const uint32_t*>(&hh);
-          l8[u] = *reinterpret_cast<const uint32_t*>(&ll);
-        }
-        umma::st8(tq + 16 * j, h8);
-        umma::st8(tq + 16 * j + 8, l8);
-      }
-      umma::wait_st();
-      umma::fence_before();
-      __syncthreads();
-      // ---- column pass (thread 0 issues)
-      if (tid == 0) {
-        umma::fence_after();
-        const uint32_t id = umma::idesc_f16(128, 128);
-        for (int j = 0; j < K / 16; ++j) {
-          const uint64_t bh = umma::desc_kmajor(thi + (E1 - 2 * j) * 256, 128, 256);
-          const uint64_t bl = umma::desc_kmajor(tlo + (E1 - 2 * j) * 256, 128, 256);
-          umma::mma_ts(tmem + 256, tmem + 16 * j, bh, id, j > 0);
-          umma::mma_ts(tmem + 256, tmem + 16 * j, bl, id, 1);
-          umma::mma_ts(tmem + 256, tmem + 16 * j + 8, bh, id, 1);
-        }
-        umma::commit(bar_mma);
-      }
-      mbar_wait(bar_mma, mma_phase);
-      mma_phase ^= 1u;
-      umma::fence_after();
-      // table buffer (g & 1) is free: prefetch level g + 2
-      if (tid == 0 && g + 2 < G) issue_table(g + 2);
-    }
-    consume(P.nlev - 1);
-    umma::fence_before();   // TMEM reads done before the next tile's MMAs (after the barrier below)
-
-    // ---- v and argmax of column c, rows 32 wg .. +32
-    {
-      const int x = tt.x0 + 32 * q + lane;
-      const bool degen = ip.degen != 0;
+        for (int u = 0; u < 32; ++u) vbest[u] = -INFINITY;
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int y = tt.y0 + 32 * wg + u;
-        if (x < s.W && y < s.H) {
-          const int64_t pidx = (int64_t)tt.b * plane + (int64_t)y * s.W + x;
-          v_out[pidx] = degen ? 0.f : vbest[u];
-          idx_out[pidx] = degen ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
-        }
+        for (int u = 0; u < 8; ++u) ibest[u] = 0u;
+        if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty); }
+      } else {
+        mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
+        umma::fence_after();
+        TC_STAMP(g, 9);
+        consume(g - 1);
+      }
+      TC_STAMP(g, 10);
+      // ---- split D1 -> A2 group by group (chunk 4 grp + wg of this warp's lane quarter)
+      const int nj = P.lev[lev].K / 16;
+      mbar_wait(&bars[1], par_g);
+      umma::fence_after();
+      TC_STAMP(g, 11);
+      for (int grp = 0; 4 * grp < nj; ++grp) {
+        const int j = 4 * grp + wg;
+        if (j < nj) tc_split_chunk(tq, j);
+        umma::wait_st();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&bars[3 + grp]);
+        TC_STAMP(g, 12 + grp);
       }
     }
-    if (tn >= ntiles) break;
-    t = tn;
-    tt = tn_t;
-    mode = mode_n;
-    __syncthreads();
+    mbar_wait(&bars[2], (uint32_t)((G - 1) & 1));
     umma::fence_after();
+    consume(G - 1);
+    write_out();
   }
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 512);
+#undef TC_STAMP
 }
 
 }  // namespace mhfd

@@ -276,7 +276,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
                                                       (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
                                                       (uint32_t)P.S);
-    k_tc<<<gb, kTcThreads, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B);
+    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B, nullptr);
     LAUNCH_CHECK("k_tc");
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
@@ -710,6 +710,23 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
   return "k_scale_space";
+}
+
+double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {
+  if (!c) return 0.0;
+  const char* name = mhfd_schedule_name(c, dtype);
+  if (strcmp(name, "k_tc") == 0) {   // banded products per 128 x 128 tile: 2 row splits, 3 column splits
+    const TcPlan& P = *c->tc;
+    double macs = 0.0;
+    for (int i = 0; i < P.nlev; ++i) {
+      const double K = P.lev[i].K;
+      macs += 2.0 * kTcTile * K * K + 3.0 * kTcTile * kTcTile * K;
+    }
+    return 2.0 * macs / ((double)kTcTile * kTcTile);
+  }
+  double f = 0.0;   // direct separable blur at R_i: 2 passes x (2R_i+1) FMA per level, + DoG/max
+  for (int i = 0; i <= c->n; ++i) f += 2.0 * 2.0 * (2.0 * c->tab->R[i] + 1.0);
+  return f + 3.0 * c->n;
 }
 
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out) {
