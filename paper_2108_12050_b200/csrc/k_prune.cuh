@@ -38,6 +38,9 @@ struct PruneArgs {
   int prune;                // overlap < 1
   double radmax;
   double rad[kMaxLevels];   // sqrt(2) * t_s
+  int32_t dmax[kMaxLevels]; // search radius of a plane-s blob: ceil(sqrt(max_{s'>=s} thr_hi(s, s')))
+  const float2* thr;        // n x n squared-distance band (lo, hi) of frac > overlap (host bisection)
+  int n;                    // DoG planes
   uint8_t* st;              // B x cap
   int32_t* rowstart;        // B x (H + 1): first candidate of each row
   int32_t* rbi;             // B x H x (nbx + 1): first candidate of row y with x >= 32 k
@@ -82,7 +85,8 @@ __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
   const uint8_t* st = a.st + (int64_t)b * a.cap;
   const mhfd_blob me = C[k];
   const double r = a.rad[me.scale];
-  const int Dm = (int)ceil(r + a.radmax);
+  const int Dm = a.dmax[me.scale];
+  const float2* th = a.thr + me.scale * a.n;
   bool blocked = false;
   const int ylo = max(0, me.y - Dm), yhi = min(a.H - 1, me.y + Dm);
   const int kb0 = max(0, me.x - Dm) >> 5, kb1 = min(a.nbx, ((me.x + Dm) >> 5) + 1);
@@ -98,8 +102,15 @@ __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
       const bool higher = o.scale > me.scale ||
                           (o.scale == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
       if (!higher) continue;
-      const double dx = (double)(o.x - me.x), dy = (double)(o.y - me.y);
-      if (lens_fraction(sqrt(dx * dx + dy * dy), r, a.rad[o.scale]) > a.overlap) {
+      // frac(d) > overlap, frac decreasing in d: d^2 < lo -> yes, d^2 >= hi -> no, else
+      // evaluate the lens formula (the band is 1e-6 relative around the bisected root)
+      const int dx = o.x - me.x, dy = o.y - me.y;
+      const float d2 = (float)(dx * dx + dy * dy);
+      const float2 t2 = __ldg(th + o.scale);
+      const bool over = d2 < t2.x ? true
+                        : d2 >= t2.y ? false
+                                     : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.scale]) > a.overlap;
+      if (over) {
         const uint8_t s = __ldcg(st + q);
         if (s == kKept) return kRemoved;
         if (s == kUndecided) blocked = true;
@@ -135,40 +146,38 @@ __global__ void __launch_bounds__(256) k_prune(PruneArgs a) {
   const int64_t total = a.img_off[a.B];
   const int64_t nchunks = a.chunk_off[a.B];
 
-  // phase 1: row index (lower bound of each row in the raster-sorted list), init states
-  for (int64_t g = gtid; g < (int64_t)a.B * (a.H + 1); g += gsize) {
-    const int b = (int)(g / (a.H + 1));
-    const int y = (int)(g - (int64_t)b * (a.H + 1));
+  // phase 1: row index rowstart[b][y] (first candidate of row >= y) and row-block index
+  // rbi[b][y][k] (first candidate of row y with x >= 32 k; k = nbx -> row end), both by
+  // scatter from the raster-sorted list: candidate k (and a sentinel k = n at row H)
+  // owns the entries between its predecessor and itself, so each entry is written once.
+  for (int64_t g = gtid; g < total + a.B; g += gsize) {
+    // g enumerates, per image, candidates 0..n (n = sentinel): image b holds entries
+    // [img_off[b] + b, img_off[b+1] + b + 1)
+    int lo = 0, hi = a.B;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.img_off[mid] + mid <= g) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const int64_t k = g - a.img_off[b] - b;
     const int64_t n = a.img_off[b + 1] - a.img_off[b];
     const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (C[mid].y < y) lo = mid + 1; else hi = mid;
+    int y, x, yp, xp;
+    if (k < n) { const mhfd_blob m = C[k]; y = m.y; x = m.x; } else { y = a.H; x = 0; }
+    if (k > 0) { const mhfd_blob m = C[k - 1]; yp = m.y; xp = m.x; } else { yp = -1; xp = 0; }
+    int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
+    for (int yy = yp + 1; yy <= y; ++yy) rs[yy] = (int32_t)k;
+    if (k < n) a.st[(int64_t)b * a.cap + k] = a.prune ? kUndecided : kKept;
+    if (!a.prune) continue;
+    int32_t* ri = a.rbi + (int64_t)b * a.H * (a.nbx + 1);
+    if (yp >= 0 && yp < y) {   // predecessor ends its row: its trailing blocks point past it
+      for (int kb = (xp >> 5) + 1; kb <= a.nbx; ++kb) ri[(int64_t)yp * (a.nbx + 1) + kb] = (int32_t)k;
     }
-    a.rowstart[g] = (int32_t)lo;
-  }
-  for (int64_t g = gtid; g < total; g += gsize) {
-    const int b = image_of(a.img_off, a.B, g);
-    a.st[(int64_t)b * a.cap + (g - a.img_off[b])] = a.prune ? kUndecided : kKept;
-  }
-  grid.sync();
-  // row-block index: first candidate of row y with x >= 32 k, k = 0 .. nbx
-  if (a.prune) {
-    const int64_t per_img = (int64_t)a.H * (a.nbx + 1);
-    for (int64_t g = gtid; g < (int64_t)a.B * per_img; g += gsize) {
-      const int b = (int)(g / per_img);
-      const int64_t rem = g - (int64_t)b * per_img;
-      const int y = (int)(rem / (a.nbx + 1));
-      const int kb = (int)(rem - (int64_t)y * (a.nbx + 1));
-      const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
-      int lo = a.rowstart[(int64_t)b * (a.H + 1) + y], hi = a.rowstart[(int64_t)b * (a.H + 1) + y + 1];
-      const int xk = 32 * kb;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (C[mid].x < xk) lo = mid + 1; else hi = mid;
-      }
-      a.rbi[g] = lo;
+    for (int yy = yp + 1; yy < y && yy < a.H; ++yy)   // empty rows in between
+      for (int kb = 0; kb <= a.nbx; ++kb) ri[(int64_t)yy * (a.nbx + 1) + kb] = (int32_t)k;
+    if (k < n) {   // blocks of row y whose first candidate is k
+      const int kb0 = (yp == y) ? (xp >> 5) + 1 : 0;
+      for (int kb = kb0; kb <= (x >> 5); ++kb) ri[(int64_t)y * (a.nbx + 1) + kb] = (int32_t)k;
     }
   }
   grid.sync();

@@ -47,6 +47,8 @@ struct mhfd_ctx {
   int band_kind;     // 3 = k_tc (default), 1 = k_band, 2 = k_band2; MHFD_SCHEDULE=tc|band|band2|generic
   TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
   uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
+  float2* d_thr;     // pruning: n x n squared-distance bands (context-owned, immutable)
+  int32_t dmax[kMaxLevels];
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
   cudaEvent_t* tev;
   int tmax, tcount;
@@ -383,6 +385,9 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   pa.prune = c->p.overlap < 1.0f ? 1 : 0;
   pa.radmax = c->radmax;
   for (int s = 0; s < c->n; ++s) pa.rad[s] = c->rad[s];
+  for (int s = 0; s < c->n; ++s) pa.dmax[s] = c->dmax[s];
+  pa.thr = c->d_thr;
+  pa.n = c->n;
   pa.st = reinterpret_cast<uint8_t*>(ws + L.st);
   pa.rowstart = reinterpret_cast<int32_t*>(ws + L.rowstart);
   pa.rbi = reinterpret_cast<int32_t*>(ws + L.rbi);
@@ -558,6 +563,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
         cudaMemcpy(c->d_tctab, tabh.data(), tabh.size(), cudaMemcpyHostToDevice) == cudaSuccess) {
     } else {
       if (c->d_tctab) cudaFree(c->d_tctab);
+  if (c->d_thr) cudaFree(c->d_thr);
       c->d_tctab = nullptr;
       cudaGetLastError();
     }
@@ -567,6 +573,53 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   for (int s = 0; s < n; ++s) {
     c->rad[s] = std::sqrt(2.0) * t[s];
     c->radmax = std::max(c->radmax, c->rad[s]);
+  }
+  // pruning thresholds: frac(d; r1, r2) (lens area / smaller disk) decreases in d, so
+  // frac > overlap <=> d < d*(r1, r2); bisect d* in f64 and keep a 1e-6 band around d*^2
+  // inside which the kernel evaluates the formula itself
+  {
+    std::vector<float2> thr((size_t)n * n);
+    auto frac = [](double d, double r1, double r2) {
+      const double rmin = std::min(r1, r2);
+      if (d >= r1 + r2) return 0.0;
+      if (d <= std::fabs(r1 - r2)) return 1.0;
+      double a1 = (d * d + r1 * r1 - r2 * r2) / (2.0 * d * r1), a2 = (d * d + r2 * r2 - r1 * r1) / (2.0 * d * r2);
+      a1 = std::min(1.0, std::max(-1.0, a1));
+      a2 = std::min(1.0, std::max(-1.0, a2));
+      double k = (-d + r1 + r2) * (d + r1 - r2) * (d - r1 + r2) * (d + r1 + r2);
+      k = std::max(k, 0.0);
+      return (r1 * r1 * std::acos(a1) + r2 * r2 * std::acos(a2) - 0.5 * std::sqrt(k)) / (M_PI * rmin * rmin);
+    };
+    for (int s1 = 0; s1 < n; ++s1) {
+      double hmax = 0.0;
+      for (int s2 = 0; s2 < n; ++s2) {
+        const double r1 = c->rad[s1], r2 = c->rad[s2];
+        double lo2 = -1.0, hi2 = -1.0;   // overlap >= 1: frac > overlap never holds
+        if (p->overlap < 1.0f) {
+          double a = 0.0, b = r1 + r2;   // frac(a) > overlap (>= 1 > overlap at containment), frac(b) = 0
+          if (!(frac(a, r1, r2) > (double)p->overlap)) b = 0.0;
+          for (int it = 0; it < 200 && b > 0.0; ++it) {
+            const double m = 0.5 * (a + b);
+            if (frac(m, r1, r2) > (double)p->overlap) a = m; else b = m;
+          }
+          lo2 = b * b * (1.0 - 1e-6) - 1e-6;
+          hi2 = b * b * (1.0 + 1e-6) + 1e-6;
+        }
+        thr[(size_t)s1 * n + s2] = make_float2((float)lo2, (float)hi2);
+        if (s2 >= s1) hmax = std::max(hmax, hi2);
+      }
+      c->dmax[s1] = hmax > 0.0 ? (int)std::ceil(std::sqrt(hmax)) + 1 : 0;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(p->device) != cudaSuccess || cudaMalloc(&c->d_thr, sizeof(float2) * thr.size()) != cudaSuccess ||
+        cudaMemcpy(c->d_thr, thr.data(), sizeof(float2) * thr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      cudaSetDevice(prev);
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_CUDA, "pruning threshold table upload failed");
+    }
+    cudaSetDevice(prev);
   }
   const int64_t half = (int64_t)((p->width + 1) / 2) * ((p->height + 1) / 2);
   c->cap = p->max_candidates > 0 ? p->max_candidates : (p->nms == MHFD_NMS_PAPER ? half : half * n);
@@ -636,6 +689,7 @@ void mhfd_destroy(mhfd_ctx* c) {
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
   }
   if (c->d_tctab) cudaFree(c->d_tctab);
+  if (c->d_thr) cudaFree(c->d_thr);
   delete c->tc;
   delete c->tab;
   delete c;

@@ -66,7 +66,7 @@ for r in data:
     tot += w
 src_cache = {}
 print(f"total samples {tot}")
-for key, w in agg_s.most_common(30):
+for key, w in agg_s.most_common(int(os.environ.get("TOPN", "30"))):
     fn, line = key
     text = ""
     for cand in (os.path.join(ROOT, "paper_2108_12050_b200/csrc", fn),):
