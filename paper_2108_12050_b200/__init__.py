@@ -9,6 +9,7 @@ without a CUDA device the context cannot be created and the calls raise.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -40,7 +41,11 @@ class Detector:
     def __init__(self, width: int, height: int, min_sigma: float = 1.0, max_sigma: float = 10.0,
                  num_scales: int = 10, threshold: float | None = None, overlap: float = 0.5,
                  sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
-                 strict: bool = False, device: int | None = None, max_candidates: int = 0):
+                 strict: bool = False, device: int | None = None, max_candidates: int = 0,
+                 schedule: str | None = None):
+        """schedule: None (library default: k_tc for u8 where the tile fits) or one of
+        "tc", "band", "band2", "generic" — forwarded as MHFD_SCHEDULE, which the library
+        reads once in mhfd_create."""
         lib = _abi.load()
         if device is None:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
@@ -52,7 +57,19 @@ class Detector:
                               nms={"paper": _abi.MHFD_NMS_PAPER, "26": _abi.MHFD_NMS_26}[str(nms)],
                               strict=int(bool(strict)), device=int(device), max_candidates=int(max_candidates))
         h = ctypes.c_void_p()
-        _abi.check(lib.mhfd_create(ctypes.byref(self.params), ctypes.byref(h)))
+        if schedule is not None and schedule not in ("tc", "band", "band2", "generic"):
+            raise ValueError(f"unknown schedule {schedule!r}")
+        saved = os.environ.get("MHFD_SCHEDULE")
+        try:
+            if schedule is not None:
+                os.environ["MHFD_SCHEDULE"] = schedule
+            _abi.check(lib.mhfd_create(ctypes.byref(self.params), ctypes.byref(h)))
+        finally:
+            if schedule is not None:
+                if saved is None:
+                    os.environ.pop("MHFD_SCHEDULE", None)
+                else:
+                    os.environ["MHFD_SCHEDULE"] = saved
         self._h = h
         self._lib = lib
         got = mhfd_params()

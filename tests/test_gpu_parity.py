@@ -35,13 +35,13 @@ def _to_t(img):
     return t
 
 
-def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None):
+def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None):
     """Full comparison on one image: percentiles, DoG stack, v/argmax, candidates,
     pruned blobs, counts and score."""
     H, W = img.shape
     tau = _tau(cfg) if tau is None else tau
     n = cfg["num_scales"]
-    det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, **cfg)
+    det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, schedule=schedule, **cfg)
     dump = det.debug_dump(_to_t(img))
     ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True)
     # a1: percentiles, exact integers
@@ -126,6 +126,15 @@ def test_c1_strict(c1_img, strict):
 def test_c2_pair_parity(defocus, bits):
     img = synth.em_tile_np(1024, 1024, 1000, defocus=defocus, dose=300.0, bits=bits)
     _full_parity(img, C3)
+
+
+@pytest.mark.parametrize("schedule", ["band", "band2", "generic"])
+def test_c2_cuda_core_schedules(schedule):
+    """The CUDA-core schedules (selectable fallbacks of k_tc) against the oracle."""
+    img = synth.em_tile_np(1024, 1024, 1000, defocus=0.0, dose=300.0, bits=8)
+    det = mhfd.Detector(1024, 1024, threshold=0.09, schedule=schedule, **C3)
+    assert det.schedule("u8") == {"band": "k_band", "band2": "k_band2", "generic": "k_scale_space"}[schedule]
+    _full_parity(img, C3, schedule=schedule)
 
 
 def test_u8_schedule_is_tensor_core():
