@@ -198,8 +198,9 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
   dim3 gn((nseg + 7) / 8, B);
   const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
+  const dim3 gr((((H + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // k_nms_rows: kNmsRows segments per warp
   if (rows_fast) {
-    k_nms_rows<false><<<gn, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0);
+    k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0);
   } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
   } else {
@@ -209,7 +210,7 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
   LAUNCH_CHECK("k_seg_scan");
   if (rows_fast) {
-    k_nms_rows<true><<<gn, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap);
+    k_nms_rows<true><<<gr, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap);
   } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {
