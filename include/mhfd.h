@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define MHFD_ABI_VERSION 1
+#define MHFD_ABI_VERSION 2
 
 typedef struct mhfd_ctx mhfd_ctx; /* opaque, immutable after mhfd_create */
 
@@ -69,6 +69,13 @@ typedef enum {
 } mhfd_status;
 
 typedef enum { MHFD_U8 = 1, MHFD_U16 = 2 } mhfd_dtype;
+
+/* Feature polarity (reading R5).  MHFD_DARK: Eq. 2 as written,
+ * DoG_i = t_i (L_{i+1} - L_i), dark blobs on a bright background respond positively
+ * (the paper's EM sections).  MHFD_BRIGHT: DoG_i = -t_i (L_{i+1} - L_i), bright blobs
+ * on a dark background; equivalent to MHFD_DARK on the inverted image 255 - I
+ * (65535 - I for u16) up to rounding. */
+typedef enum { MHFD_DARK = 0, MHFD_BRIGHT = 1 } mhfd_polarity;
 
 typedef enum {
   MHFD_NMS_PAPER = 0, /* Eq. 3: global argmax over scale, 3x3 local max in space (default) */
@@ -97,6 +104,8 @@ typedef struct {
   int32_t max_candidates; /* per-image candidate capacity before pruning;
                              0 = default ceil(W/2)*ceil(H/2) (PAPER mode) or
                              n*ceil(W/2)*ceil(H/2) (26 mode)                         */
+  int32_t polarity;       /* mhfd_polarity (ABI 2; a struct_size without this field
+                             reads as MHFD_DARK)                                     */
 } mhfd_params;
 
 /* One detected feature (x^_j, y^_j, i^_j) of Eq. 3 and its DoG

@@ -74,6 +74,8 @@ def _load():
                 "oracle_prune": (i64, [P, i64, f64, f64, i32, f64, P]),
                 "oracle_detect": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32,
                                         P, i64, P, P, P, P, P, P]),
+                "oracle_detect_pol": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
+                                            P, i64, P, P, P, P, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(lib, name)
@@ -221,8 +223,9 @@ def prune(blobs: np.ndarray, min_t: float, max_t: float, n: int, overlap: float)
 
 def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, overlap: float,
            sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
-           strict: bool = False, dump: bool = False) -> dict:
-    """Algorithm 1 + threshold + pruning; returns blobs, count, candidates."""
+           strict: bool = False, dump: bool = False, polarity: str = "dark") -> dict:
+    """Algorithm 1 + threshold + pruning; returns blobs, count, candidates.
+    polarity "bright" negates the Eq. 2 response (not in the paper)."""
     img, bpp = _img(img)
     H, W = img.shape
     mode = {"paper": 0, "26": 1}[str(nms)]
@@ -233,9 +236,10 @@ def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, over
     D = np.empty((n, H, W), np.float64) if dump else None
     v = np.empty((H, W), np.float64) if (dump and mode == 0) else None
     idx = np.empty((H, W), np.int32) if (dump and mode == 0) else None
-    k = _load().oracle_detect(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
-                              mode, int(strict), _ptr(out), cap, ctypes.byref(ncand),
-                              _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
+    pol = {"dark": 0, "bright": 1}[str(polarity)]
+    k = _load().oracle_detect_pol(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
+                                  mode, int(strict), pol, _ptr(out), cap, ctypes.byref(ncand),
+                                  _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
     if k < 0:
         raise MemoryError("oracle_detect failed")
     res = {"blobs": out[:k].copy(), "count": int(k), "n_candidates": int(ncand.value),

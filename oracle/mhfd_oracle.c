@@ -390,12 +390,12 @@ int64_t oracle_prune(const oracle_blob* c, int64_t nc, double min_t, double max_
  * order; *n_cand receives the candidate count before pruning; D_dump
  * (nullable) receives the n DoG planes; v_dump/idx_dump (nullable) the
  * Eq. 3 inner argmax.  Returns -1 on allocation failure.                 */
-int64_t oracle_detect(const void* img, int bytes_per_px, int H, int W,
-                      double min_t, double max_t, int n, double tau, double overlap,
-                      double sat_low, double sat_high, int nms, int strict,
-                      oracle_blob* out, int64_t cap, int64_t* n_cand,
-                      double* D_dump, double* v_dump, int32_t* idx_dump,
-                      int64_t* lo_out, int64_t* hi_out) {
+int64_t oracle_detect_pol(const void* img, int bytes_per_px, int H, int W,
+                          double min_t, double max_t, int n, double tau, double overlap,
+                          double sat_low, double sat_high, int nms, int strict, int polarity,
+                          oracle_blob* out, int64_t cap, int64_t* n_cand,
+                          double* D_dump, double* v_dump, int32_t* idx_dump,
+                          int64_t* lo_out, int64_t* hi_out) {
   int64_t plane = (int64_t)H * W;
   int64_t lo, hi;
   if (oracle_percentiles(img, bytes_per_px, plane, sat_low, sat_high, &lo, &hi) != 0) return -1;
@@ -406,6 +406,10 @@ int64_t oracle_detect(const void* img, int bytes_per_px, int H, int W,
   if (!f || !D) return -1;
   oracle_stretch(img, bytes_per_px, plane, lo, hi, f);
   oracle_dog_stack(f, H, W, min_t, max_t, n, D);
+  /* polarity (not in the paper): bright features use the negated
+   * Eq. 2 response D_i = -t_i (L_{i+1} - L_i) */
+  if (polarity)
+    for (int64_t i = 0; i < plane * n; ++i) D[i] = -D[i];
   int64_t ccap = nms == 0 ? plane : plane * n;
   oracle_blob* cand = (oracle_blob*)malloc(sizeof(oracle_blob) * (size_t)ccap);
   int64_t nc;
@@ -428,4 +432,15 @@ int64_t oracle_detect(const void* img, int bytes_per_px, int H, int W,
   free(keep); free(cand); free(f);
   if (!D_dump) free(D);
   return nk;
+}
+
+/* Algorithm 1 as written (dark features, Eq. 2). */
+int64_t oracle_detect(const void* img, int bytes_per_px, int H, int W,
+                      double min_t, double max_t, int n, double tau, double overlap,
+                      double sat_low, double sat_high, int nms, int strict,
+                      oracle_blob* out, int64_t cap, int64_t* n_cand,
+                      double* D_dump, double* v_dump, int32_t* idx_dump,
+                      int64_t* lo_out, int64_t* hi_out) {
+  return oracle_detect_pol(img, bytes_per_px, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high, nms, strict, 0,
+                           out, cap, n_cand, D_dump, v_dump, idx_dump, lo_out, hi_out);
 }

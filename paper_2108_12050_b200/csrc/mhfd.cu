@@ -10,6 +10,7 @@
 //   k_nms_count -> k_seg_scan -> k_nms_write        NMS+threshold+compaction, rows a7-a8
 //   k_prune (cooperative, one launch)               pruning + score + ordered list, a9-a10
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -452,13 +453,23 @@ void mhfd_params_default(mhfd_params* p) {
   p->strict = 0;
   p->device = 0;
   p->max_candidates = 0;
+  p->polarity = MHFD_DARK;
 }
 
 mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   g_err.clear();
   if (!p || !out) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
   *out = nullptr;
-  if (p->struct_size < sizeof(mhfd_params)) return fail(MHFD_ERR_INVALID_ARGUMENT, "struct_size %u", p->struct_size);
+  // ABI 1 callers pass the struct without `polarity` (it then reads as MHFD_DARK)
+  const size_t v1_size = offsetof(mhfd_params, polarity);
+  if (p->struct_size < v1_size) return fail(MHFD_ERR_INVALID_ARGUMENT, "struct_size %u", p->struct_size);
+  mhfd_params pp;
+  memset(&pp, 0, sizeof(pp));
+  memcpy(&pp, p, std::min<size_t>(p->struct_size, sizeof(mhfd_params)));
+  pp.struct_size = sizeof(mhfd_params);
+  p = &pp;
+  if (p->polarity != MHFD_DARK && p->polarity != MHFD_BRIGHT)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "polarity %d", p->polarity);
   if (!(std::isfinite(p->min_sigma) && p->min_sigma > 0.f))
     return fail(MHFD_ERR_INVALID_ARGUMENT, "min_sigma must be > 0 (NonPositiveScale)");
   if (!(std::isfinite(p->max_sigma) && p->max_sigma > p->min_sigma))
@@ -541,7 +552,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     T.pre[i] = pre;
     T.ntap[i] = ntap;
     T.woff[i] = off;
-    T.tdog[i] = (float)t[i];
+    T.tdog[i] = (float)(p->polarity == MHFD_BRIGHT ? -t[i] : t[i]);   // Eq. 2 factor, signed by polarity
     off += ntap + 8;   // >= 1 zero after the taps (the FFMA2 odd-output pair reads w[ntap])
     c->t[i] = t[i];
   }
@@ -549,6 +560,8 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   // tensor-core plan and its Toeplitz tables (device copy owned by the context)
   c->tc = new (std::nothrow) TcPlan;
   if (c->tc && tc_plan_build(*c->tc, n + 1, R, t)) {
+    if (p->polarity == MHFD_BRIGHT)
+      for (int i = 0; i <= n; ++i) c->tc->lev[i].tdog = -c->tc->lev[i].tdog;
     std::vector<std::vector<double>> wv(n + 1);
     for (int i = 0; i <= n; ++i) {
       double sum = 0.0;

@@ -29,7 +29,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert not missing, missing
     for s in declared:
         assert hasattr(lib, s)
-    assert lib.mhfd_abi_version() == 1
+    assert lib.mhfd_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
@@ -49,13 +49,28 @@ def test_params_default_and_struct_size():
     _abi.load().mhfd_params_default(ctypes.byref(p))
     assert p.struct_size == ctypes.sizeof(_abi.mhfd_params)
     assert (p.min_sigma, p.max_sigma, p.num_scales) == (1.0, 10.0, 10)
-    assert p.sat_low == pytest.approx(0.00175) and p.nms == 0 and p.strict == 0
+    assert p.sat_low == pytest.approx(0.00175) and p.nms == 0 and p.strict == 0 and p.polarity == 0
+
+
+def test_abi1_struct_size_reads_polarity_as_dark():
+    """An ABI-1 caller's struct (without `polarity`) is accepted; validation still runs."""
+    lib = _abi.load()
+    p = _abi.mhfd_params()
+    lib.mhfd_params_default(ctypes.byref(p))
+    p.width, p.height, p.max_sigma = 256, 256, 5.0
+    p.struct_size = _abi.mhfd_params.polarity.offset   # ABI 1 layout
+    p.polarity = 7                                     # beyond struct_size: ignored
+    p.min_sigma = 0.0                                  # still validated
+    h = ctypes.c_void_p()
+    assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == 1
+    assert "min_sigma" in lib.mhfd_last_error().decode()
 
 
 @pytest.mark.parametrize("field,value,status", [
     ("min_sigma", 0.0, 1), ("max_sigma", 0.5, 1), ("num_scales", 0, 1), ("num_scales", 63, 1),
     ("threshold", -1.0, 1), ("threshold", float("nan"), 1), ("overlap", 1.5, 1), ("sat_low", 0.6, 1),
     ("nms", 7, 1), ("strict", 2, 1), ("max_sigma", 40.0, 1), ("width", 50, 2), ("height", 70000, 2),
+    ("polarity", 2, 1), ("struct_size", 8, 1),
 ])
 def test_create_validates_before_device(field, value, status):
     lib = _abi.load()

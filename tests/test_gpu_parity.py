@@ -35,15 +35,17 @@ def _to_t(img):
     return t
 
 
-def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None):
+def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None, polarity="dark"):
     """Full comparison on one image: percentiles, DoG stack, v/argmax, candidates,
     pruned blobs, counts and score."""
     H, W = img.shape
     tau = _tau(cfg) if tau is None else tau
     n = cfg["num_scales"]
-    det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, schedule=schedule, **cfg)
+    det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, schedule=schedule,
+                        polarity=polarity, **cfg)
     dump = det.debug_dump(_to_t(img))
-    ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True)
+    ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True,
+                        polarity=polarity)
     # a1: percentiles, exact integers
     lo, hi = dump["lohi"][0].tolist()
     assert (lo, hi) == (ref["lo"], ref["hi"])
@@ -135,6 +137,16 @@ def test_c2_cuda_core_schedules(schedule):
     det = mhfd.Detector(1024, 1024, threshold=0.09, schedule=schedule, **C3)
     assert det.schedule("u8") == {"band": "k_band", "band2": "k_band2", "generic": "k_scale_space"}[schedule]
     _full_parity(img, C3, schedule=schedule)
+
+
+@pytest.mark.parametrize("nms,bits,size", [("paper", 8, 256), ("paper", 8, 1024), ("26", 8, 256), ("paper", 16, 256)])
+def test_bright_polarity_parity(nms, bits, size):
+    """Bright features (negated Eq. 2) on every schedule kind: k_tc (u8),
+    26-mode and u16 (generic)."""
+    img = synth.em_tile_np(size, size, 1002, dose=300.0, bits=bits)
+    cfg = C1 if size == 256 else C3
+    s = _full_parity(img, cfg, nms=nms, polarity="bright")
+    assert s["n_oracle"] > 50
 
 
 def test_u8_schedule_is_tensor_core():

@@ -428,3 +428,47 @@ def test_detect_shift_equivariance_interior():
     A = interior(a["blobs"], dy, dx)
     B = {(int(p["y"]), int(p["x"]), int(p["scale"])) for p in b["blobs"]}
     assert A and A <= B
+
+
+# ---------------------------------------------------------------- polarity
+def test_bright_polarity_equals_dark_on_inverted_image():
+    """bright(I) == dark(M - I): the inverted image's nearest-rank percentiles are
+    (M - hi, M - lo), its stretch is 1 - I', and the unit-sum blur maps 1 - I' to 1 - L,
+    so its Eq. 2 stack is exactly the negated one (up to f64 rounding)."""
+    for bits, M in ((8, 255), (16, 65535)):
+        img = synth.em_tile_np(96, 112, 1000, dose=300.0, bits=bits)
+        inv = (M - img.astype(np.int64)).astype(img.dtype)
+        a = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5, dump=True, polarity="bright")
+        b = oracle.detect(inv, 1.0, 5.0, 5, 0.08, 0.5, dump=True, polarity="dark")
+        assert (a["lo"], a["hi"]) == (M - b["hi"], M - b["lo"])
+        peak = float(np.abs(a["D"]).max())
+        assert float(np.abs(a["D"] - b["D"]).max()) <= 1e-12 * peak
+        ka = {(int(r["x"]), int(r["y"]), int(r["scale"])) for r in a["blobs"]}
+        kb = {(int(r["x"]), int(r["y"]), int(r["scale"])) for r in b["blobs"]}
+        assert ka == kb and a["count"] == b["count"] > 10
+
+
+def test_bright_polarity_negates_dark_response():
+    """Polarity only flips the sign of Eq. 2: D_bright = -D_dark on the same image."""
+    img = synth.em_tile_np(80, 80, 1001, dose=300.0, bits=8)
+    a = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5, dump=True, polarity="bright")
+    b = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5, dump=True, polarity="dark")
+    assert np.array_equal(a["D"], -b["D"])
+
+
+@pytest.mark.parametrize("r", [4.0, 7.0])
+def test_bright_disk_detected_only_with_bright_polarity(r):
+    """A bright disk on a dark background: one blob at the centre with bright polarity,
+    at the scale the dark-disk closed form gives (SURVEY A.9: |t + dt/2 - r/sqrt 2| <= 0.61);
+    with the paper's dark polarity its centre responds negatively and is not a blob."""
+    n, tmin, tmax = 10, 1.0, 10.0
+    dt = (tmax - tmin) / n
+    dark = synth.disk_image(96, 96, 48.5, 48.5, r, contrast=0.6, bits=16)
+    bright = (65535 - dark.astype(np.int64)).astype(np.uint16)
+    res = oracle.detect(bright, tmin, tmax, n, 0.1 * dt, 0.5, polarity="bright")
+    assert res["count"] == 1
+    b = res["blobs"][0]
+    assert (int(b["x"]), int(b["y"])) == (48, 48)
+    assert abs(tmin + int(b["scale"]) * dt + dt / 2 - r / math.sqrt(2)) <= 0.61 + 1e-9
+    res_dark = oracle.detect(bright, tmin, tmax, n, 0.1 * dt, 0.5, polarity="dark")
+    assert (48, 48) not in {(int(q["x"]), int(q["y"])) for q in res_dark["blobs"]}
