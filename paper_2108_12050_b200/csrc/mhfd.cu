@@ -643,6 +643,10 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     return fail(MHFD_ERR_CUDA, "occupancy query for k_prune failed");
   }
   c->prune_grid = bps * c->sms;
+  {
+    const char* pg = getenv("MHFD_PRUNE_CTAS_PER_SM");   // tuning knob (<= the occupancy limit)
+    if (pg && atoi(pg) > 0) c->prune_grid = std::min(bps, atoi(pg)) * c->sms;
+  }
   if (scale_space_smem(rmax, 128, T.ntaps_total) > kSmemLimit) {
     mhfd_destroy(c);
     return fail(MHFD_ERR_INVALID_ARGUMENT, "ceil(5*max_sigma) = %d: the generic schedule's shared memory exceeds the "
@@ -741,8 +745,12 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
   if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[1], st);
   if (e != cudaSuccess) return cuda_fail(e, "event record");
   int launches = 0;
-  for (int b0 = 0, k = 0; b0 < batch; b0 += chunk, ++k) {
-    const int nb = std::min(chunk, batch - b0);
+  // chunk sizes ramp up (chunk/4, chunk/2, chunk, chunk, ...): the first copy, which
+  // nothing can hide, is short, and later chunks are large enough that per-call fixed
+  // costs stay small
+  for (int b0 = 0, k = 0, nb = 0; b0 < batch; b0 += nb, ++k) {
+    const int want = k == 0 ? std::max(1, chunk / 4) : k == 1 ? std::max(1, chunk / 2) : chunk;
+    nb = std::min(want, batch - b0);
     const int h = k & 1;
     char* dst = static_cast<char*>(d_staging) + (size_t)h * chunk * img_bytes;
     e = cudaStreamWaitEvent(c->copy_stream, c->ev_free[h], 0);
