@@ -236,6 +236,50 @@ def roofline_of(det, B: int, kern_ms: float, step_ms: float) -> dict:
             "frac": achieved / ALU_PEAK_TFLOPS, "peak_note": alu["note"], **common}
 
 
+def other_configs(dev) -> dict:
+    """The other configs of SURVEY.md §8(d), measured on rank 0 after the main step (not
+    part of `value`): C2 = one 1024^2 u8 tile, host-visible latency of focus_score_host
+    (H2D + compute + score on the host) and device time; C3 = the same for one 4096^2
+    tile; C5 = one 8192^2 u16 tile, sigma 1-30, 20 scales (generic CUDA-core schedule),
+    device time.  Median of 11 after 3 warm-ups."""
+    import synth
+    import paper_2108_12050_b200 as mhfd
+    out = {}
+
+    def timed(det, img_dev, img_host):
+        for _ in range(3):
+            det.focus_score(img_dev)
+            det.focus_score_host(img_host, chunk=1)
+        torch.cuda.synchronize()
+        dev_ms, host_ms = [], []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(11):
+            torch.cuda.synchronize()
+            e0.record()
+            det.focus_score(img_dev)
+            e1.record()
+            torch.cuda.synchronize()
+            dev_ms.append(e0.elapsed_time(e1))
+            t0 = time.perf_counter()
+            s = det.focus_score_host(img_host, chunk=1)
+            torch.cuda.synchronize()
+            host_ms.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(dev_ms), statistics.median(host_ms), float(s[0])
+
+    for name, size, bits, sig, n in (("C2", 1024, 8, (1.0, 10.0), 10), ("C3", 4096, 8, (1.0, 10.0), 10),
+                                     ("C5", 8192, 16, (1.0, 30.0), 20)):
+        img = synth.em_tile(size, size, 7 if name == "C5" else 1000, defocus=0.0, dose=300.0, bits=bits, device=dev)
+        if bits == 16:   # as the C5 parity test: via numpy to a torch.uint16 tensor
+            img = torch.from_numpy(img.to(torch.int32).cpu().numpy().astype(np.uint16)).to(dev)
+        tau = 0.1 * (sig[1] - sig[0]) / n
+        det = mhfd.Detector(size, size, sig[0], sig[1], n, threshold=tau, overlap=0.5, device=dev.index)
+        dms, hms, score = timed(det, img.unsqueeze(0), img.unsqueeze(0).cpu().pin_memory())
+        out[name] = {"size": size, "dtype": f"u{bits}", "sigma": list(sig), "scales": n, "schedule": det.schedule(
+            f"u{bits}"), "device_ms": dms, "host_visible_ms": hms, "MPix_per_s_device": size * size / dms / 1e3,
+            "score": score}
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -246,6 +290,7 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=64, help="images per GPU per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2/C3/C5 single-image measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -345,6 +390,9 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(imgs[0].cpu().numpy())
+    configs = None
+    if rank == 0 and not args.no_configs:
+        configs = other_configs(dev)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
@@ -358,7 +406,7 @@ def main() -> None:
                            "parallelism": f"dp{world} (image sharding, NCCL all-gather of (count, score))",
                            "l2": "inputs larger than L2 (1.07 GB per GPU per step)"},
                 "roofline": roofline, "stage_ms": stage_ms, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_call * args.steps, "clocks": clk.summary(),
+                "gpu_launches": launches_per_call * args.steps, "clocks": clk.summary(), "other_configs": configs,
                 "mean_score": float(scores.mean())}
         print(json.dumps(line), flush=True)
     if dist is not None:
