@@ -13,7 +13,7 @@ if [ $rc -ne 0 ]; then echo "gpu tests failed, stopping"; exit 1; fi
 timeout 300 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench_rc=$?" >> gpurun_out/${TAG}_bench.err
 [ "${NO_NCU:-0}" = "1" ] && exit 0
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
-  python bench.py --steps 2 --warmup 3 --batch 16 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1
+  python bench.py --steps 2 --warmup 3 --batch 16 --no-e2e --no-cpu-baseline --no-configs > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "ncu_launch_rc=$?" >> gpurun_out/${TAG}_ncu_launch.log
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k_tc|k_prune|k_nms_rows|k_hist" -s 5 -c 5 -o gpurun_out/${TAG}_tc \
   python tools/prof_run.py --batch 2 > gpurun_out/${TAG}_prof_ncu.log 2>&1
