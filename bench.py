@@ -277,7 +277,73 @@ def other_configs(dev) -> dict:
         out[name] = {"size": size, "dtype": f"u{bits}", "sigma": list(sig), "scales": n, "schedule": det.schedule(
             f"u{bits}"), "device_ms": dms, "host_visible_ms": hms, "MPix_per_s_device": size * size / dms / 1e3,
             "score": score}
+    out["C3_bands_1gpu"] = band_times(dev)
     return out
+
+
+def band_times(dev) -> dict:
+    """Single-image sharding measured on one GPU: for G bands of one
+    4096^2 tile, the device time of each rank's mhfd_detect_band (max over bands) and of
+    mhfd_prune_candidates on the full list — the compute a G-GPU run does per image
+    (the broadcast and the two all-gathers are not included)."""
+    import synth
+    import paper_2108_12050_b200 as mhfd
+    from paper_2108_12050_b200.dist import band_rows
+    img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
+    det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP, device=dev.index)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def t(fn):
+        for _ in range(3):
+            fn()
+        ms = []
+        for _ in range(7):
+            torch.cuda.synchronize()
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.median(ms)
+
+    res = {}
+    for G in (1, 2, 4, 8):
+        bands, parts = [], []
+        for r in range(G):
+            y0, y1 = band_rows(SIZE, G, r)
+            bands.append(t(lambda: det.detect_band(img, y0, y1)))
+            c, nn = det.detect_band(img, y0, y1)
+            parts.append(c[:int(nn)].clone())
+        allc = torch.cat(parts, 0)
+        pr = t(lambda: det.prune_candidates(allc, allc.shape[0]))
+        res[str(G)] = {"band_ms_max": max(bands), "prune_ms": pr, "per_image_ms": max(bands) + pr}
+    return res
+
+
+def sharded_single_image(dev, dist, steps: int) -> dict:
+    """Single-image sharding across the job's ranks (f2): one 4096^2 tile per step,
+    broadcast + bands + all-gathers + pruning; device time, max over ranks."""
+    import synth
+    import paper_2108_12050_b200 as mhfd
+    from paper_2108_12050_b200.dist import focus_score_single_image
+    img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
+    det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP, device=dev.index)
+    ref = float(det.focus_score(img)[0])
+    for _ in range(3):
+        focus_score_single_image(det, img)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        _, _, score, _ = focus_score_single_image(det, img)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    assert float(score[0]) == ref, "sharded score differs from the single-GPU score"
+    return {"workload": "one 4096^2 u8 tile per step, row bands across ranks (SURVEY §8(f) f2)",
+            "ms_per_image": float(ms.item()), "score": ref}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -393,6 +459,12 @@ def main() -> None:
     configs = None
     if rank == 0 and not args.no_configs:
         configs = other_configs(dev)
+    sharded = None
+    if dist is not None and not args.no_configs:
+        try:   # an extra measurement: never let it take the main line down
+            sharded = sharded_single_image(dev, dist, args.steps)
+        except Exception as exc:  # noqa: BLE001
+            sharded = {"error": repr(exc)[:300]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
@@ -407,6 +479,7 @@ def main() -> None:
                            "l2": "inputs larger than L2 (1.07 GB per GPU per step)"},
                 "roofline": roofline, "stage_ms": stage_ms, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_call * args.steps, "clocks": clk.summary(), "other_configs": configs,
+                "single_image_sharded": sharded,
                 "mean_score": float(scores.mean())}
         print(json.dumps(line), flush=True)
     if dist is not None:

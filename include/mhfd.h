@@ -195,6 +195,37 @@ mhfd_status mhfd_debug_dump(mhfd_ctx* c, const void* d_images, int32_t dtype, in
                             int32_t* d_lohi, float* d_dog, float* d_v, uint8_t* d_idx,
                             mhfd_blob* d_cands, int32_t* d_ncand, void* stream);
 
+/* Single-image multi-GPU spatial sharding.  The image is split into
+ * row bands, one per GPU; every GPU holds the whole image (the caller broadcasts it),
+ * so a band needs no halo exchange: its blur windows and its Eq. 3 NMS neighbours
+ * (rows y0-1 and y1) are evaluated locally, and the percentiles are those of the whole
+ * image.  The bands' candidate lists, concatenated in band order (NCCL all-gather), are
+ * the whole image's candidate list in raster order, bit-identical to the one
+ * mhfd_detect_batch prunes; mhfd_prune_candidates then prunes it and scores the image
+ * (the only step that needs every band: overlaps cross band edges).
+ *
+ * mhfd_detect_band: candidates of rows [y0, y1) of ONE image.
+ *  d_image        : height x pitch_bytes bytes (u8; the "k_tc" schedule, Eq. 3 NMS)
+ *  0 <= y0 < y1 <= height; width % 1024 == 0
+ *  d_workspace    : >= mhfd_workspace_bytes(c, 1)
+ *  d_cands        : cand_capacity records; the band's candidates in (y, x) order,
+ *                   truncated to cand_capacity (the count is exact)
+ *  d_ncand        : 1 int32, the band's exact candidate count
+ * Errors: as mhfd_detect_batch; SHAPE for the band/width; INVALID_ARGUMENT when the
+ * context's u8 schedule is not "k_tc". */
+mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, int64_t pitch_bytes, int32_t y0,
+                             int32_t y1, void* d_workspace, size_t workspace_bytes, mhfd_blob* d_cands,
+                             int32_t cand_capacity, int32_t* d_ncand, void* stream);
+
+/* mhfd_prune_candidates: pruning + focus score of one image from its full candidate
+ * list (ncand records at d_cands, raster (y, x) order, ncand <= the context's
+ * max_candidates).  d_blobs (nullable if blob_capacity == 0): kept blobs in (y, x,
+ * scale) order; d_count, d_score (nullable), d_flags (nullable): as mhfd_detect_batch /
+ * mhfd_focus_score for one image.  d_workspace as mhfd_detect_band. */
+mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t ncand, void* d_workspace,
+                                  size_t workspace_bytes, mhfd_blob* d_blobs, int32_t blob_capacity,
+                                  int32_t* d_count, double* d_score, int32_t* d_flags, void* stream);
+
 /* Read back the parameters a context was built with (derived fields filled). */
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
 

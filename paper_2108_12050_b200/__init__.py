@@ -196,6 +196,38 @@ class Detector:
                                                    self._stream()))
         return (self._hs[:B], self._hc[:B]) if counts else self._hs[:B]
 
+    # -------------------------------------------------- single-image sharding (f2)
+    def detect_band(self, image: torch.Tensor, y0: int, y1: int, capacity: int | None = None):
+        """Candidates of rows [y0, y1) of ONE image (mhfd_detect_band): (cands (cap, 4)
+        int32 records in (y, x) order, exact count as a 1-element int32 device tensor)."""
+        imgs, dt, B, pitch = self.prepare(image)
+        if B != 1:
+            raise ValueError("detect_band takes one image")
+        ws = self._workspace(1)
+        cap = self.max_candidates if capacity is None else int(capacity)
+        cands = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=self.device)
+        n = torch.empty(1, dtype=torch.int32, device=self.device)
+        _abi.check(self._lib.mhfd_detect_band(self._h, imgs.data_ptr(), dt, pitch, int(y0), int(y1),
+                                              self._ws_ptr(ws), ws.numel() - 256, cands.data_ptr(), cap,
+                                              n.data_ptr(), self._stream()))
+        return cands, n
+
+    def prune_candidates(self, cands: torch.Tensor, ncand: int, blob_capacity: int | None = None):
+        """Pruning + score of one image's full raster-ordered candidate list
+        (mhfd_prune_candidates): (blobs (cap, 4), count (1,), score (1,) float64, flags (1,))."""
+        ws = self._workspace(1)
+        cap = self.max_candidates if blob_capacity is None else int(blob_capacity)
+        cands = cands.contiguous()
+        blobs = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=self.device)
+        cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+        score = torch.empty(1, dtype=torch.float64, device=self.device)
+        flags = torch.empty(1, dtype=torch.int32, device=self.device)
+        _abi.check(self._lib.mhfd_prune_candidates(self._h, cands.data_ptr() if ncand > 0 else None, int(ncand),
+                                                   self._ws_ptr(ws), ws.numel() - 256, blobs.data_ptr(), cap,
+                                                   cnt.data_ptr(), score.data_ptr(), flags.data_ptr(),
+                                                   self._stream()))
+        return blobs, cnt, score, flags
+
     def timing_enable(self, max_calls: int) -> None:
         _abi.check(self._lib.mhfd_timing_enable(self._h, int(max_calls)))
 

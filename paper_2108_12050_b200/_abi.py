@@ -23,7 +23,7 @@ EXPORTS = ["mhfd_params_default", "mhfd_create", "mhfd_workspace_bytes", "mhfd_d
            "mhfd_focus_score", "mhfd_debug_dump", "mhfd_get_params", "mhfd_last_launch_count",
            "mhfd_destroy", "mhfd_status_string", "mhfd_last_error", "mhfd_abi_version",
            "mhfd_focus_score_host", "mhfd_timing_enable", "mhfd_timing_read", "mhfd_schedule_name",
-           "mhfd_schedule_flops_per_pixel"]
+           "mhfd_schedule_flops_per_pixel", "mhfd_detect_band", "mhfd_prune_candidates"]
 
 
 class mhfd_params(ctypes.Structure):
@@ -70,6 +70,8 @@ def load() -> ctypes.CDLL:
             "mhfd_timing_read": (i32, [P, P, ctypes.POINTER(i32)]),
             "mhfd_schedule_name": (ctypes.c_char_p, [P, i32]),
             "mhfd_schedule_flops_per_pixel": (ctypes.c_double, [P, i32]),
+            "mhfd_detect_band": (i32, [P, P, i32, i64, i32, i32, P, sz, P, i32, P, P]),
+            "mhfd_prune_candidates": (i32, [P, P, i32, P, sz, P, i32, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -229,7 +229,7 @@ constexpr int kNmsRows = 2;   // output rows per warp in k_nms_rows (4: 2.98 ms,
 template <bool WRITE>
 __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* __restrict__ segcnt,
                                                   const int32_t* __restrict__ segoff, mhfd_blob* __restrict__ cand,
-                                                  int64_t cap) {
+                                                  int64_t cap, int row0, int row1) {
   // a warp owns kNmsRows vertically adjacent 1024-pixel segments (rows y0.., piece xs):
   // kNmsRows + 2 rows are loaded per step, so each v row leaves L2 1.5 times, not 3
   constexpr int NR = kNmsRows;
@@ -237,10 +237,12 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
   const int lane = threadIdx.x & 31;
   const int W = a.W, H = a.H;
   const int spr = W / kSeg;                                   // segments per row
+  // output rows [row0, row1) (the image, or one band of it; neighbours come from v
+  // rows row0-1 and row1, which the caller has computed); segments are numbered from row0
   const int grp = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int ngrp = ((H + NR - 1) / NR) * spr;
+  const int ngrp = ((row1 - row0 + NR - 1) / NR) * spr;
   if (grp >= ngrp) return;
-  const int y0 = NR * (grp / spr);
+  const int y0 = row0 + NR * (grp / spr);
   const int xseg = (grp % spr) * kSeg;
   const float* vb = a.v + (int64_t)b * H * W;
   const float* rows[NR + 2];
@@ -250,12 +252,12 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
     rows[k] = (y >= 0 && y < H) ? vb + (int64_t)y * W : nullptr;
   }
   const float NEG = -INFINITY;
-  const int seg0 = (y0 * W + xseg) / kSeg;
+  const int seg0 = ((y0 - row0) * W + xseg) / kSeg;
   int64_t off[NR];
   int total[NR];
 #pragma unroll
   for (int o = 0; o < NR; ++o) {
-    off[o] = (WRITE && y0 + o < H) ? (int64_t)segoff[(int64_t)b * nseg + seg0 + o * spr] : 0;
+    off[o] = (WRITE && y0 + o < row1) ? (int64_t)segoff[(int64_t)b * nseg + seg0 + o * spr] : 0;
     total[o] = 0;
   }
   mhfd_blob* out = WRITE ? cand + (int64_t)b * cap : nullptr;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
         const bool ok = (c[k] > a.tau) && (a.strict ? (c[k] > m) : (c[k] >= m));
         bb |= (uint32_t)ok << (k - 1);
       }
-      if (!rows[o + 1]) bb = 0u;
+      if (y0 + o >= row1) bb = 0u;
       const int n = __popc(bb);
       if (WRITE) {
         int incl = n;
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
       int t = total[o];
 #pragma unroll
       for (int sh = 16; sh; sh >>= 1) t += __shfl_xor_sync(0xffffffffu, t, sh);
-      if (lane == 0 && y0 + o < H) segcnt[(int64_t)b * nseg + seg0 + o * spr] = t;
+      if (lane == 0 && y0 + o < row1) segcnt[(int64_t)b * nseg + seg0 + o * spr] = t;
     }
   }
 }

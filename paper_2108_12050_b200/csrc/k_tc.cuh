@@ -48,11 +48,11 @@ inline bool tc_ok(const TcPlan& P, int W, int H) {
 struct TcTile {
   int b, x0, y0;
 };
-__device__ __forceinline__ TcTile tc_tile(int t, int tx, int ty) {
+__device__ __forceinline__ TcTile tc_tile(int t, int tx, int ty, int row_lo) {
   TcTile r;
   r.x0 = (t % tx) * kTcTile;
   t /= tx;
-  r.y0 = (t % ty) * kTcTile;
+  r.y0 = row_lo + (t % ty) * kTcTile;
   r.b = t / ty;
   return r;
 }
@@ -176,7 +176,8 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" :::
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
-     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, int batch, unsigned long long* __restrict__ trace) {
+     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, int batch, int row_lo, int row_hi,
+     unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int S = P.S, LW = tc_lw(P), OFF = tc_off(P);
   uint8_t* B1 = smem_raw;                                          // S x S fp16, canonical K-major
@@ -190,7 +191,8 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
   do { if (tr && (g) < 64) tr[(g) * 16 + (slot)] = clock64(); } while (0)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tx = (s.W + kTcTile - 1) / kTcTile, ty = (s.H + kTcTile - 1) / kTcTile;
+  // rows [row_lo, row_hi) of every image (the whole image, or one band: mhfd_detect_band)
+  const int tx = (s.W + kTcTile - 1) / kTcTile, ty = (row_hi - row_lo + kTcTile - 1) / kTcTile;
   const int ntiles = tx * ty * batch;
   const int t0 = blockIdx.x;
   if (t0 >= ntiles) return;
@@ -274,7 +276,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
     const int64_t plane = (int64_t)s.H * s.W;
     int t = t0;
-    TcTile tt = tc_tile(t, tx, ty);
+    TcTile tt = tc_tile(t, tx, ty, row_lo);
     int mode = tc_fetch_epi(tt, land, &bars[0], images, s, &tmap, use_tmap, P);
     uint32_t land_phase = 0;
     TcTile ot = tt;
@@ -311,7 +313,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
         const int y = ot.y0 + 32 * wg + u;
-        if (x < s.W && y < s.H) {
+        if (x < s.W && y < row_hi) {
           const int64_t pidx = (int64_t)ot.b * plane + (int64_t)y * s.W + x;
           v_out[pidx] = odeg ? 0.f : vbest[u];
           idx_out[pidx] = odeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
@@ -338,7 +340,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         if (lane == 0) mbar_arrive1(&bars[7]);
         epi_sync();   // landing zone free
         const int tn = t + gridDim.x;
-        if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty), land, &bars[0], images, s, &tmap, use_tmap, P);
+        if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty, row_lo), land, &bars[0], images, s, &tmap, use_tmap, P);
         // ---- DoG of the previous tile's last level, then its output
         if (g > 0) {
           mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
@@ -353,7 +355,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         for (int u = 0; u < 32; ++u) vbest[u] = -INFINITY;
 #pragma unroll
         for (int u = 0; u < 8; ++u) ibest[u] = 0u;
-        if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty); }
+        if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty, row_lo); }
       } else {
         mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
         umma::fence_after();

@@ -188,20 +188,22 @@ cudaEvent_t* next_timing(mhfd_ctx* c) {
   } while (0)
 
 mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L, float* v, uint8_t* idx,
-                    float* dog, cudaStream_t st, int& launches, cudaEvent_t* ev) {
+                    float* dog, cudaStream_t st, int& launches, cudaEvent_t* ev, int band_lo = 0, int band_hi = 0) {
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   // ---- a7-a8: NMS + threshold + ordered compaction
   NmsArgs na{W, H, c->n, c->p.threshold, c->p.strict, v, idx, dog};
-  const int nseg = nseg_of(c);
+  const bool band = band_lo < band_hi;
+  const int row0 = band ? band_lo : 0, row1 = band ? band_hi : H;
+  const int nseg = band ? (int)((int64_t)(row1 - row0) * W / kSeg) : nseg_of(c);   // band: W % kSeg == 0
   int32_t* segcnt = reinterpret_cast<int32_t*>(ws + L.segcnt);
   int32_t* segoff = reinterpret_cast<int32_t*>(ws + L.segoff);
   int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
   mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
   dim3 gn((nseg + 7) / 8, B);
   const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
-  const dim3 gr((((H + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // k_nms_rows: kNmsRows segments per warp
+  const dim3 gr((((row1 - row0 + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // kNmsRows segments per warp
   if (rows_fast) {
-    k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0);
+    k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1);
   } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
   } else {
@@ -211,7 +213,7 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
   LAUNCH_CHECK("k_seg_scan");
   if (rows_fast) {
-    k_nms_rows<true><<<gr, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap);
+    k_nms_rows<true><<<gr, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap, row0, row1);
   } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {
@@ -222,8 +224,11 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   return MHFD_OK;
 }
 
+// band_lo < band_hi: single-image band mode (mhfd_detect_band): blur/DoG/argmax for rows
+// [band_lo - 1, band_hi + 1) of the image, Eq. 3 NMS + compaction for rows [band_lo, band_hi)
 mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t B, int64_t pitch, char* ws,
-                      const Layout& L, float* dog_dump, cudaStream_t st, int& launches, cudaEvent_t* ev) {
+                      const Layout& L, float* dog_dump, cudaStream_t st, int& launches, cudaEvent_t* ev,
+                      int band_lo = 0, int band_hi = 0) {
   MARK(0);
   const int W = c->p.width, H = c->p.height;
   const int bpp = dtype == MHFD_U8 ? 1 : 2;
@@ -267,24 +272,31 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   float* v = reinterpret_cast<float*>(ws + L.v);
   uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
   // ---- a2-a6 on u8 images on the tensor cores (banded-Toeplitz blur)
+  const bool band = band_lo < band_hi;
   if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 3 && c->d_tctab &&
       tc_ok(*c->tc, W, H)) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
     cudaError_t ea = cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc attribute");
-    const int64_t ntiles = (int64_t)((W + kTcTile - 1) / kTcTile) * ((H + kTcTile - 1) / kTcTile) * B;
+    // band mode: rows [band_lo - 1, band_hi + 1) on the whole image's 128-row tile grid, so
+    // every pixel sees the same K-step grouping (and rounding) as in the whole-image run
+    const int r_lo = band ? std::max(0, band_lo - 1) / kTcTile * kTcTile : 0;
+    const int r_hi = band ? std::min(H, (std::min(H, band_hi + 1) + kTcTile - 1) / kTcTile * kTcTile) : H;
+    const int64_t ntiles = (int64_t)((W + kTcTile - 1) / kTcTile) * ((r_hi - r_lo + kTcTile - 1) / kTcTile) * B;
     dim3 gb((unsigned)std::min<int64_t>(ntiles, c->sms));   // persistent: one CTA per SM
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
                                                       (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
                                                       (uint32_t)P.S);
-    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B, nullptr);
+    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B, r_lo, r_hi,
+                                            nullptr);
     LAUNCH_CHECK("k_tc");
     MARK(2);
-    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
+    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev, band_lo, band_hi);
   }
+  if (band) return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
   // ---- a2-a6 on u8 images, two-CTA band schedule
   if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
       band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
@@ -374,14 +386,14 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
 
 mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_blob* blobs, int32_t blob_cap,
                       int32_t* counts, double* scores, int32_t* flags, cudaStream_t st, int& launches,
-                      cudaEvent_t* ev) {
+                      cudaEvent_t* ev, const mhfd_blob* ext_cand = nullptr) {
   PruneArgs pa;
   memset(&pa, 0, sizeof(pa));
   pa.B = B;
   pa.W = c->p.width;
   pa.H = c->p.height;
   pa.cap = c->cap;
-  pa.cand = reinterpret_cast<const mhfd_blob*>(ws + L.cand);
+  pa.cand = ext_cand ? ext_cand : reinterpret_cast<const mhfd_blob*>(ws + L.cand);
   pa.ncand = reinterpret_cast<const int32_t*>(ws + L.ncand);
   pa.overlap = c->p.overlap;
   pa.prune = c->p.overlap < 1.0f ? 1 : 0;
@@ -411,6 +423,15 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   MARK(4);
   return MHFD_OK;
 }
+
+// band mode helpers: copy min(n, cap) candidate records; set one device int
+__global__ void k_copy_cands(const mhfd_blob* __restrict__ src, const int32_t* __restrict__ n, int64_t cap,
+                             mhfd_blob* __restrict__ dst) {
+  const int64_t m = min((int64_t)*n, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
 
 __global__ void k_copy_lohi(const ImgPar* par, int32_t* lohi, int B) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -803,6 +824,66 @@ double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {
   double f = 0.0;   // direct separable blur at R_i: 2 passes x (2R_i+1) FMA per level, + DoG/max
   for (int i = 0; i <= c->n; ++i) f += 2.0 * 2.0 * (2.0 * c->tab->R[i] + 1.0);
   return f + 3.0 * c->n;
+}
+
+mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, int64_t pitch_bytes, int32_t y0,
+                             int32_t y1, void* d_workspace, size_t workspace_bytes, mhfd_blob* d_cands,
+                             int32_t cand_capacity, int32_t* d_ncand, void* stream) {
+  g_err.clear();
+  mhfd_status s = check_call(c, d_image, dtype, 1, pitch_bytes, d_workspace, workspace_bytes);
+  if (s != MHFD_OK) return s;
+  const int W = c->p.width, H = c->p.height;
+  if (!(0 <= y0 && y0 < y1 && y1 <= H)) return fail(MHFD_ERR_SHAPE, "band rows [%d, %d) not inside [0, %d)", y0, y1, H);
+  if (W % kSeg != 0) return fail(MHFD_ERR_SHAPE, "band mode needs width %% %d == 0", kSeg);
+  if (strcmp(mhfd_schedule_name(c, dtype), "k_tc") != 0)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
+  if (!d_ncand || (!d_cands && cand_capacity > 0) || cand_capacity < 0)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "d_ncand / d_cands / cand_capacity");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  const Layout L = layout(c, 1);
+  int launches = 0;
+  s = run_front(c, d_image, dtype, 1, pitch_bytes, ws, L, nullptr, st, launches, nullptr, y0, y1);
+  if (s != MHFD_OK) return s;
+  const int32_t* nc = reinterpret_cast<const int32_t*>(ws + L.ncand);
+  if (cand_capacity > 0) {
+    k_copy_cands<<<c->sms * 4, 256, 0, st>>>(reinterpret_cast<const mhfd_blob*>(ws + L.cand), nc, cand_capacity,
+                                              d_cands);
+    ++launches;
+  }
+  cudaError_t e = cudaMemcpyAsync(d_ncand, nc, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "band outputs");
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t ncand, void* d_workspace,
+                                  size_t workspace_bytes, mhfd_blob* d_blobs, int32_t blob_capacity,
+                                  int32_t* d_count, double* d_score, int32_t* d_flags, void* stream) {
+  g_err.clear();
+  if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (ncand < 0 || ncand > c->cap) return fail(MHFD_ERR_CAPACITY, "ncand %d not in [0, %lld]", ncand, (long long)c->cap);
+  if (ncand > 0 && !d_cands) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_cands is NULL");
+  if (!d_count) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_count is NULL");
+  if (blob_capacity < 0 || (blob_capacity > 0 && !d_blobs)) return fail(MHFD_ERR_INVALID_ARGUMENT, "blobs");
+  if (!d_workspace || ((uintptr_t)d_workspace) % 256 != 0) return fail(MHFD_ERR_WORKSPACE, "workspace");
+  const Layout L = layout(c, 1);
+  if (workspace_bytes < L.total) return fail(MHFD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, L.total);
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != c->p.device)
+    return fail(MHFD_ERR_DEVICE, "current device %d != context device %d", dev, c->p.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  k_set_i32<<<1, 1, 0, st>>>(reinterpret_cast<int32_t*>(ws + L.ncand), ncand);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_set_i32");
+  int launches = 1;
+  mhfd_status s = run_prune(c, 1, ws, L, blob_capacity > 0 ? d_blobs : nullptr, blob_capacity, d_count, d_score,
+                            d_flags, st, launches, nullptr, ncand > 0 ? d_cands : reinterpret_cast<const mhfd_blob*>(ws + L.cand));
+  if (s != MHFD_OK) return s;
+  g_launches = launches;
+  return MHFD_OK;
 }
 
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out) {

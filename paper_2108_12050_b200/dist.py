@@ -30,3 +30,49 @@ def gather_results(counts: torch.Tensor, scores: torch.Tensor, out: torch.Tensor
         out = torch.empty((world * local.shape[0], 2), dtype=torch.float64, device=local.device)
     dist.all_gather_into_tensor(out, local)   # rank r's block at rows [r*n, (r+1)*n)
     return out.view(world, local.shape[0], 2)
+
+
+# ------------------------------------------------------------------ single-image sharding
+# SURVEY.md §8(f) f2 (the paper's own multi-GPU goal, without its
+# gather of whole L planes): one image split into row bands, one per rank.  Every rank
+# holds the image (broadcast, 1 B/px), computes the candidates of its band
+# (mhfd_detect_band: its blur windows and NMS neighbours are evaluated locally, the
+# percentiles are the whole image's), the bands' lists are all-gathered in rank order
+# (= raster order of the whole image), and every rank prunes the full list.
+
+def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row band [y0, y1) of `rank` (heights differ by <= 1)."""
+    return shard(height, world, rank)
+
+
+def gather_candidates(cands: torch.Tensor, n: int | torch.Tensor) -> tuple[torch.Tensor, int]:
+    """All-gather every rank's first `n` candidate records (rows of `cands`) in rank
+    order -> (concatenated records, total).  Two collectives: the counts, then the
+    records padded to the largest count."""
+    world = dist.get_world_size()
+    dev = cands.device
+    n_t = (n.reshape(1) if isinstance(n, torch.Tensor) else torch.tensor([int(n)])).to(dev, torch.int64)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(counts, n_t)
+    counts_h = [int(c) for c in counts.cpu().tolist()]
+    m = max(max(counts_h), 1)
+    rec = cands.shape[1]
+    local = torch.zeros((m, rec), dtype=cands.dtype, device=dev)
+    k = counts_h[dist.get_rank()]
+    local[:k] = cands[:k]
+    allc = torch.empty((world * m, rec), dtype=cands.dtype, device=dev)
+    dist.all_gather_into_tensor(allc, local)
+    parts = [allc[r * m: r * m + counts_h[r]] for r in range(world)]
+    return torch.cat(parts, 0), sum(counts_h)
+
+
+def focus_score_single_image(det, image: torch.Tensor, src: int = 0):
+    """Score ONE image on all ranks (each rank a row band; NCCL broadcast + all-gathers).
+    `image` is the (H, W) u8 tile on this rank's device (its content matters on `src`
+    only).  Returns (blobs, count, score, flags) of mhfd_prune_candidates, identical on
+    every rank and bit-identical to det.detect / det.focus_score on the whole image."""
+    dist.broadcast(image, src)
+    y0, y1 = band_rows(det.height, dist.get_world_size(), dist.get_rank())
+    cands, n = det.detect_band(image, y0, y1)
+    allc, total = gather_candidates(cands, n)
+    return det.prune_candidates(allc, total)

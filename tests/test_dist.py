@@ -71,3 +71,55 @@ def test_gather_world2_matches_single_process():
     assert g.shape == (2, 2, 2)
     np.testing.assert_array_equal(g.reshape(-1, 2)[:, 0], ref)
     np.testing.assert_array_equal(g.reshape(-1, 2)[:, 1], ref)
+
+
+# ---------------------------------------------------------------- single-image sharding (f2)
+def _band_worker(rank, world, port, img, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2108_12050_b200.dist import band_rows, gather_candidates
+    # the per-band candidates the GPU computes (mhfd_detect_band), here from the oracle:
+    # the whole image's Eq. 3 candidates restricted to this rank's rows
+    H = img.shape[0]
+    ref = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5, dump=True)
+    allc = oracle.nms_paper(ref["D"], 0.08)
+    y0, y1 = band_rows(H, world, rank)
+    mine = allc[(allc["y"] >= y0) & (allc["y"] < y1)]
+    rec = torch.from_numpy(np.stack([mine["x"], mine["y"], mine["scale"]], 1).astype(np.int32))
+    got, total = gather_candidates(rec, len(mine))
+    if rank == 0:
+        q.put((got.numpy(), total))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_band_sharding_world2_reassembles_raster_list():
+    """Bands partition the rows; the all-gathered band lists are the whole image's
+    candidate list in raster order, and pruning it gives the single-process result."""
+    import oracle
+    import synth
+    from paper_2108_12050_b200.dist import band_rows
+    for H in (64, 67):
+        parts = [band_rows(H, 3, r) for r in range(3)]
+        assert parts[0][0] == 0 and parts[-1][1] == H and all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+    img = synth.em_tile_np(96, 80, 1003, dose=300.0)
+    ref = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5, dump=True)
+    allc = oracle.nms_paper(ref["D"], 0.08)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, 2, port, img, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, total = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert total == len(allc)
+    np.testing.assert_array_equal(got[:, 0], allc["x"])
+    np.testing.assert_array_equal(got[:, 1], allc["y"])
+    np.testing.assert_array_equal(got[:, 2], allc["scale"])
+    keep = oracle.prune(allc, 1.0, 5.0, 5, 0.5)
+    assert int(keep.sum()) == ref["count"]

@@ -324,3 +324,34 @@ def test_c5_large_radius_sampled():
 def test_c2_26_mode_parity():
     img = synth.em_tile_np(1024, 1024, 1000, defocus=0.0, dose=300.0, bits=8)
     _full_parity(img, C3, nms="26")
+
+
+# ------------------------------------------------------------------ f2: single-image bands
+@pytest.mark.parametrize("size,G", [(1024, 1), (1024, 3), (4096, 2), (4096, 8)])
+def test_band_sharding_matches_whole_image(size, G):
+    """Single-image multi-GPU sharding, the G ranks run one after
+    another on this GPU: the bands' candidate lists (mhfd_detect_band) concatenated in
+    band order are bit-identical to the whole image's list, and pruning them
+    (mhfd_prune_candidates) reproduces detect()/focus_score() exactly."""
+    from paper_2108_12050_b200.dist import band_rows
+    img = synth.em_tile(size, size, 1004, defocus=0.5, dose=300.0, device="cuda")
+    det = mhfd.Detector(size, size, threshold=0.09, **C3)
+    full = det.debug_dump(img, dog=False, cands=True)
+    nfull = int(full["ncand"][0])
+    blobs_full, cnt_full, _ = det.detect(img)
+    score_full = det.focus_score(img)
+    parts, total = [], 0
+    for r in range(G):
+        y0, y1 = band_rows(size, G, r)
+        c, n = det.detect_band(img, y0, y1)
+        n = int(n)
+        parts.append(c[:n].clone())
+        total += n
+    allc = torch.cat(parts, 0)
+    assert total == nfull
+    assert torch.equal(allc, full["cands"][0, :nfull])
+    blobs, cnt, score, flags = det.prune_candidates(allc, total)
+    torch.cuda.synchronize()
+    k = int(cnt[0])
+    assert k == int(cnt_full[0]) and float(score[0]) == float(score_full[0]) == float(k) and int(flags[0]) == 0
+    assert torch.equal(blobs[:k], blobs_full[0, :k])
