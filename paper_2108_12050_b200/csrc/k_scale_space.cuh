@@ -47,11 +47,11 @@ __host__ __device__ inline int hbuf_rows(int rmax, int BH) { return BH + 2 * rma
 // hbuf floats, rounded to 32 so the tap table and mbarriers after it stay 128-byte aligned
 __host__ __device__ inline int hbuf_floats(int rmax, int BH) { return (hbuf_rows(rmax, BH) * kHP + 31) & ~31; }
 __host__ __device__ inline int wtab_floats(int ntaps_total) { return (ntaps_total + 31) & ~31; }
-// layout: [stage: kStages x 32 x SP][hbuf][weights wA][weights wB][mbarriers]
-__host__ __device__ inline size_t scale_space_smem(int rmax, int BH, int ntaps_total) {
-  return sizeof(float) * ((size_t)kStages * kChunkRows * stage_pitch(rmax) + 64 + (size_t)hbuf_floats(rmax, BH) +
+// layout: [stage: stages x 32 x SP][hbuf][weights wA][weights wB][mbarriers]
+__host__ __device__ inline size_t scale_space_smem(int rmax, int BH, int ntaps_total, int stages = kStages) {
+  return sizeof(float) * ((size_t)stages * kChunkRows * stage_pitch(rmax) + 64 + (size_t)hbuf_floats(rmax, BH) +
                           2 * wtab_floats(ntaps_total)) +
-         8 * kStages;
+         8 * stages;
 }
 // 2-D TMA boxes hold SP <= 256 columns
 __host__ __device__ inline bool tma_boxes(int rmax) { return stage_pitch(rmax) <= 256; }
@@ -290,8 +290,11 @@ __device__ __forceinline__ void stage_rows(float* dst0, uint64_t* bar, const flo
   }
 }
 
-template <int RPT, bool WRITE_V, bool WRITE_DOG, bool FAST>
-__global__ void __launch_bounds__(kThreads, 2)
+// RPT rows per thread (band height BH = 8 RPT), NST copy stages.  The 384-row band
+// (RPT = 48, two stages, one CTA per SM) is for large radii, where the row pass
+// recomputes (BH + 2R) / BH rows per output (3.3x at R = 150 with 128-row bands).
+template <int RPT, bool WRITE_V, bool WRITE_DOG, bool FAST, int NST = kStages>
+__global__ void __launch_bounds__(kThreads, RPT > 32 ? 1 : 2)
 k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict__ par,
               const __grid_constant__ LevelTable tab, const __grid_constant__ CUtensorMap tmap, int use_tmap,
               float* __restrict__ v_out,
@@ -301,8 +304,8 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
   float* smem = reinterpret_cast<float*>(smem_raw);
   const int rmax = tab.rmax;
   const int SP = stage_pitch(rmax);
-  float* stage = smem;                                         // kStages x kChunkRows x SP
-  float* hbuf = smem + kStages * kChunkRows * SP + 64;         // hbuf_rows x kHP
+  float* stage = smem;                                         // NST x kChunkRows x SP
+  float* hbuf = smem + NST * kChunkRows * SP + 64;             // hbuf_rows x kHP
   float* wsm = hbuf + hbuf_floats(rmax, BH);                   // tap table
   float* wsmB = wsm + wtab_floats(tab.ntaps_total);            // shifted tap table w[i-1]
   uint64_t* bars = reinterpret_cast<uint64_t*>(wsmB + wtab_floats(tab.ntaps_total));
@@ -331,14 +334,14 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
 
   // zero stage and hbuf once: entries past a level's valid columns / rows are read only
   // against zero (padding) taps and must stay finite
-  const int nzero = kStages * kChunkRows * SP + 64 + hbuf_floats(rmax, BH);
+  const int nzero = NST * kChunkRows * SP + 64 + hbuf_floats(rmax, BH);
   for (int i = threadIdx.x; i < nzero; i += kThreads) smem[i] = 0.f;
   for (int i = threadIdx.x; i < tab.ntaps_total; i += kThreads) wsm[i] = tab.w[i];
   for (int l = 0; l < tab.nlev; ++l)  // wB = each level's taps shifted right by one (zero in front)
     for (int i = threadIdx.x; i < tab.ntap[l] + 8; i += kThreads)
       wsmB[tab.woff[l] + i] = i ? tab.w[tab.woff[l] + i - 1] : 0.f;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < kStages; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < NST; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const void* tm = use_tmap ? (const void*)&tmap : nullptr;
@@ -354,21 +357,19 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
 
   const int nlev = tab.nlev;
   uint32_t phases = 0u;   // bit k: parity of mbarrier k
-  // (lev, r0) of the items one and two ahead of the current one
+  // copy cursor: the (level, first row) of the next item to stage; items rotate through
+  // the NST buffers, NST-1 of them in flight ahead of the one being convolved
   auto rows_of = [BH](int R, int p) { return BH + 2 * R + p; };
-  int l1 = 0, q1 = 0, l2 = 0, q2 = 0;
-  {  // prologue: stage items 0 and 1
-    stage_rows<FAST>(stage, &bars[0], img, tm, b, s.W, s.H, x0, Y0, tab.R[0], tab.pre[0], 0,
-                     min(kChunkRows, rows_of(tab.R[0], tab.pre[0])), SP, warp, lane);
-    l1 = 0; q1 = kChunkRows;
-    if (q1 >= rows_of(tab.R[0], tab.pre[0])) { l1 = 1; q1 = 0; }
-    if (l1 < nlev) {
-      const int R1 = tab.R[l1], p1 = tab.pre[l1];
-      stage_rows<FAST>(stage + kChunkRows * SP, &bars[1], img, tm, b, s.W, s.H, x0, Y0, R1, p1, q1,
-                       min(kChunkRows, rows_of(R1, p1) - q1), SP, warp, lane);
-    }
-  }
-  int item = 0;           // (level, chunk) items rotate through the kStages buffers
+  int cl = 0, cq = 0;
+  auto stage_next = [&](int dst) {
+    if (cl >= nlev) return;
+    const int R = tab.R[cl], p = tab.pre[cl];
+    stage_rows<FAST>(stage + dst * kChunkRows * SP, &bars[dst], img, tm, b, s.W, s.H, x0, Y0, R, p, cq,
+                     min(kChunkRows, rows_of(R, p) - cq), SP, warp, lane);
+    cq += kChunkRows;
+    if (cq >= rows_of(R, p)) { ++cl; cq = 0; }
+  };
+  for (int k = 0; k + 1 < NST; ++k) stage_next(k);   // prologue
   int buf = 0;
 
   for (int lev = 0; lev < nlev; ++lev) {
@@ -378,18 +379,8 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
     const int nrow = rows_of(tab.R[lev], tab.pre[lev]);   // hbuf rows: band rows -R-p .. BH+R-1
 
     // ---------------- row pass (chunks of 32 rows) ----------------
-    for (int r0 = 0; r0 < nrow; r0 += kChunkRows, ++item) {
-      {  // prefetch item + 2 into the buffer freed by item - 1
-        l2 = l1; q2 = q1 + kChunkRows;
-        if (l2 < nlev && q2 >= rows_of(tab.R[l2], tab.pre[l2])) { ++l2; q2 = 0; }
-        if (l1 < nlev && l2 < nlev) {
-          const int R2 = tab.R[l2], p2 = tab.pre[l2];
-          const int b2 = buf == 0 ? 2 : buf - 1;
-          stage_rows<FAST>(stage + b2 * kChunkRows * SP, &bars[b2], img, tm, b, s.W, s.H, x0, Y0, R2, p2, q2,
-                           min(kChunkRows, rows_of(R2, p2) - q2), SP, warp, lane);
-        }
-        l1 = l2; q1 = q2;
-      }
+    for (int r0 = 0; r0 < nrow; r0 += kChunkRows) {
+      stage_next((buf + NST - 1) % NST);   // into the buffer the previous item freed
       if (FAST) {
         mbar_wait(&bars[buf], (phases >> buf) & 1u);
         phases ^= 1u << buf;
@@ -404,8 +395,8 @@ k_scale_space(const float* __restrict__ fimg, Shape s, const ImgPar* __restrict_
 #pragma unroll
         for (int o = 0; o < 4; ++o) h[o] = acc[o];
       }
-      buf = buf == 2 ? 0 : buf + 1;
-      __syncthreads();   // stage[item % 3] is free for the copy issued in the next iteration
+      buf = (buf + 1) % NST;
+      __syncthreads();   // this stage buffer is free for the copy issued in the next iteration
     }
 
     // ---------------- column pass + DoG + running argmax ----------------

@@ -350,9 +350,21 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // band height: 256 rows when that still gives >= 4 waves of 2 CTAs/SM, else 128
   const int64_t ctas256 = (int64_t)strips * ((H + 255) / 256) * B;
   const bool fits256 = scale_space_smem(c->tab->rmax, 256, c->tab->ntaps_total) <= kSmemLimit;
-  const int RPT = (fits256 && ctas256 >= (int64_t)c->sms * 2 * 4) ? 32 : 16;
+  int RPT = (fits256 && ctas256 >= (int64_t)c->sms * 2 * 4) ? 32 : 16;
+  int NST = kStages;
+  // large radii: 384-row bands with two copy stages (one CTA per SM) when the 256-row
+  // band does not fit, if that still gives >= 2 waves: the row pass recomputes
+  // (BH + 2R) / BH rows per output
+  {
+    const int64_t ctas384 = (int64_t)strips * ((H + 383) / 384) * B;
+    if (!fits256 && scale_space_smem(c->tab->rmax, 384, c->tab->ntaps_total, 2) <= kSmemLimit &&
+        ctas384 >= (int64_t)c->sms * 2 && getenv("MHFD_NO_BH384") == nullptr) {
+      RPT = 48;
+      NST = 2;
+    }
+  }
   const int BH = 8 * RPT;
-  const size_t smem = scale_space_smem(c->tab->rmax, BH, c->tab->ntaps_total);
+  const size_t smem = scale_space_smem(c->tab->rmax, BH, c->tab->ntaps_total, NST);
   const bool fast = fast_staging(W, c->tab->rmax);
   // 2-D TMA descriptor of the normalised batch viewed as a (B*H) x W f32 matrix
   CUtensorMap tmap;
@@ -373,10 +385,16 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   (paper && write_dog) ? launch_ss(k_scale_space<RPTV, true, true, FASTV>)                    \
   : paper              ? launch_ss(k_scale_space<RPTV, true, false, FASTV>)                   \
                        : launch_ss(k_scale_space<RPTV, false, true, FASTV>)
+#define SS_VARIANTS2(RPTV, FASTV)                                                             \
+  (paper && write_dog) ? launch_ss(k_scale_space<RPTV, true, true, FASTV, 2>)                 \
+  : paper              ? launch_ss(k_scale_space<RPTV, true, false, FASTV, 2>)                \
+                       : launch_ss(k_scale_space<RPTV, false, true, FASTV, 2>)
   cudaError_t es;
-  if (RPT == 32) es = fast ? (SS_VARIANTS(32, true)) : (SS_VARIANTS(32, false));
+  if (RPT == 48) es = fast ? (SS_VARIANTS2(48, true)) : (SS_VARIANTS2(48, false));
+  else if (RPT == 32) es = fast ? (SS_VARIANTS(32, true)) : (SS_VARIANTS(32, false));
   else es = fast ? (SS_VARIANTS(16, true)) : (SS_VARIANTS(16, false));
 #undef SS_VARIANTS
+#undef SS_VARIANTS2
   if (es != cudaSuccess) return cuda_fail(es, "k_scale_space");
   ++launches;
   MARK(2);
