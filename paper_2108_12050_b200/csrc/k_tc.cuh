@@ -176,7 +176,8 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" :::
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
-     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, int batch, int row_lo, int row_hi,
+     float* __restrict__ v_out, uint8_t* __restrict__ idx_out, float* __restrict__ dog_out, int batch,
+     int row_lo, int row_hi,
      unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int S = P.S, LW = tc_lw(P), OFF = tc_off(P);
@@ -300,6 +301,11 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         for (int uu = 0; uu < 16; ++uu) {
           const int u = 16 * hlf + uu;
           const float D = tf * (__uint_as_float(a[uu]) - __uint_as_float(b[uu]));
+          if (dog_out) {   // the DoG planes themselves (26-neighbour NMS, debug dumps)
+            const int x = ot.x0 + 32 * q + lane, y = ot.y0 + 32 * wg + u;
+            if (x < s.W && y < row_hi)
+              dog_out[((int64_t)ot.b * (P.nlev - 1) + (lev - 1)) * plane + (int64_t)y * s.W + x] = D;
+          }
           if (D > vbest[u]) {
             vbest[u] = D;
             const int sh = (u & 3) * 8;
@@ -309,6 +315,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
       }
     };
     auto write_out = [&]() {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
+      if (!v_out) return;
       const int x = ot.x0 + 32 * q + lane;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {

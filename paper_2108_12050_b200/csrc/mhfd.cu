@@ -273,8 +273,10 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   uint8_t* idx = reinterpret_cast<uint8_t*>(ws + L.idx);
   // ---- a2-a6 on u8 images on the tensor cores (banded-Toeplitz blur)
   const bool band = band_lo < band_hi;
-  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 3 && c->d_tctab &&
-      tc_ok(*c->tc, W, H)) {
+  // k_tc also writes the DoG planes: for the 26-neighbour NMS and for debug dumps
+  float* tc_dog = dog_dump ? dog_dump : (paper ? nullptr : reinterpret_cast<float*>(ws + L.dog));
+  if (bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
+      (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
     cudaError_t ea = cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -290,11 +292,11 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
                                                       (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
                                                       (uint32_t)P.S);
-    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, v, idx, B, r_lo, r_hi,
-                                            nullptr);
+    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, paper ? v : nullptr,
+                                            paper ? idx : nullptr, tc_dog, B, r_lo, r_hi, nullptr);
     LAUNCH_CHECK("k_tc");
     MARK(2);
-    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev, band_lo, band_hi);
+    return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
   }
   if (band) return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
   // ---- a2-a6 on u8 images, two-CTA band schedule
@@ -819,8 +821,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (!c) return "none";
   const int W = c->p.width, H = c->p.height;
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
   if (dtype == MHFD_U8 && paper && c->band_enabled) {
-    if (c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
