@@ -30,6 +30,7 @@
 #include "k_band.cuh"
 #include "k_band2.cuh"
 #include "k_tc.cuh"
+#include "k_twopass.cuh"
 
 using namespace mhfd;
 
@@ -46,6 +47,7 @@ struct mhfd_ctx {
   int sms;
   int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
   int band_kind;     // 3 = k_tc (default), 1 = k_band, 2 = k_band2; MHFD_SCHEDULE=tc|band|band2|generic
+  int twopass;       // generic path for large radii: k_rows2 / k_cols2 (MHFD_NO_TWOPASS=1 disables)
   TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
   uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
   float2* d_thr;     // pruning: n x n squared-distance bands (context-owned, immutable)
@@ -83,7 +85,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
-      chunkcnt, chunkpos, counters, scores, counts, total;
+      chunkcnt, chunkpos, counters, scores, counts, rx, lb0, lb1, total;
 };
 
 int nseg_of(const mhfd_ctx* c) {
@@ -121,6 +123,9 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.counters = take(sizeof(int32_t) * 8);
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
+  L.rx = take(c->twopass ? sizeof(float) * plane * B : 0);    // two-pass schedule intermediates
+  L.lb0 = take(c->twopass ? sizeof(float) * plane * B : 0);
+  L.lb1 = take(c->twopass ? sizeof(float) * plane * B : 0);
   L.total = o;
   return L;
 }
@@ -348,6 +353,26 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // ---- a3-a6: fused blur + DoG + argmax
   float* dog = dog_dump ? dog_dump : reinterpret_cast<float*>(ws + L.dog);
   const bool write_dog = dog_dump != nullptr || !paper;
+  if (c->twopass && W % kR2Cols == 0) {   // large radii: two passes per level through HBM
+    const LevelTable& T = *c->tab;
+    const size_t sm_r = rows2_smem(T.rmax), sm_c = cols2_smem(T.rmax);
+    cudaError_t ea = cudaFuncSetAttribute(k_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_r);
+    if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_cols2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+    if (ea != cudaSuccess) return cuda_fail(ea, "two-pass attributes");
+    float* rx = reinterpret_cast<float*>(ws + L.rx);
+    float* lb[2] = {reinterpret_cast<float*>(ws + L.lb0), reinterpret_cast<float*>(ws + L.lb1)};
+    const dim3 gr(W / kR2Cols, (H + 31) / 32, B), gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
+    for (int lev = 0; lev < T.nlev; ++lev) {
+      k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx);
+      LAUNCH_CHECK("k_rows2");
+      k_cols2<<<gc, 256, sm_c, st>>>(rx, W, H, T, lev, lev > 0 ? lb[(lev - 1) & 1] : nullptr,
+                                     lev + 1 < T.nlev ? lb[lev & 1] : nullptr, paper ? v : nullptr,
+                                     paper ? idx : nullptr, write_dog ? dog : nullptr, par);
+      LAUNCH_CHECK("k_cols2");
+    }
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
+  }
   const int strips = (W + kStripW - 1) / kStripW;
   // band height: 256 rows when that still gives >= 4 waves of 2 CTAs/SM, else 128
   const int64_t ctas256 = (int64_t)strips * ((H + 255) / 256) * B;
@@ -684,6 +709,12 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     return fail(MHFD_ERR_CUDA, "occupancy query for k_prune failed");
   }
   c->prune_grid = bps * c->sms;
+  {   // large radii: the two-pass generic schedule (no halo recompute) when the fused
+      // band kernel would recompute more than ~1.5x of its row pass
+    const char* nt = getenv("MHFD_NO_TWOPASS");
+    c->twopass = (rmax >= 96 && p->width % kR2Cols == 0 && !(nt && nt[0] == '1') &&
+                  rows2_smem(rmax) <= kSmemLimit && cols2_smem(rmax) <= kSmemLimit) ? 1 : 0;
+  }
   {
     const char* pg = getenv("MHFD_PRUNE_CTAS_PER_SM");   // tuning knob (<= the occupancy limit)
     if (pg && atoi(pg) > 0) c->prune_grid = std::min(bps, atoi(pg)) * c->sms;
@@ -826,7 +857,7 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
-  return "k_scale_space";
+  return c->twopass && W % kR2Cols == 0 ? "k_rows2+k_cols2" : "k_scale_space";
 }
 
 double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {
