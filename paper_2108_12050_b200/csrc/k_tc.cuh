@@ -173,6 +173,7 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" :::
 // Hazards: row(g) writes D1 after col(g-1) read A2 (in-order tcgen05.mma); col(g) writes
 // D2[g&1] (= L_{g-2}) after every warp's DoG of g-1 (it precedes their split arrivals);
 // B1 is restaged after rowDone of the tile's last level (waited before its split).
+template <bool DOG>   // DOG: also write every DoG plane to dog_out (26-neighbour NMS, dumps)
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
@@ -301,7 +302,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         for (int uu = 0; uu < 16; ++uu) {
           const int u = 16 * hlf + uu;
           const float D = tf * (__uint_as_float(a[uu]) - __uint_as_float(b[uu]));
-          if (dog_out) {   // the DoG planes themselves (26-neighbour NMS, debug dumps)
+          if (DOG) {   // the DoG planes themselves (26-neighbour NMS, debug dumps)
             const int x = ot.x0 + 32 * q + lane, y = ot.y0 + 32 * wg + u;
             if (x < s.W && y < row_hi)
               dog_out[((int64_t)ot.b * (P.nlev - 1) + (lev - 1)) * plane + (int64_t)y * s.W + x] = D;
@@ -315,7 +316,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
       }
     };
     auto write_out = [&]() {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
-      if (!v_out) return;
+      if (DOG && !v_out) return;
       const int x = ot.x0 + 32 * q + lane;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {

@@ -284,7 +284,8 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
-    cudaError_t ea = cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = tc_dog ? k_tc<true> : k_tc<false>;
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc attribute");
     // band mode: rows [band_lo - 1, band_hi + 1) on the whole image's 128-row tile grid, so
     // every pixel sees the same K-step grouping (and rounding) as in the whole-image run
@@ -297,7 +298,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
                                                       (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
                                                       (uint32_t)P.S);
-    k_tc<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, paper ? v : nullptr,
+    kern<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, paper ? v : nullptr,
                                             paper ? idx : nullptr, tc_dog, B, r_lo, r_hi, nullptr);
     LAUNCH_CHECK("k_tc");
     MARK(2);

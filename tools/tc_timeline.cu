@@ -38,12 +38,12 @@ int main(int argc, char** argv) {
   enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dimg, gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const size_t smem = tc_smem(P);
-  cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   Shape s{W, H, (int64_t)W, 1};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    k_tc<<<148, kTcThreads + 32, smem>>>(dimg, s, dpar, P, dtab, tm, 1, dv, didx, nullptr, B, 0, H, rep == 2 ? dtr : nullptr);
+    k_tc<false><<<148, kTcThreads + 32, smem>>>(dimg, s, dpar, P, dtab, tm, 1, dv, didx, nullptr, B, 0, H, rep == 2 ? dtr : nullptr);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
