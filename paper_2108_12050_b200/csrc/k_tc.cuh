@@ -293,14 +293,14 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
       const float tf = P.lev[lev - 1].tdog * oinv;
       const uint32_t cur = tq + 256 + 128 * (gg & 1) + 32 * wg, prv = tq + 256 + 128 * ((gg - 1) & 1) + 32 * wg;
 #pragma unroll
-      for (int hlf = 0; hlf < 2; ++hlf) {
-        uint32_t a[16], b[16];
-        umma::ld16(cur + 16 * hlf, a);
-        umma::ld16(prv + 16 * hlf, b);
+      for (int qq = 0; qq < 4; ++qq) {   // 8 rows at a time: fewer live registers (96 with 17 warps)
+        uint32_t a[8], b[8];
+        umma::ld8(cur + 8 * qq, a);
+        umma::ld8(prv + 8 * qq, b);
         umma::wait_ld();
 #pragma unroll
-        for (int uu = 0; uu < 16; ++uu) {
-          const int u = 16 * hlf + uu;
+        for (int uu = 0; uu < 8; ++uu) {
+          const int u = 8 * qq + uu;
           const float D = tf * (__uint_as_float(a[uu]) - __uint_as_float(b[uu]));
           if (DOG) {   // the DoG planes themselves (26-neighbour NMS, debug dumps)
             const int x = ot.x0 + 32 * q + lane, y = ot.y0 + 32 * wg + u;
