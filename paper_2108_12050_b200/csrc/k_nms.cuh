@@ -226,10 +226,13 @@ namespace mhfd {
 // segment bookkeeping as k_nms_count / k_nms_write.
 constexpr int kNmsRows = 2;   // output rows per warp in k_nms_rows (4: 2.98 ms, 2: 2.77 ms per 64 images)
 
+constexpr int kSlab = 32;    // records a segment parks in its slab during the count pass
+
 template <bool WRITE>
 __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* __restrict__ segcnt,
                                                   const int32_t* __restrict__ segoff, mhfd_blob* __restrict__ cand,
-                                                  int64_t cap, int row0, int row1) {
+                                                  int64_t cap, int row0, int row1,
+                                                  mhfd_blob* __restrict__ slab = nullptr) {
   // a warp owns kNmsRows vertically adjacent 1024-pixel segments (rows y0.., piece xs):
   // kNmsRows + 2 rows are loaded per step, so each v row leaves L2 1.5 times, not 3
   constexpr int NR = kNmsRows;
@@ -254,11 +257,12 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
   const float NEG = -INFINITY;
   const int seg0 = ((y0 - row0) * W + xseg) / kSeg;
   int64_t off[NR];
-  int total[NR];
+  int total[NR], parked[NR];
 #pragma unroll
   for (int o = 0; o < NR; ++o) {
     off[o] = (WRITE && y0 + o < row1) ? (int64_t)segoff[(int64_t)b * nseg + seg0 + o * spr] : 0;
     total[o] = 0;
+    parked[o] = 0;
   }
   mhfd_blob* out = WRITE ? cand + (int64_t)b * cap : nullptr;
   const uint8_t* ib = a.idx + (int64_t)b * H * W;
@@ -307,6 +311,30 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
       }
       if (y0 + o >= row1) bb = 0u;
       const int n = __popc(bb);
+      if (!WRITE && slab) {   // park this step's records in the segment's slab (raster order)
+        int incl = n;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, sh);
+          if (lane >= sh) incl += t;
+        }
+        int pos = parked[o] + incl - n;   // segment-wide running position
+        parked[o] += __shfl_sync(0xffffffffu, incl, 31);
+        const int y = y0 + o;
+        const uint8_t* irow = ib + (int64_t)y * W;
+        mhfd_blob* sl = slab + ((int64_t)b * nseg + seg0 + o * spr) * kSlab;
+        uint32_t m = bb;
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          if (pos < kSlab) {
+            mhfd_blob r;
+            r.x = x + k; r.y = y; r.scale = irow[x + k]; r.response = __ldg(rows[o + 1] + x + k);
+            sl[pos] = r;
+          }
+          ++pos;
+        }
+      }
       if (WRITE) {
         int incl = n;
 #pragma unroll
@@ -341,6 +369,44 @@ __global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* 
       for (int sh = 16; sh; sh >>= 1) t += __shfl_xor_sync(0xffffffffu, t, sh);
       if (lane == 0 && y0 + o < row1) segcnt[(int64_t)b * nseg + seg0 + o * spr] = t;
     }
+  }
+}
+
+// Gather after the scan: one warp per segment copies its parked records to its final
+// offset; a segment with more than kSlab candidates (its slab overflowed) re-evaluates
+// its 1024 pixels with the full predicate instead (same records, same order).
+__global__ void __launch_bounds__(256) k_nms_gather(NmsArgs a, int nseg, const int32_t* __restrict__ segcnt,
+                                                    const int32_t* __restrict__ segoff,
+                                                    const mhfd_blob* __restrict__ slab, mhfd_blob* __restrict__ cand,
+                                                    int64_t cap, int row0) {
+  const int b = blockIdx.y;
+  const int seg = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  const int cnt = segcnt[(int64_t)b * nseg + seg];
+  int64_t off = segoff[(int64_t)b * nseg + seg];
+  mhfd_blob* out = cand + (int64_t)b * cap;
+  if (cnt <= kSlab) {
+    if (lane < cnt && off + lane < cap) out[off + lane] = slab[((int64_t)b * nseg + seg) * kSlab + lane];
+    return;
+  }
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int64_t p0 = (int64_t)row0 * a.W + (int64_t)seg * kSeg;
+  for (int k = 0; k < kSeg; k += 32) {
+    const int64_t p = p0 + k + lane;
+    const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);
+    float val = 0.f;
+    const bool c = paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val);
+    const uint32_t m = __ballot_sync(0xffffffffu, c);
+    if (c) {
+      const int64_t pos = off + __popc(m & ((1u << lane) - 1u));
+      if (pos < cap) {
+        mhfd_blob r;
+        r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
+        out[pos] = r;
+      }
+    }
+    off += __popc(m);
   }
 }
 

@@ -85,7 +85,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
-      chunkcnt, chunkpos, counters, scores, counts, rx, lb0, lb1, total;
+      chunkcnt, chunkpos, counters, scores, counts, rx, lb0, lb1, slab, total;
 };
 
 int nseg_of(const mhfd_ctx* c) {
@@ -126,6 +126,8 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.rx = take(c->twopass ? sizeof(float) * plane * B : 0);    // two-pass schedule intermediates
   L.lb0 = take(c->twopass ? sizeof(float) * plane * B : 0);
   L.lb1 = take(c->twopass ? sizeof(float) * plane * B : 0);
+  // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
+  L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
   L.total = o;
   return L;
 }
@@ -204,11 +206,12 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   int32_t* segoff = reinterpret_cast<int32_t*>(ws + L.segoff);
   int32_t* ncand = reinterpret_cast<int32_t*>(ws + L.ncand);
   mhfd_blob* cand = reinterpret_cast<mhfd_blob*>(ws + L.cand);
+  mhfd_blob* slab = reinterpret_cast<mhfd_blob*>(ws + L.slab);
   dim3 gn((nseg + 7) / 8, B);
   const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
   const dim3 gr((((row1 - row0 + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // kNmsRows segments per warp
   if (rows_fast) {
-    k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1);
+    k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1, slab);
   } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
   } else {
@@ -217,8 +220,8 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   LAUNCH_CHECK("k_nms_count");
   k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
   LAUNCH_CHECK("k_seg_scan");
-  if (rows_fast) {
-    k_nms_rows<true><<<gr, 256, 0, st>>>(na, nseg, nullptr, segoff, cand, c->cap, row0, row1);
+  if (rows_fast) {   // parked records to their offsets (overflowing segments re-evaluated)
+    k_nms_gather<<<gn, 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
   } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {

@@ -385,3 +385,25 @@ def test_twopass_matches_fused_generic_bitwise():
     n = int(a["ncand"][0])
     assert torch.equal(a["cands"][0, :n], b["cands"][0, :n])
     assert ka == kb > 0 and torch.equal(ba[0, :ka], bb[0, :kb])
+
+
+def test_nms_dense_candidates_exact():
+    """Dense local maxima (uniform noise, tiny threshold): most 1024-pixel segments hold
+    more candidates than their count-pass slab (32), so the gather re-evaluates them.  The
+    candidate list must equal the oracle's Eq. 3 NMS applied to the GPU's own v (same f32
+    values, so the comparison is exact), in raster order, with the GPU's argmax."""
+    rng = np.random.default_rng(17)
+    img = rng.integers(0, 256, size=(1024, 1024), dtype=np.uint8)
+    det = mhfd.Detector(1024, 1024, min_sigma=1.0, max_sigma=3.0, num_scales=2, threshold=1e-6, overlap=1.0)
+    d = det.debug_dump(_to_t(img), dog=False, cands=True)
+    torch.cuda.synchronize()
+    v = d["v"][0].cpu().numpy().astype(np.float64)
+    ref = oracle.nms_paper(v[None], 1e-6)
+    n = int(d["ncand"][0])
+    assert n == len(ref) and n > 32 * 1024   # > 32 per segment on average
+    got = d["cands"][0, :n].cpu()
+    np.testing.assert_array_equal(got[:, 0].numpy(), ref["x"])
+    np.testing.assert_array_equal(got[:, 1].numpy(), ref["y"])
+    idx = d["idx"][0].cpu().numpy()
+    np.testing.assert_array_equal(got[:, 2].numpy(), idx[ref["y"], ref["x"]])
+    np.testing.assert_array_equal(got[:, 3].view(torch.float32).numpy().astype(np.float64), ref["response"])
