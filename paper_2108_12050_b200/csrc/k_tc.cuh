@@ -132,24 +132,36 @@ __device__ __forceinline__ void tc_stage_b1(const uint8_t* land, uint8_t* B1, in
   }
 }
 
-// D1 chunk j (16 f32 columns of this thread's lane) -> hi fp16 at 16j, lo fp16 at 16j+8
-__device__ __forceinline__ void tc_split_chunk(uint32_t tq, int j) {
-  uint32_t r[16];
-  umma::ld16(tq + 16 * j, r);
-  umma::wait_ld();
-  uint32_t h8[8], l8[8];
+// D1 chunk j (16 f32 columns of this thread's lane) -> hi fp16 at 16j, lo fp16 at 16j+8,
+// in two 8-column halves (fewer live registers).  In-place order: columns 16j..+7 are
+// read, their hi goes to 16j..+3 (already read); their lo waits until columns 16j+8..+15
+// have been read too, then lo(0-7) -> 16j+8..+11, hi(8-15) -> 16j+4..+7, lo(8-15) ->
+// 16j+12..+15.
+__device__ __forceinline__ void split_half(const uint32_t (&r)[8], uint32_t (&h4)[4], uint32_t (&l4)[4]) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < 4; ++u) {
     const float y0 = __uint_as_float(r[2 * u]) * (1.f / kTcWScale);
     const float y1 = __uint_as_float(r[2 * u + 1]) * (1.f / kTcWScale);
     const __half2 hh = __floats2half2_rn(y0, y1);
     const float2 hf = __half22float2(hh);
     const __half2 ll = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
-    h8[u] = *reinterpret_cast<const uint32_t*>(&hh);
-    l8[u] = *reinterpret_cast<const uint32_t*>(&ll);
+    h4[u] = *reinterpret_cast<const uint32_t*>(&hh);
+    l4[u] = *reinterpret_cast<const uint32_t*>(&ll);
   }
-  umma::st8(tq + 16 * j, h8);
-  umma::st8(tq + 16 * j + 8, l8);
+}
+__device__ __forceinline__ void tc_split_chunk(uint32_t tq, int j) {
+  const uint32_t base = tq + 16 * j;
+  uint32_t r[8], h4[4], l4a[4], l4b[4];
+  umma::ld8(base, r);
+  umma::wait_ld();
+  split_half(r, h4, l4a);
+  umma::st4(base, h4);            // hi(0-7) over columns 0-3: read already
+  umma::ld8(base + 8, r);
+  umma::wait_ld();
+  split_half(r, h4, l4b);
+  umma::st4(base + 4, h4);        // hi(8-15)
+  umma::st4(base + 8, l4a);       // lo(0-7): columns 8-11 have been read
+  umma::st4(base + 12, l4b);      // lo(8-15)
 }
 
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }   // epilogue warps only
