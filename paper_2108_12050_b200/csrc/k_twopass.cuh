@@ -41,7 +41,7 @@ __host__ __device__ inline size_t cols2_smem(int rmax) {
 __global__ void __launch_bounds__(256) k_rows2(const float* __restrict__ fimg, int W, int H,
                                                const __grid_constant__ LevelTable tab, int lev,
                                                float* __restrict__ rx) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int R = tab.R[lev], p = tab.pre[lev], ntap = tab.ntap[lev];
   const int SP = rows2_pitch(R, p);
   float* in = reinterpret_cast<float*>(smem_raw);              // 32 x SP
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256, 2) k_cols2(const float* __restrict__ rx, 
                                                   const float* __restrict__ lprev, float* __restrict__ lcur,
                                                   float* __restrict__ v, uint8_t* __restrict__ idx,
                                                   float* __restrict__ dog, const ImgPar* __restrict__ par) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int R = tab.R[lev], p = tab.pre[lev], ntap = tab.ntap[lev];
   float* hb = reinterpret_cast<float*>(smem_raw);              // cols2_rows x kHP
   const int b = blockIdx.z, Y0 = blockIdx.y * kC2Rows, x0 = blockIdx.x * kStripW;
