@@ -229,7 +229,7 @@ constexpr int kNmsRows = 2;   // output rows per warp in k_nms_rows (4: 2.98 ms,
 constexpr int kSlab = 32;    // records a segment parks in its slab during the count pass
 
 template <bool WRITE>
-__global__ void __launch_bounds__(256) k_nms_rows(NmsArgs a, int nseg, int32_t* __restrict__ segcnt,
+__global__ void __launch_bounds__(256, 4) k_nms_rows(NmsArgs a, int nseg, int32_t* __restrict__ segcnt,
                                                   const int32_t* __restrict__ segoff, mhfd_blob* __restrict__ cand,
                                                   int64_t cap, int row0, int row1,
                                                   mhfd_blob* __restrict__ slab = nullptr) {
