@@ -120,7 +120,7 @@ __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
   return blocked ? kUndecided : kKept;
 }
 
-__global__ void __launch_bounds__(256) k_prune(PruneArgs a) {
+__global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
