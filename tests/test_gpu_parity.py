@@ -164,7 +164,8 @@ def test_c2_sharp_beats_defocused():
     assert sc[0] > sc[1] > 0
 
 
-@pytest.mark.parametrize("shape,bits", [((257, 300), 8), ((300, 257), 16), ((51, 51), 8), ((77, 130), 16)])
+@pytest.mark.parametrize("shape,bits", [((257, 300), 8), ((300, 257), 16), ((51, 51), 8), ((77, 130), 16),
+                                        ((200, 1100), 8), ((1030, 250), 8), ((700, 1000), 8)])
 def test_ragged_and_minimum_shapes(shape, bits):
     H, W = shape
     img = synth.em_tile_np(H, W, 42, dose=300.0, bits=bits)
