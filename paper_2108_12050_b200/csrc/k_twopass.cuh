@@ -9,13 +9,11 @@
 //            columns, the 32 x (256 + 2R + p) input window staged by bulk copies (wrap at
 //            the image edge), conv4_row with lane = row, results transposed through
 //            shared memory into coalesced rows.
-//   k_cols2 (level i): L_i = column blur of Rx_i; CTA = 32 columns x 256 rows, the
-//            (256 + 2R + p) x 32 window of Rx_i in shared memory, conv8_col with lane =
-//            column; DoG_{i-1} = t_{i-1} (L_i - L_{i-1}) against L_{i-1} read back from
-//            HBM, running max / first argmax kept in v / idx (HBM); L_i written for the
-//            next level.
-// HBM per level and pixel: 4 (Rx) + 4 (Rx read, +halo through L2) + 4 (L_{i-1}) + 4
-// (L_i) + 10 (v / idx read-modify-write) bytes.
+//   k_cols_all (all levels): CTA = 32 columns x 256 rows; per level the (256 + 2R + p)
+//            x 32 window of Rx_i in shared memory, conv8_col with lane = column, DoG
+//            against L_{i-1} and the running max / first argmax in registers across the
+//            levels (one write of v / argmax per pixel at the end).
+// HBM per level and pixel: 4 (Rx write) + ~4-9 (Rx window reads, halo through L2) bytes.
 #pragma once
 #include "common.cuh"
 #include "k_scale_space.cuh"
@@ -98,56 +96,82 @@ __global__ void __launch_bounds__(256) k_rows2(const float* __restrict__ fimg, i
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_cols2(const float* __restrict__ rx, int W, int H,
-                                                  const __grid_constant__ LevelTable tab, int lev,
-                                                  const float* __restrict__ lprev, float* __restrict__ lcur,
-                                                  float* __restrict__ v, uint8_t* __restrict__ idx,
-                                                  float* __restrict__ dog, const ImgPar* __restrict__ par) {
+// Column pass over ALL levels of one 32-column x 256-row tile (replaces per-level k_cols2
+// launches): Rx of every level is in HBM (rx_all, level-major), each level's window is
+// staged into shared memory, L_{i-1}, the running max and the first argmax stay in
+// registers for the whole tile, so the only per-level HBM traffic is the Rx window.
+__global__ void __launch_bounds__(256, 2) k_cols_all(const float* __restrict__ rx_all, int W, int H, int B,
+                                                     const __grid_constant__ LevelTable tab,
+                                                     float* __restrict__ v, uint8_t* __restrict__ idx,
+                                                     float* __restrict__ dog, const ImgPar* __restrict__ par) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int R = tab.R[lev], p = tab.pre[lev], ntap = tab.ntap[lev];
-  float* hb = reinterpret_cast<float*>(smem_raw);              // cols2_rows x kHP
+  float* hb = reinterpret_cast<float*>(smem_raw);              // cols2_rows(rmax) x kHP
+  __shared__ __align__(16) float wsA[kMaxTaps / 4], wsB[kMaxTaps / 4];
   const int b = blockIdx.z, Y0 = blockIdx.y * kC2Rows, x0 = blockIdx.x * kStripW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const float* src = rx + (int64_t)b * H * W;
-  const int nr = kC2Rows + 2 * R + p + 16;                     // staged rows: band rows -R-p ..
-  {   // one coalesced 128-byte row piece per warp iteration (periodic in y)
-    int y = wrap_idx(Y0 - R - p + warp, H);
-    const bool inx = x0 + lane < W;
-    for (int r = warp; r < cols2_rows(R, p); r += 8) {
-      hb[r * kHP + lane] = (r < nr && inx) ? __ldg(src + (int64_t)y * W + x0 + lane) : 0.f;
-      y += 8;
-      if (y >= H) y -= H;
-    }
-  }
-  __shared__ __align__(16) float wsA[kMaxTaps / 4], wsB[kMaxTaps / 4];
-  const float* wA = tab.w + tab.woff[lev];
-  for (int i = tid; i < ntap + 8; i += 256) {
-    wsA[i] = wA[i];
-    wsB[i] = i ? wA[i - 1] : 0.f;
-  }
-  __syncthreads();
   const int64_t plane = (int64_t)H * W;
   const int x = x0 + lane;
-  const float tdog = lev > 0 ? tab.tdog[lev - 1] : 0.f;   // fimg is already stretched (k_normalize)
-  const bool degen = par[b].degen != 0;   // hi == lo: every DoG plane is exactly 0
+  const bool inx = x < W;
+  const bool degen = par[b].degen != 0;
+  float lprev[32], vbest[32];
+  uint32_t ibest[8];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int rb = warp * 32 + q * 8;
-    float acc[8];
-    conv8_col(acc, hb + rb * kHP + lane, kHP, wsA, wsB, ntap);
+  for (int u = 0; u < 32; ++u) { lprev[u] = 0.f; vbest[u] = -INFINITY; }
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      const int y = Y0 + rb + o;
-      if (x >= W || y >= H) continue;
-      const int64_t pi = (int64_t)b * plane + (int64_t)y * W + x;
-      const float L = acc[o];
-      if (lcur) lcur[pi] = L;
-      if (lev > 0) {
-        const float D = degen ? 0.f : tdog * (L - lprev[pi]);
-        if (dog) dog[((int64_t)b * (tab.nlev - 1) + (lev - 1)) * plane + (int64_t)y * W + x] = D;
-        if (v) {
-          if (lev == 1 || D > v[pi]) { v[pi] = D; idx[pi] = (uint8_t)(lev - 1); }
+  for (int u = 0; u < 8; ++u) ibest[u] = 0u;
+  for (int lev = 0; lev < tab.nlev; ++lev) {
+    const int R = tab.R[lev], p = tab.pre[lev], ntap = tab.ntap[lev];
+    const float* src = rx_all + ((int64_t)lev * B + b) * plane;
+    const int nr = kC2Rows + 2 * R + p + 16;
+    __syncthreads();   // the previous level's hb / taps are no longer read
+    {
+      int y = wrap_idx(Y0 - R - p + warp, H);
+      for (int r = warp; r < cols2_rows(R, p); r += 8) {
+        hb[r * kHP + lane] = (r < nr && inx) ? __ldg(src + (int64_t)y * W + x) : 0.f;
+        y += 8;
+        if (y >= H) y -= H;
+      }
+    }
+    const float* wA = tab.w + tab.woff[lev];
+    for (int i = tid; i < ntap + 8; i += 256) {
+      wsA[i] = wA[i];
+      wsB[i] = i ? wA[i - 1] : 0.f;
+    }
+    __syncthreads();
+    const float tdog = lev > 0 ? tab.tdog[lev - 1] : 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rb = warp * 32 + q * 8;
+      float acc[8];
+      conv8_col(acc, hb + rb * kHP + lane, kHP, wsA, wsB, ntap);
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int u = q * 8 + o;
+        const float L = acc[o];
+        if (lev > 0) {
+          const float D = degen ? 0.f : tdog * (L - lprev[u]);
+          if (dog) {
+            const int y = Y0 + rb + o;
+            if (inx && y < H) dog[((int64_t)b * (tab.nlev - 1) + (lev - 1)) * plane + (int64_t)y * W + x] = D;
+          }
+          if (D > vbest[u]) {
+            vbest[u] = D;
+            const int sh = (u & 3) * 8;
+            ibest[u >> 2] = (ibest[u >> 2] & ~(0xffu << sh)) | ((uint32_t)(lev - 1) << sh);
+          }
         }
+        lprev[u] = L;
+      }
+    }
+  }
+  if (v) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const int y = Y0 + warp * 32 + u;
+      if (inx && y < H) {
+        const int64_t pi = (int64_t)b * plane + (int64_t)y * W + x;
+        v[pi] = degen ? 0.f : vbest[u];
+        idx[pi] = degen ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
       }
     }
   }

@@ -85,7 +85,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
-      chunkcnt, chunkpos, counters, scores, counts, rx, lb0, lb1, slab, total;
+      chunkcnt, chunkpos, counters, scores, counts, rx, slab, total;
 };
 
 int nseg_of(const mhfd_ctx* c) {
@@ -123,9 +123,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.counters = take(sizeof(int32_t) * 8);
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
-  L.rx = take(c->twopass ? sizeof(float) * plane * B : 0);    // two-pass schedule intermediates
-  L.lb0 = take(c->twopass ? sizeof(float) * plane * B : 0);
-  L.lb1 = take(c->twopass ? sizeof(float) * plane * B : 0);
+  L.rx = take(c->twopass ? sizeof(float) * plane * B * (c->n + 1) : 0);   // two-pass: Rx of every level
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
   L.total = o;
@@ -361,19 +359,19 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     const LevelTable& T = *c->tab;
     const size_t sm_r = rows2_smem(T.rmax), sm_c = cols2_smem(T.rmax);
     cudaError_t ea = cudaFuncSetAttribute(k_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_r);
-    if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_cols2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
     if (ea != cudaSuccess) return cuda_fail(ea, "two-pass attributes");
     float* rx = reinterpret_cast<float*>(ws + L.rx);
-    float* lb[2] = {reinterpret_cast<float*>(ws + L.lb0), reinterpret_cast<float*>(ws + L.lb1)};
+    const int64_t plane = (int64_t)W * H;
     const dim3 gr(W / kR2Cols, (H + 31) / 32, B), gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
     for (int lev = 0; lev < T.nlev; ++lev) {
-      k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx);
+      k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx + (int64_t)lev * B * plane);
       LAUNCH_CHECK("k_rows2");
-      k_cols2<<<gc, 256, sm_c, st>>>(rx, W, H, T, lev, lev > 0 ? lb[(lev - 1) & 1] : nullptr,
-                                     lev + 1 < T.nlev ? lb[lev & 1] : nullptr, paper ? v : nullptr,
-                                     paper ? idx : nullptr, write_dog ? dog : nullptr, par);
-      LAUNCH_CHECK("k_cols2");
     }
+    ea = cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+    if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_all attribute");
+    k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
+                                      write_dog ? dog : nullptr, par);
+    LAUNCH_CHECK("k_cols_all");
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
   }
@@ -861,7 +859,7 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
-  return c->twopass && W % kR2Cols == 0 ? "k_rows2+k_cols2" : "k_scale_space";
+  return c->twopass && W % kR2Cols == 0 ? "k_rows2+k_cols_all" : "k_scale_space";
 }
 
 double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {

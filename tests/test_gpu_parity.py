@@ -375,7 +375,7 @@ def test_twopass_matches_fused_generic_bitwise():
             det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, **cfg)
         finally:
             os.environ.pop("MHFD_NO_TWOPASS", None)
-        assert det.schedule("u16") == ("k_rows2+k_cols2" if flag is None else "k_scale_space")
+        assert det.schedule("u16") == ("k_rows2+k_cols_all" if flag is None else "k_scale_space")
         d = det.debug_dump(img, dog=True, cands=True)
         blobs, cnt, _ = det.detect(img)
         torch.cuda.synchronize()
