@@ -21,7 +21,7 @@
 namespace mhfd {
 
 constexpr int kR2Cols = 256;   // k_rows2 output columns per CTA
-constexpr int kC2Rows = 256;   // k_cols2 output rows per CTA
+constexpr int kC2Rows = 256;   // k_cols_all output rows per CTA
 
 __host__ __device__ inline int rows2_pitch(int R, int p) {   // 4 x odd floats, >= window + overrun
   int q = (kR2Cols + 2 * R + p + 16 + 3) / 4;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) k_rows2(const float* __restrict__ fimg, i
   }
 }
 
-// Column pass over ALL levels of one 32-column x 256-row tile (replaces per-level k_cols2
+// Column pass over ALL levels of one 32-column x 256-row tile (instead of per-level column
 // launches): Rx of every level is in HBM (rx_all, level-major), each level's window is
 // staged into shared memory, L_{i-1}, the running max and the first argmax stay in
 // registers for the whole tile, so the only per-level HBM traffic is the Rx window.

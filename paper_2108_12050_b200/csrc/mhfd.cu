@@ -47,7 +47,7 @@ struct mhfd_ctx {
   int sms;
   int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
   int band_kind;     // 3 = k_tc (default), 1 = k_band, 2 = k_band2; MHFD_SCHEDULE=tc|band|band2|generic
-  int twopass;       // generic path for large radii: k_rows2 / k_cols2 (MHFD_NO_TWOPASS=1 disables)
+  int twopass;       // generic path for large radii: k_rows2 / k_cols_all (MHFD_NO_TWOPASS=1 disables)
   TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
   uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
   float2* d_thr;     // pruning: n x n squared-distance bands (context-owned, immutable)
