@@ -7,8 +7,8 @@
 //
 //   k_rows2 (level i): Rx_i = row blur of the centred image; CTA = 32 rows x 256 output
 //            columns, the 32 x (256 + 2R + p) input window staged by bulk copies (wrap at
-//            the image edge), conv4_row with lane = row, results transposed through
-//            shared memory into coalesced rows.
+//            the image edge), conv4_row with lane = row, 16-byte stores per lane (no
+//            transpose buffer: three CTAs per SM).
 //   k_cols_all (all levels): CTA = 32 columns x 256 rows; per level the (256 + 2R + p)
 //            x 32 window of Rx_i in shared memory, conv8_col with lane = column, DoG
 //            against L_{i-1} and the running max / first argmax in registers across the
@@ -29,7 +29,7 @@ __host__ __device__ inline int rows2_pitch(int R, int p) {   // 4 x odd floats, 
   return 4 * q;
 }
 __host__ __device__ inline size_t rows2_smem(int rmax) {
-  return sizeof(float) * ((size_t)32 * rows2_pitch(rmax, 3) + (size_t)32 * (kR2Cols + 4)) + 16;
+  return sizeof(float) * ((size_t)32 * rows2_pitch(rmax, 3)) + 16;
 }
 __host__ __device__ inline int cols2_rows(int R, int p) { return kC2Rows + 2 * R + p + 19; }
 __host__ __device__ inline size_t cols2_smem(int rmax) {
@@ -43,8 +43,7 @@ __global__ void __launch_bounds__(256) k_rows2(const float* __restrict__ fimg, i
   const int R = tab.R[lev], p = tab.pre[lev], ntap = tab.ntap[lev];
   const int SP = rows2_pitch(R, p);
   float* in = reinterpret_cast<float*>(smem_raw);              // 32 x SP
-  float* out = in + 32 * SP;                                   // 32 x (kR2Cols + 4)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(out + 32 * (kR2Cols + 4));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(in + 32 * SP);
   const int b = blockIdx.z, y0 = blockIdx.y * 32, x0 = blockIdx.x * kR2Cols;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const float* img = fimg + (int64_t)b * H * W;
@@ -81,18 +80,13 @@ __global__ void __launch_bounds__(256) k_rows2(const float* __restrict__ fimg, i
   }
   mbar_wait(bar, 0);
   __syncthreads();
-  // lane = row; warp w covers output columns 32 k + 4 w .. +4 for k = 0..7
+  // lane = row; warp w covers output columns 32 k + 4 w .. +4 for k = 0..7 (16-byte stores)
+  float* orow = rx + ((int64_t)b * H + y0 + lane) * W + x0;
   for (int k = 0; k < kR2Cols / 32; ++k) {
     const int c = 32 * k + 4 * warp;
     float acc[4];
     conv4_row(acc, in + lane * SP + c, wsA, wsB, ntap);
-    *reinterpret_cast<float4*>(out + lane * (kR2Cols + 4) + c) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  }
-  __syncthreads();
-  for (int i = tid; i < nrow * (kR2Cols / 4); i += 256) {   // coalesced rows
-    const int r = i / (kR2Cols / 4), c4 = i % (kR2Cols / 4);
-    *reinterpret_cast<float4*>(rx + ((int64_t)b * H + y0 + r) * W + x0 + 4 * c4) =
-        *reinterpret_cast<const float4*>(out + r * (kR2Cols + 4) + 4 * c4);
+    if (lane < nrow) *reinterpret_cast<float4*>(orow + c) = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
 }
 
