@@ -17,6 +17,7 @@
 #pragma once
 #include "common.cuh"
 #include "k_scale_space.cuh"
+#include "k_band.cuh"
 
 namespace mhfd {
 
@@ -166,6 +167,168 @@ __global__ void __launch_bounds__(256, 2) k_cols_all(const float* __restrict__ r
         const int64_t pi = (int64_t)b * plane + (int64_t)y * W + x;
         v[pi] = degen ? 0.f : vbest[u];
         idx[pi] = degen ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+      }
+    }
+  }
+}
+
+// Column pass over all levels, paper mode (no DoG planes): the same tile and the same
+// register-resident L_{i-1} / max / first argmax as k_cols_all, but the conv is the u8
+// band kernel's col_pass (8 rows x 2 columns per thread, float2 loads, column-pair FFMA2
+// with a broadcast tap: 4 FFMA2 per shared load where conv8_col issues 2, which left
+// conv8_col load-issue bound at ~31 % FMA activity), and the next level's Rx window is
+// prefetched with cp.async into a second buffer while the current level convolves.
+// Same taps, f32, summed in tap order d = -R..R in one accumulator per pixel (conv8_col
+// sums two interleaved partial sums), so results agree with k_cols_all to rounding, not
+// bit for bit; the DoG-dump path keeps k_cols_all.
+constexpr int kC3Threads = 512;
+__host__ __device__ inline int c3_taps(int R) { return ((2 * R + 1 + 15) & ~15) + 16; }   // zero-padded
+__host__ __device__ inline int c3_rows(int R) { return kC2Rows + ((2 * R + 1 + 15) & ~15) + 24; }
+__host__ __device__ inline int c3_buf_floats(int rmax) { return c3_rows(rmax) * kBandHP + c3_taps(rmax); }
+__host__ __device__ inline size_t c3_smem(int rmax) { return sizeof(float) * 2 * (size_t)c3_buf_floats(rmax) + 16; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __restrict__ rx_all, int W, int H, int B,
+                                                             const __grid_constant__ LevelTable tab,
+                                                             float* __restrict__ v, uint8_t* __restrict__ idx,
+                                                             const ImgPar* __restrict__ par) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* buf0 = reinterpret_cast<float*>(smem_raw);
+  const int bufsz = c3_buf_floats(tab.rmax);
+  const int b = blockIdx.z, Y0 = blockIdx.y * kC2Rows, x0 = blockIdx.x * kStripW;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t plane = (int64_t)H * W;
+  // stage level `lev` into buffer `k`: rows Y0 - R .. (c3_rows), wrapped; taps 0..2R
+  auto stage = [&](int lev, int k) {
+    float* hb = buf0 + k * bufsz;
+    float* wc = hb + c3_rows(tab.rmax) * kBandHP;
+    const int R = tab.R[lev];
+    const float* src = rx_all + ((int64_t)lev * B + b) * plane + x0;
+    const int nr = c3_rows(R);
+    for (int i = tid; i < nr * 8; i += kC3Threads) {
+      const int r = i >> 3, c = i & 7;
+      int y = (Y0 - R + r) % H;
+      if (y < 0) y += H;
+      cp_async16(hb + r * kBandHP + 4 * c, src + (int64_t)y * W + 4 * c);
+    }
+    const float* w = tab.w + tab.woff[lev] + tab.pre[lev];
+    for (int i = tid; i < c3_taps(R); i += kC3Threads) wc[i] = i < 2 * R + 1 ? w[i] : 0.f;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int cp = lane & 15;
+  const int rg = 2 * warp + (lane >> 4);
+  float lprev[16], vbest[16];
+  uint32_t ibest[4];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) { lprev[k] = 0.f; vbest[k] = -INFINITY; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ibest[k] = 0u;
+  stage(0, 0);
+  for (int lev = 0; lev < tab.nlev; ++lev) {
+    if (lev + 1 < tab.nlev) {
+      stage(lev + 1, (lev + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();   // level lev's window and taps are in
+    const float* hb = buf0 + (lev & 1) * bufsz;
+    const float* wc = hb + c3_rows(tab.rmax) * kBandHP;
+    col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, lev,
+                      lev > 0 ? tab.tdog[lev - 1] : 0.f, lprev, vbest, ibest);
+    __syncthreads();   // buffer lev & 1 is free for level lev + 2
+  }
+  const bool degen = par[b].degen != 0;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    const int y = Y0 + 8 * rg + o;
+    if (y < H) {
+      const int64_t pi = (int64_t)b * plane + (int64_t)y * W + x0 + 2 * cp;
+      const int k = 2 * o;
+      *reinterpret_cast<float2*>(v + pi) = degen ? make_float2(0.f, 0.f) : make_float2(vbest[k], vbest[k + 1]);
+      const uint32_t i0 = (ibest[k >> 2] >> ((k & 3) * 8)) & 0xffu, i1 = (ibest[(k + 1) >> 2] >> (((k + 1) & 3) * 8)) & 0xffu;
+      *reinterpret_cast<uchar2*>(idx + pi) = degen ? make_uchar2(0, 0) : make_uchar2((uint8_t)i0, (uint8_t)i1);
+    }
+  }
+}
+
+// Row pass over ALL levels of one 32-row x 256-column tile, paper mode (pairs with
+// k_cols_pair): the centred image window (32 rows x 256 + 2 R_max + pad columns) is staged
+// ONCE, transposed (column-major, pitch kBandHP), and every level's row blur is col_pass
+// run along x on that buffer (8 outputs along x x 2 rows per thread, row-pair FFMA2 with a
+// broadcast tap), written to Rx_i.  Against k_rows2 (one launch per level, the window
+// re-staged per level, conv4_row at ~40 % FMA activity) the staging is amortised over the
+// levels and the FFMA2 : shared-load ratio is 4 : 1.  Tap-order f32 sums.
+constexpr int kR3Cols = 256;
+__host__ __device__ inline int r3_pre(int rmax) { return (4 - rmax % 4) % 4; }
+__host__ __device__ inline int r3_nx(int rmax) { return (2 * rmax + r3_pre(rmax) + 288 + 7) & ~7; }
+__host__ __device__ inline int r3_taps_total(const LevelTable& t) {
+  int n = 0;
+  for (int l = 0; l < t.nlev; ++l) n += c3_taps(t.R[l]);
+  return n;
+}
+__host__ __device__ inline size_t r3_smem(int rmax, int taps_total) {
+  return sizeof(float) * ((size_t)r3_nx(rmax) * kBandHP + taps_total) + 16;
+}
+
+__global__ void __launch_bounds__(kC3Threads, 1) k_rows_pair(const float* __restrict__ fimg, int W, int H,
+                                                             const __grid_constant__ LevelTable tab,
+                                                             float* __restrict__ rx_all, int B) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* T = reinterpret_cast<float*>(smem_raw);                 // r3_nx x kBandHP, T[xi][row]
+  const int NX = r3_nx(tab.rmax);
+  float* wc_all = T + NX * kBandHP;
+  const int b = blockIdx.z, y0 = blockIdx.y * 32, x0 = blockIdx.x * kR3Cols;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t plane = (int64_t)H * W;
+  const int pm = r3_pre(tab.rmax);
+  const int xs = x0 - tab.rmax - pm;                             // multiple of 4
+  {
+    // lane = row (conflict-free transposed stores), 32 contiguous bytes of that row per chunk
+    const float* row = fimg + (int64_t)b * plane + (int64_t)min(y0 + lane, H - 1) * W;
+    for (int q = warp; q < NX / 8; q += kC3Threads / 32) {
+      int xa = (xs + 8 * q) % W;
+      if (xa < 0) xa += W;
+      int xb = xa + 4;
+      if (xb >= W) xb -= W;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(row + xa));
+      const float4 c = __ldg(reinterpret_cast<const float4*>(row + xb));
+      float* d = T + (8 * q) * kBandHP + lane;
+      d[0 * kBandHP] = a.x; d[1 * kBandHP] = a.y; d[2 * kBandHP] = a.z; d[3 * kBandHP] = a.w;
+      d[4 * kBandHP] = c.x; d[5 * kBandHP] = c.y; d[6 * kBandHP] = c.z; d[7 * kBandHP] = c.w;
+    }
+    int off = 0;
+    for (int l = 0; l < tab.nlev; ++l) {
+      const int R = tab.R[l], n = c3_taps(R);
+      const float* w = tab.w + tab.woff[l] + tab.pre[l];
+      for (int i = tid; i < n; i += kC3Threads) wc_all[off + i] = i < 2 * R + 1 ? w[i] : 0.f;
+      off += n;
+    }
+  }
+  __syncthreads();
+  const int cp = lane & 15;                  // row pair 2cp, 2cp + 1
+  const int rg = 2 * warp + (lane >> 4);     // output columns 8 rg .. 8 rg + 7
+  float L[16], vd[16];
+  uint32_t id[4];
+  int off = 0;
+  for (int lev = 0; lev < tab.nlev; ++lev) {
+    const int R = tab.R[lev];
+    col_pass<kBandHP>(T + (tab.rmax + pm - R + 8 * rg) * kBandHP + 2 * cp, wc_all + off, 2 * R + 1, 0, 0.f, L, vd,
+                      id);
+    off += c3_taps(R);
+    float* out = rx_all + ((int64_t)lev * B + b) * plane + x0 + 8 * rg;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int y = y0 + 2 * cp + c;
+      if (y < H) {
+        float4* o4 = reinterpret_cast<float4*>(out + (int64_t)y * W);
+        o4[0] = make_float4(L[0 + c], L[2 + c], L[4 + c], L[6 + c]);
+        o4[1] = make_float4(L[8 + c], L[10 + c], L[12 + c], L[14 + c]);
       }
     }
   }

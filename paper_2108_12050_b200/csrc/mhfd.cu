@@ -363,15 +363,33 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     float* rx = reinterpret_cast<float*>(ws + L.rx);
     const int64_t plane = (int64_t)W * H;
     const dim3 gr(W / kR2Cols, (H + 31) / 32, B), gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
-    for (int lev = 0; lev < T.nlev; ++lev) {
-      k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx + (int64_t)lev * B * plane);
-      LAUNCH_CHECK("k_rows2");
+    const bool pair = !write_dog && c3_smem(T.rmax) <= kSmemLimit &&
+                      r3_smem(T.rmax, r3_taps_total(T)) <= kSmemLimit && getenv("MHFD_NO_COLS_PAIR") == nullptr;
+    if (pair) {   // paper mode: all levels' row blur in one launch
+      const size_t sm_p = r3_smem(T.rmax, r3_taps_total(T));
+      ea = cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
+      if (ea != cudaSuccess) return cuda_fail(ea, "k_rows_pair attribute");
+      k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, B), kC3Threads, sm_p, st>>>(fimg, W, H, T, rx, B);
+      LAUNCH_CHECK("k_rows_pair");
+    } else {
+      for (int lev = 0; lev < T.nlev; ++lev) {
+        k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx + (int64_t)lev * B * plane);
+        LAUNCH_CHECK("k_rows2");
+      }
     }
-    ea = cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
-    if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_all attribute");
-    k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
-                                      write_dog ? dog : nullptr, par);
-    LAUNCH_CHECK("k_cols_all");
+    if (pair) {
+      const size_t sm_3 = c3_smem(T.rmax);
+      ea = cudaFuncSetAttribute(k_cols_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
+      if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_pair attribute");
+      k_cols_pair<<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, v, idx, par);
+      LAUNCH_CHECK("k_cols_pair");
+    } else {
+      ea = cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+      if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_all attribute");
+      k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
+                                        write_dog ? dog : nullptr, par);
+      LAUNCH_CHECK("k_cols_all");
+    }
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
   }

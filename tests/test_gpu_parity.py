@@ -377,8 +377,12 @@ def test_twopass_matches_fused_generic_bitwise():
             os.environ.pop("MHFD_NO_TWOPASS", None)
         assert det.schedule("u16") == ("k_rows2+k_cols_all" if flag is None else "k_scale_space")
         d = det.debug_dump(img, dog=True, cands=True)
-        blobs, cnt, _ = det.detect(img)
-        torch.cuda.synchronize()
+        os.environ["MHFD_NO_COLS_PAIR"] = "1"   # paper mode: k_cols_all, not k_cols_pair
+        try:
+            blobs, cnt, _ = det.detect(img)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("MHFD_NO_COLS_PAIR", None)
         outs.append((d, blobs, int(cnt[0])))
     (a, ba, ka), (b, bb, kb) = outs
     for key in ("lohi", "dog", "v", "idx", "ncand"):
@@ -386,6 +390,47 @@ def test_twopass_matches_fused_generic_bitwise():
     n = int(a["ncand"][0])
     assert torch.equal(a["cands"][0, :n], b["cands"][0, :n])
     assert ka == kb > 0 and torch.equal(ba[0, :ka], bb[0, :kb])
+
+
+def test_cols_pair_matches_cols_all():
+    """k_rows_pair + k_cols_pair (paper-mode passes of the two-pass schedule: tap-order
+    sums, 8x2 pixels per thread) against k_rows2 + k_cols_all (conv4_row / conv8_col):
+    the same f32 taps, so v agrees to a few ulp of the level sums; the argmax agrees except
+    at near-ties; the kept blob count agrees within a few near-threshold blobs.  Ragged
+    last band (H = 1000) and a degenerate (constant) image in the batch."""
+    import os
+    imgs = [synth.em_tile(1000, 1024, 1105 + k, defocus=0.5 * k, dose=300.0, bits=16, device="cuda") for k in range(2)]
+    imgs.append(torch.full((1000, 1024), 777, dtype=torch.int32))
+    img = torch.from_numpy(np.stack([t.to(torch.int32).cpu().numpy() for t in imgs]).astype(np.uint16))
+    det = mhfd.Detector(1024, 1000, min_sigma=1.0, max_sigma=20.0, num_scales=12, threshold=0.1 * 19.0 / 12)
+    assert det.schedule("u16") == "k_rows2+k_cols_all"
+    res = []
+    for flag in (None, "1"):
+        if flag:
+            os.environ["MHFD_NO_COLS_PAIR"] = flag
+        try:
+            d = det.debug_dump(img, dog=False, cands=False)
+            blobs, cnt, _ = det.detect(img)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("MHFD_NO_COLS_PAIR", None)
+        res.append((d["v"].cpu(), d["idx"].cpu(), cnt.cpu()))
+    (va, ia, ca), (vb, ib, cb) = res
+    scale = float(vb.abs().max())
+    diff = float((va - vb).abs().max())
+    mism = float((ia != ib).float().mean())
+    print(f"cols_pair: max|dv| {diff:.3e} (max|v| {scale:.3e}), argmax mismatch {mism:.2e}, counts {ca.tolist()} {cb.tolist()}")
+    # both sides sum the same 2R+1 <= 201 f32 products per pass (|x| <= 1 normalised,
+    # taps summing to 1), each pass within (2R+1) u of the exact sum, and the column pass
+    # carries the row pass's error through taps summing to 1; the DoG scales the
+    # difference of two levels by t_i <= 20: |dv| <= 20 * 2 * 2 * 201 * 2^-24 = 9.6e-4
+    # (worst case); typical errors are random-walk sized, so the mean is held far lower
+    assert diff <= 9.6e-4, (diff, scale)
+    assert float((va - vb).abs().mean()) <= 1e-6
+    assert mism < 1e-3
+    assert float(va[2].abs().max()) == 0.0 and int(ia[2].max()) == 0 and int(ca[2]) == 0
+    for k in range(2):
+        assert abs(int(ca[k]) - int(cb[k])) <= max(2, int(cb[k]) // 500), (k, int(ca[k]), int(cb[k]))
 
 
 def test_nms_dense_candidates_exact():
