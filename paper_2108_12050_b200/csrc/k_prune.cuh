@@ -49,7 +49,10 @@ struct PruneArgs {
   int64_t* chunk_off;       // B + 1: prefix of chunk counts
   int32_t* chunk_cnt;       // kept per chunk
   int32_t* chunk_pos;       // exclusive kept offsets per chunk (within the image)
-  int32_t* counters;        // 4 ints: undecided counters (3) + round count
+  int32_t* counters;        // 8 ints: undecided counters (3), round count, worklist length
+  int4* wl;                 // worklist of blobs undecided after round 0: 2 int4 per record
+                            // {k_global, cnt, q0, q1}, {q2, q3, q4, q5}; cnt = kNbMax + 1: list overflow
+  int64_t wl_cap;           // records
   mhfd_blob* blobs;         // nullable: B x blob_cap output
   int32_t blob_cap;
   int32_t* counts;          // nullable
@@ -80,18 +83,25 @@ __device__ __forceinline__ int image_of(const int64_t* off, int B, int64_t g) {
   return lo;
 }
 
-__device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
+constexpr int kNbMax = 6;   // neighbour indices kept per worklist record
+
+// Scan the candidates around blob k for higher-priority blobs that overlap it by more
+// than `overlap`; rows ylo + r0, ylo + r0 + rstep, ...  Returns true as soon as one of
+// them is KEPT (k is then REMOVED); otherwise sets *blocked if one is UNDECIDED and
+// passes every overlapping one to rec(q).
+template <class Rec>
+__device__ __forceinline__ bool scan_rows(const PruneArgs& a, int b, int64_t k, int r0, int rstep, bool* blocked,
+                                          Rec rec) {
   const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
   const uint8_t* st = a.st + (int64_t)b * a.cap;
   const mhfd_blob me = C[k];
   const double r = a.rad[me.scale];
   const int Dm = a.dmax[me.scale];
   const float2* th = a.thr + me.scale * a.n;
-  bool blocked = false;
   const int ylo = max(0, me.y - Dm), yhi = min(a.H - 1, me.y + Dm);
   const int kb0 = max(0, me.x - Dm) >> 5, kb1 = min(a.nbx, ((me.x + Dm) >> 5) + 1);
   const int32_t* ri = a.rbi + (int64_t)b * a.H * (a.nbx + 1);
-  for (int yy = ylo; yy <= yhi; ++yy) {
+  for (int yy = ylo + r0; yy <= yhi; yy += rstep) {
     const int32_t* rrow = ri + (int64_t)yy * (a.nbx + 1);
     const int lo = __ldcg(rrow + kb0), hi = __ldcg(rrow + kb1);
     for (int q = lo; q < hi; ++q) {
@@ -112,9 +122,46 @@ __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
                                      : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.scale]) > a.overlap;
       if (over) {
         const uint8_t s = __ldcg(st + q);
-        if (s == kKept) return kRemoved;
-        if (s == kUndecided) blocked = true;
+        if (s == kKept) return true;
+        if (s == kUndecided) *blocked = true;
+        rec(q);
       }
+    }
+  }
+  return false;
+}
+
+__device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
+  bool blocked = false;
+  if (scan_rows(a, b, k, 0, 1, &blocked, [](int) {})) return kRemoved;
+  return blocked ? kUndecided : kKept;
+}
+
+// round-0 decision of blob k that also records its overlapping higher-priority
+// neighbours (all of them: a blob that stays UNDECIDED scanned every row)
+__device__ uint8_t decide_collect(const PruneArgs& a, int b, int64_t k, int* nq, int (&qs)[kNbMax]) {
+  bool blocked = false;
+  int n = 0;
+  if (scan_rows(a, b, k, 0, 1, &blocked, [&](int q) {
+        if (n < kNbMax) qs[n] = q;
+        ++n;
+      }))
+    return kRemoved;
+  *nq = n;
+  return blocked ? kUndecided : kKept;
+}
+
+// later rounds: the recorded neighbours decide (no geometric search)
+__device__ uint8_t decide_list(const PruneArgs& a, int b, const int4& r0, const int4& r1) {
+  const uint8_t* st = a.st + (int64_t)b * a.cap;
+  const int q[kNbMax] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  bool blocked = false;
+#pragma unroll
+  for (int i = 0; i < kNbMax; ++i) {
+    if (i < r0.y) {
+      const uint8_t s = __ldcg(st + q[i]);
+      if (s == kKept) return kRemoved;
+      if (s == kUndecided) blocked = true;
     }
   }
   return blocked ? kUndecided : kKept;
@@ -141,6 +188,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     a.chunk_off[a.B] = c;
     a.counters[0] = a.counters[1] = a.counters[2] = 0;
     a.counters[3] = 0;
+    a.counters[4] = 0;
   }
   grid.sync();
   const int64_t total = a.img_off[a.B];
@@ -182,24 +230,100 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   }
   grid.sync();
 
-  // phase 2: decision rounds
+  // phase 2: decision rounds.  Round 0 visits every blob; a blob it leaves UNDECIDED is
+  // appended to the worklist with its overlapping higher-priority neighbours, and later
+  // rounds visit only the worklist, deciding from those lists (a list that overflowed
+  // kNbMax, or a full worklist, falls back to the geometric search).  Small inputs (one
+  // tile) run round 0 one warp per blob, the rows of its search window split over the
+  // lanes: the serial chain of dependent row-index loads, not throughput, bounds them.
   if (a.prune) {
-    for (int round = 0;; ++round) {
-      if (gtid == 0) a.counters[(round + 1) % 3] = 0;
-      int undecided = 0;
+    const int64_t gw = gtid >> 5, nwarps = gsize >> 5;
+    const int lane0 = threadIdx.x & 31;
+    int undecided = 0;
+    if (gtid == 0) a.counters[1] = 0;
+    auto append = [&](int64_t g, int nq, const int (&qs)[kNbMax]) -> bool {
+      const int pos = atomicAdd(&a.counters[4], 1);
+      if (pos >= a.wl_cap) return false;
+      a.wl[2 * pos] = make_int4((int)g, nq > kNbMax ? kNbMax + 1 : nq, qs[0], qs[1]);
+      a.wl[2 * pos + 1] = make_int4(qs[2], qs[3], qs[4], qs[5]);
+      return true;
+    };
+    if (total * 32 <= gsize * 4) {   // warp per blob
+      __shared__ int wq[8][kNbMax + 1];
+      const int wib = threadIdx.x >> 5;
+      for (int64_t g = gw; g < total; g += nwarps) {
+        const int b = image_of(a.img_off, a.B, g);
+        const int64_t k = g - a.img_off[b];
+        if (lane0 == 0) wq[wib][kNbMax] = 0;
+        __syncwarp();
+        bool blocked = false;
+        const bool rem = scan_rows(a, b, k, lane0, 32, &blocked, [&](int q) {
+          const int pos = atomicAdd(&wq[wib][kNbMax], 1);
+          if (pos < kNbMax) wq[wib][pos] = q;
+        });
+        const bool any_rem = __any_sync(0xffffffffu, rem);
+        const bool any_blk = __any_sync(0xffffffffu, blocked);
+        __syncwarp();
+        if (lane0 == 0) {
+          uint8_t d = any_rem ? kRemoved : any_blk ? kUndecided : kKept;
+          if (d == kUndecided) {
+            int qs[kNbMax];
+            for (int i = 0; i < kNbMax; ++i) qs[i] = wq[wib][i];
+            ++undecided;
+            append(g, wq[wib][kNbMax], qs);
+          }
+          if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
+        }
+        __syncwarp();
+      }
+    } else {
       for (int64_t g = gtid; g < total; g += gsize) {
         const int b = image_of(a.img_off, a.B, g);
         const int64_t k = g - a.img_off[b];
-        uint8_t* sp = a.st + (int64_t)b * a.cap + k;
-        if (__ldcg(sp) != kUndecided) continue;
-        const uint8_t d = decide(a, b, k);
-        if (d != kUndecided) __stcg(sp, d); else ++undecided;
+        int nq = 0, qs[kNbMax] = {0, 0, 0, 0, 0, 0};
+        const uint8_t d = decide_collect(a, b, k, &nq, qs);
+        if (d != kUndecided) {
+          __stcg(a.st + (int64_t)b * a.cap + k, d);
+        } else {
+          ++undecided;
+          append(g, nq, qs);
+        }
+      }
+    }
+    if (undecided) atomicAdd(&a.counters[0], undecided);
+    grid.sync();
+    int left = *((volatile int32_t*)&a.counters[0]);
+    const int64_t nwl = *((volatile int32_t*)&a.counters[4]);
+    const bool full = nwl > a.wl_cap;   // some undecided blob is not on the list
+    if (gtid == 0) a.counters[3] = 1;
+    for (int round = 1; left > 0; ++round) {
+      if (gtid == 0) a.counters[(round + 1) % 3] = 0;
+      undecided = 0;
+      if (!full) {
+        for (int64_t i = gtid; i < nwl; i += gsize) {
+          const int4 r0 = a.wl[2 * i];
+          const int64_t g = r0.x;
+          const int b = image_of(a.img_off, a.B, g);
+          const int64_t k = g - a.img_off[b];
+          uint8_t* sp = a.st + (int64_t)b * a.cap + k;
+          if (__ldcg(sp) != kUndecided) continue;
+          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1]) : decide(a, b, k);
+          if (d != kUndecided) __stcg(sp, d); else ++undecided;
+        }
+      } else {
+        for (int64_t g = gtid; g < total; g += gsize) {
+          const int b = image_of(a.img_off, a.B, g);
+          const int64_t k = g - a.img_off[b];
+          uint8_t* sp = a.st + (int64_t)b * a.cap + k;
+          if (__ldcg(sp) != kUndecided) continue;
+          const uint8_t d = decide(a, b, k);
+          if (d != kUndecided) __stcg(sp, d); else ++undecided;
+        }
       }
       if (undecided) atomicAdd(&a.counters[round % 3], undecided);
       grid.sync();
-      const int left = *((volatile int32_t*)&a.counters[round % 3]);
+      left = *((volatile int32_t*)&a.counters[round % 3]);
       if (gtid == 0) a.counters[3] = round + 1;
-      if (left == 0) break;
     }
   }
   grid.sync();

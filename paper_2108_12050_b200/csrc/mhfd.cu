@@ -85,12 +85,19 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
-      chunkcnt, chunkpos, counters, scores, counts, rx, slab, total;
+      chunkcnt, chunkpos, counters, scores, counts, rx, slab, wl, total;
 };
 
 int nseg_of(const mhfd_ctx* c) {
   const int64_t plane = (int64_t)c->p.width * c->p.height;
   return (int)((plane + kSeg - 1) / kSeg);
+}
+
+// pruning worklist capacity (records of blobs left undecided by round 0; overflow falls
+// back to the geometric search, so this is a size/speed trade, not a correctness bound)
+int64_t wl_cap_of(const mhfd_ctx* c, int B) {
+  const int64_t all = c->cap * (int64_t)B;
+  return std::min(all, ((int64_t)1 << 20) + all / 64);
 }
 
 Layout layout(const mhfd_ctx* c, int B) {
@@ -126,6 +133,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.rx = take(c->twopass ? sizeof(float) * plane * B * (c->n + 1) : 0);   // two-pass: Rx of every level
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
+  L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
   L.total = o;
   return L;
 }
@@ -476,6 +484,8 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   pa.chunk_cnt = reinterpret_cast<int32_t*>(ws + L.chunkcnt);
   pa.chunk_pos = reinterpret_cast<int32_t*>(ws + L.chunkpos);
   pa.counters = reinterpret_cast<int32_t*>(ws + L.counters);
+  pa.wl = reinterpret_cast<int4*>(ws + L.wl);
+  pa.wl_cap = wl_cap_of(c, B);
   pa.blobs = blobs;
   pa.blob_cap = blob_cap;
   pa.counts = counts;
@@ -485,6 +495,14 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   cudaError_t e = cudaLaunchCooperativeKernel((void*)k_prune, dim3(c->prune_grid), dim3(256), args, 0, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_prune (cooperative)");
   ++launches;
+  if (getenv("MHFD_PRUNE_TRACE")) {   // debug: decision rounds of this call (synchronises)
+    int32_t r = -1;
+    int64_t tot = -1;
+    cudaMemcpyAsync(&r, pa.counters + 3, sizeof(r), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&tot, pa.img_off + B, sizeof(tot), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "mhfd prune: %lld candidates, %d rounds\n", (long long)tot, r);
+  }
   MARK(4);
   return MHFD_OK;
 }
