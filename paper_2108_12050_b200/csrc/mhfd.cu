@@ -262,22 +262,23 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   cudaError_t e = cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 256 * B, st);
   if (e == cudaSuccess && bpp == 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset hist");
-  int rows_per_cta = std::max(1, (int)((int64_t)H * B / (c->sms * 8)));
+  // ~2 CTAs per SM of rows (fewer, fuller CTAs: each flushes 256 global atomics)
+  int rows_per_cta = std::max(1, (int)(((int64_t)H * B + 2 * c->sms - 1) / (2 * c->sms)));
   rows_per_cta = std::min(rows_per_cta, 64);
   dim3 hg((H + rows_per_cta - 1) / rows_per_cta, B);
   if (bpp == 1) {
     k_hist<1, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
     LAUNCH_CHECK("k_hist");
-    k_select1<1><<<(B + 127) / 128, 128, 0, st>>>(h1, rp, sel, par, B);
+    k_select1<1><<<(B + 3) / 4, 128, 0, st>>>(h1, rp, sel, par, B);
     LAUNCH_CHECK("k_select1");
   } else {
     k_hist<2, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
     LAUNCH_CHECK("k_hist");
-    k_select1<2><<<(B + 127) / 128, 128, 0, st>>>(h1, rp, sel, par, B);
+    k_select1<2><<<(B + 3) / 4, 128, 0, st>>>(h1, rp, sel, par, B);
     LAUNCH_CHECK("k_select1");
     k_hist<2, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
     LAUNCH_CHECK("k_hist2");
-    k_select2<<<(B + 127) / 128, 128, 0, st>>>(h2, sel, par, B);
+    k_select2<<<(B + 3) / 4, 128, 0, st>>>(h2, sel, par, B);
     LAUNCH_CHECK("k_select2");
   }
 
