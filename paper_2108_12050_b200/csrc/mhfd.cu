@@ -100,6 +100,14 @@ int64_t wl_cap_of(const mhfd_ctx* c, int B) {
   return std::min(all, ((int64_t)1 << 20) + all / 64);
 }
 
+// paper-mode two-pass kernels (k_rows_pair / k_cols_pair) fit; MHFD_NO_COLS_PAIR=1 selects
+// k_rows2 / k_cols_all instead
+bool pair_ok(const mhfd_ctx* c) {
+  const LevelTable& T = *c->tab;
+  return c->p.nms == MHFD_NMS_PAPER && c3_smem(T.rmax) <= kSmemLimit &&
+         r3_smem(T.rmax, r3_taps_total(T)) <= kSmemLimit && getenv("MHFD_NO_COLS_PAIR") == nullptr;
+}
+
 Layout layout(const mhfd_ctx* c, int B) {
   Layout L{};
   const int64_t plane = (int64_t)c->p.width * c->p.height;
@@ -372,8 +380,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     float* rx = reinterpret_cast<float*>(ws + L.rx);
     const int64_t plane = (int64_t)W * H;
     const dim3 gr(W / kR2Cols, (H + 31) / 32, B), gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
-    const bool pair = !write_dog && c3_smem(T.rmax) <= kSmemLimit &&
-                      r3_smem(T.rmax, r3_taps_total(T)) <= kSmemLimit && getenv("MHFD_NO_COLS_PAIR") == nullptr;
+    const bool pair = !write_dog && pair_ok(c);
     if (pair) {   // paper mode: all levels' row blur in one launch
       const size_t sm_p = r3_smem(T.rmax, r3_taps_total(T));
       ea = cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
@@ -896,7 +903,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
-  return c->twopass && W % kR2Cols == 0 ? "k_rows2+k_cols_all" : "k_scale_space";
+  if (c->twopass && W % kR2Cols == 0) return pair_ok(c) ? "k_rows_pair+k_cols_pair" : "k_rows2+k_cols_all";
+  return "k_scale_space";
 }
 
 double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {

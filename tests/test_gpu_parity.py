@@ -375,7 +375,7 @@ def test_twopass_matches_fused_generic_bitwise():
             det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, **cfg)
         finally:
             os.environ.pop("MHFD_NO_TWOPASS", None)
-        assert det.schedule("u16") == ("k_rows2+k_cols_all" if flag is None else "k_scale_space")
+        assert det.schedule("u16") == ("k_rows_pair+k_cols_pair" if flag is None else "k_scale_space")
         d = det.debug_dump(img, dog=True, cands=True)
         os.environ["MHFD_NO_COLS_PAIR"] = "1"   # paper mode: k_cols_all, not k_cols_pair
         try:
@@ -403,7 +403,7 @@ def test_cols_pair_matches_cols_all():
     imgs.append(torch.full((1000, 1024), 777, dtype=torch.int32))
     img = torch.from_numpy(np.stack([t.to(torch.int32).cpu().numpy() for t in imgs]).astype(np.uint16))
     det = mhfd.Detector(1024, 1000, min_sigma=1.0, max_sigma=20.0, num_scales=12, threshold=0.1 * 19.0 / 12)
-    assert det.schedule("u16") == "k_rows2+k_cols_all"
+    assert det.schedule("u16") == "k_rows_pair+k_cols_pair"
     res = []
     for flag in (None, "1"):
         if flag:
