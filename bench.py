@@ -278,7 +278,36 @@ def other_configs(dev) -> dict:
             f"u{bits}"), "device_ms": dms, "host_visible_ms": hms, "MPix_per_s_device": size * size / dms / 1e3,
             "score": score}
     out["C3_bands_1gpu"] = band_times(dev)
+    out["downsample_f2"] = downsample_times(dev)
     return out
+
+
+def downsample_times(dev) -> dict:
+    """The bilinear downsampling pre-step (mhfd_downsample) on 16 x
+    4096^2 u8 tiles (268 MB in, larger than L2) at factor 2: device time and achieved HBM
+    bandwidth (bytes read + written) against the measured HBM peak."""
+    import paper_2108_12050_b200 as mhfd
+    B, f = 16, 2
+    g = torch.Generator(device=dev).manual_seed(5)
+    imgs = torch.randint(0, 256, (B, SIZE, SIZE), dtype=torch.uint8, device=dev, generator=g)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        mhfd.downsample(imgs, f)
+    ms = []
+    for _ in range(11):
+        torch.cuda.synchronize()
+        e0.record()
+        mhfd.downsample(imgs, f)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    nbytes = B * SIZE * SIZE * (1 + 1 / (f * f))
+    pk, pk_note = peaks()
+    return {"batch": B, "size": SIZE, "factor": f, "dtype": "u8", "device_ms": t, "GB_per_s": nbytes / t / 1e6,
+            "hbm_peak_GB_per_s": pk.get("hbm_gbs"), "peak_note": pk_note,
+            "hbm_frac": (nbytes / t / 1e6) / pk["hbm_gbs"] if pk.get("hbm_gbs") else None,
+            "kernel": "k_downsample2<uint8_t>"}
 
 
 def band_times(dev) -> dict:

@@ -226,6 +226,25 @@ mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t
                                   size_t workspace_bytes, mhfd_blob* d_blobs, int32_t blob_capacity,
                                   int32_t* d_count, double* d_score, int32_t* d_flags, void* stream);
 
+/* mhfd_downsample: the bilinear downsampling pre-step (PAPER.md:401
+ * "preprocessing by downsampling, by bilinear interpolation, in order to satisfy GPU RAM
+ * constraints"; SPEC.md:48-56 fixes the output shape ceil(W/f) x ceil(H/f) and factor 1 =
+ * identity).  Context-free.  Output pixel (X, Y) samples the input at the pixel-centre
+ * coordinates x = (X + 1/2) f - 1/2, y = (Y + 1/2) f - 1/2 (half-pixel convention), with
+ * bilinear weights and both neighbour indices clamped to the last row/column; for an integer
+ * factor the fractional parts are 0 (odd f: the sample is one pixel) or 1/2 (even f: the
+ * mean of a 2 x 2, 2 x 1 or 1 x 1 block), so the exact value is a multiple of 1/4 and is
+ * rounded half up to the input's integer type (reading R22).
+ *  d_in      : batch images, height x in_pitch bytes each (u8 or u16, row-major)
+ *  d_out     : batch images, ceil(height/f) x out_pitch bytes each, same dtype
+ *  factor    : 1 <= factor <= min(width, height)
+ * Errors: INVALID_ARGUMENT (null pointer, bad dtype, factor, batch < 0); SHAPE (width or
+ * height < 1 or > 65535, a pitch smaller than its row or not a multiple of the pixel
+ * size); CUDA (launch).  Enqueued on
+ * `stream`; nothing is enqueued on a validation error. */
+mhfd_status mhfd_downsample(const void* d_in, int32_t dtype, int32_t width, int32_t height, int64_t in_pitch,
+                            int32_t factor, void* d_out, int64_t out_pitch, int32_t batch, void* stream);
+
 /* Read back the parameters a context was built with (derived fields filled). */
 mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
 

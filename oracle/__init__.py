@@ -76,6 +76,7 @@ def _load():
                                         P, i64, P, P, P, P, P, P]),
                 "oracle_detect_pol": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
                                             P, i64, P, P, P, P, P, P]),
+                "oracle_downsample": (i32, [P, i32, i32, i32, i32, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(lib, name)
@@ -249,3 +250,18 @@ def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, over
         if mode == 0:
             res["v"], res["idx"] = v, idx
     return res
+
+
+def downsample(img: np.ndarray, factor: int) -> np.ndarray:
+    """Bilinear downsampling pre-step (reading R22): textbook
+    bilinear in f64 at half-pixel sample centres, rounded half up; (H, W) u8/u16 ->
+    (ceil(H/f), ceil(W/f)) of the same dtype."""
+    img, bpp = _img(img)
+    H, W = img.shape
+    f = int(factor)
+    if f < 1 or f > min(H, W):
+        raise ValueError("factor must be in [1, min(H, W)]")
+    out = np.empty((-(-H // f), -(-W // f)), img.dtype)
+    if _load().oracle_downsample(_ptr(img), bpp, H, W, f, _ptr(out)) != 0:
+        raise ValueError("oracle_downsample failed")
+    return out

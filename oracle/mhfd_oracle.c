@@ -444,3 +444,45 @@ int64_t oracle_detect(const void* img, int bytes_per_px, int H, int W,
   return oracle_detect_pol(img, bytes_per_px, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high, nms, strict, 0,
                            out, cap, n_cand, D_dump, v_dump, idx_dump, lo_out, hi_out);
 }
+
+/* Bilinear downsampling pre-step.  PAPER.md:401: "preprocessing by
+ * downsampling, by bilinear interpolation"; output ceil(W/f) x ceil(H/f),
+ * factor 1 = identity, values by a scalar bilinear formula at sample centres.  Textbook
+ * bilinear interpolation in f64: output (X, Y) samples the input at x = (X + 1/2) f - 1/2,
+ * y = (Y + 1/2) f - 1/2; x0 = floor(x), fx = x - x0, both neighbours x0, x0 + 1 clamped
+ * to W - 1 (the last of ceil(W/f) samples may lie past the last column; same for y); value = (1-fy)((1-fx) p(y0,x0) + fx p(y0,x1)) + fy((1-fx) p(y1,x0) + fx p(y1,x1)),
+ * rounded half up to the input's integer type (reading R22).  Returns 0, or -1 on bad
+ * arguments. */
+int oracle_downsample(const void* img, int bytes_per_px, int H, int W, int f, void* out) {
+  if (f < 1 || f > H || f > W || (bytes_per_px != 1 && bytes_per_px != 2)) return -1;
+  const int OH = (H + f - 1) / f, OW = (W + f - 1) / f;
+  for (int Y = 0; Y < OH; ++Y) {
+    const double y = (Y + 0.5) * f - 0.5;
+    const int y0f = (int)floor(y);
+    const double fy = y - y0f;
+    const int y0 = y0f < H ? y0f : H - 1;   /* ceil(H/f) rows: the last sample may lie past row H-1 */
+    const int y1 = y0f + 1 < H ? y0f + 1 : H - 1;
+    for (int X = 0; X < OW; ++X) {
+      const double x = (X + 0.5) * f - 0.5;
+      const int x0f = (int)floor(x);
+      const double fx = x - x0f;
+      const int x0 = x0f < W ? x0f : W - 1;
+      const int x1 = x0f + 1 < W ? x0f + 1 : W - 1;
+      double p00, p01, p10, p11;
+      if (bytes_per_px == 1) {
+        const uint8_t* a = (const uint8_t*)img;
+        p00 = a[(int64_t)y0 * W + x0]; p01 = a[(int64_t)y0 * W + x1];
+        p10 = a[(int64_t)y1 * W + x0]; p11 = a[(int64_t)y1 * W + x1];
+      } else {
+        const uint16_t* a = (const uint16_t*)img;
+        p00 = a[(int64_t)y0 * W + x0]; p01 = a[(int64_t)y0 * W + x1];
+        p10 = a[(int64_t)y1 * W + x0]; p11 = a[(int64_t)y1 * W + x1];
+      }
+      const double v = (1.0 - fy) * ((1.0 - fx) * p00 + fx * p01) + fy * ((1.0 - fx) * p10 + fx * p11);
+      const double r = floor(v + 0.5);
+      if (bytes_per_px == 1) ((uint8_t*)out)[(int64_t)Y * OW + X] = (uint8_t)r;
+      else ((uint16_t*)out)[(int64_t)Y * OW + X] = (uint16_t)r;
+    }
+  }
+  return 0;
+}

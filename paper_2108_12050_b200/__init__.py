@@ -16,7 +16,7 @@ import torch
 from . import _abi
 from ._abi import MHFDError, mhfd_blob, mhfd_params  # noqa: F401
 
-__all__ = ["Detector", "MHFDError", "BLOB_FIELDS"]
+__all__ = ["Detector", "MHFDError", "BLOB_FIELDS", "downsample"]
 
 BLOB_FIELDS = ("x", "y", "scale", "response")
 
@@ -259,3 +259,26 @@ def blob_rows(blobs: torch.Tensor, count: int) -> list[tuple[int, int, int, floa
     b = blobs[:count].cpu()
     resp = b[:, 3].view(torch.float32) if b.numel() else torch.empty(0)
     return [(int(x), int(y), int(s), float(r)) for (x, y, s), r in zip(b[:, :3].tolist(), resp.tolist())]
+
+
+def downsample(images: torch.Tensor, factor: int) -> torch.Tensor:
+    """Bilinear downsampling pre-step (mhfd_downsample):
+    (B, H, W) or (H, W) uint8/uint16 CUDA tensor -> (B, ceil(H/f), ceil(W/f)) of the same
+    dtype, half-pixel sample centres, exact value rounded half up (R22)."""
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    if images.dim() != 3 or images.device.type != "cuda":
+        raise ValueError("images must be a (B, H, W) CUDA tensor")
+    codes = {torch.uint8: (_abi.MHFD_U8, 1), torch.uint16: (_abi.MHFD_U16, 2)}
+    if images.dtype not in codes:
+        raise TypeError("images must be torch.uint8 or torch.uint16")
+    dt, bpp = codes[images.dtype]
+    images = images.contiguous()
+    B, H, W = images.shape
+    f = int(factor)
+    out = torch.empty((B, -(-H // f) if f > 0 else 0, -(-W // f) if f > 0 else 0), dtype=images.dtype,
+                      device=images.device)
+    stream = torch.cuda.current_stream(images.device).cuda_stream
+    _abi.check(_abi.load().mhfd_downsample(images.data_ptr(), dt, W, H, W * bpp, f, out.data_ptr(),
+                                           out.shape[2] * bpp, B, stream))
+    return out

@@ -31,6 +31,7 @@
 #include "k_band2.cuh"
 #include "k_tc.cuh"
 #include "k_twopass.cuh"
+#include "k_downsample.cuh"
 
 using namespace mhfd;
 
@@ -980,6 +981,47 @@ mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t
   mhfd_status s = run_prune(c, 1, ws, L, blob_capacity > 0 ? d_blobs : nullptr, blob_capacity, d_count, d_score,
                             d_flags, st, launches, nullptr, ncand > 0 ? d_cands : reinterpret_cast<const mhfd_blob*>(ws + L.cand));
   if (s != MHFD_OK) return s;
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+mhfd_status mhfd_downsample(const void* d_in, int32_t dtype, int32_t width, int32_t height, int64_t in_pitch,
+                            int32_t factor, void* d_out, int64_t out_pitch, int32_t batch, void* stream) {
+  g_launches = 0;
+  if (!d_in || !d_out) return fail(MHFD_ERR_INVALID_ARGUMENT, "downsample: null image pointer");
+  if (dtype != MHFD_U8 && dtype != MHFD_U16) return fail(MHFD_ERR_INVALID_ARGUMENT, "downsample: dtype %d", dtype);
+  if (batch < 0) return fail(MHFD_ERR_INVALID_ARGUMENT, "downsample: batch < 0");
+  if (width < 1 || height < 1 || width > 65535 || height > 65535)
+    return fail(MHFD_ERR_SHAPE, "downsample: %dx%d", width, height);
+  if (factor < 1 || factor > std::min(width, height))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "downsample: factor %d not in [1, min(W, H) = %d]", factor,
+                std::min(width, height));
+  const int bpp = dtype == MHFD_U16 ? 2 : 1;
+  const int OW = (width + factor - 1) / factor, OH = (height + factor - 1) / factor;
+  if (in_pitch < (int64_t)width * bpp || out_pitch < (int64_t)OW * bpp || in_pitch % bpp || out_pitch % bpp)
+    return fail(MHFD_ERR_SHAPE, "downsample: pitch smaller than a row or not a multiple of the pixel size");
+  if (batch == 0) return MHFD_OK;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t work = (int64_t)batch * OH * ((OW + 3) / 4);
+  const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 8);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint8_t* in = static_cast<const uint8_t*>(d_in);
+  uint8_t* out = static_cast<uint8_t*>(d_out);
+  int launches = 0;
+  const bool fast2 = factor == 2 && ((int64_t)width * bpp) % 16 == 0 && in_pitch % 16 == 0 && out_pitch % 8 == 0 &&
+                     reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 8 == 0;
+  if (fast2) {
+    const int64_t work2 = (int64_t)batch * OH * ((int64_t)width * bpp / 16);
+    const int grid2 = (int)std::min<int64_t>((work2 + 255) / 256, (int64_t)sms * 16);
+    if (bpp == 1) k_downsample2<uint8_t><<<grid2, 256, 0, st>>>(in, width, height, in_pitch, out, OH, out_pitch, batch);
+    else k_downsample2<uint16_t><<<grid2, 256, 0, st>>>(in, width, height, in_pitch, out, OH, out_pitch, batch);
+  } else if (bpp == 1) {
+    k_downsample<uint8_t><<<grid, 256, 0, st>>>(in, width, height, in_pitch, factor, out, OW, OH, out_pitch, batch);
+  } else {
+    k_downsample<uint16_t><<<grid, 256, 0, st>>>(in, width, height, in_pitch, factor, out, OW, OH, out_pitch, batch);
+  }
+  LAUNCH_CHECK("k_downsample");
   g_launches = launches;
   return MHFD_OK;
 }

@@ -103,3 +103,25 @@ def test_null_and_destroy_safe():
     n = ctypes.c_size_t()
     assert lib.mhfd_workspace_bytes(None, 1, ctypes.byref(n)) == 1
     assert lib.mhfd_focus_score(None, None, 1, 1, 256, None, 0, None, None, None) == 1
+
+
+@pytest.mark.parametrize("args,status", [
+    # (dtype, W, H, in_pitch, factor, out_pitch, batch) -> status; pointers are dummies:
+    # validation runs before any device work
+    ((1, 16, 16, 16, 0, 16, 1), 1),      # factor 0
+    ((1, 16, 8, 16, 9, 16, 1), 1),       # factor > min(W, H)
+    ((3, 16, 16, 16, 2, 16, 1), 1),      # bad dtype
+    ((1, 16, 16, 16, 2, 16, -1), 1),     # negative batch
+    ((1, 16, 16, 8, 2, 8, 1), 2),        # input pitch < row
+    ((1, 16, 16, 16, 2, 4, 1), 2),       # output pitch < ceil(W/f)
+    ((2, 16, 16, 33, 2, 16, 1), 2),      # u16 pitch not a multiple of 2
+    ((1, 0, 16, 16, 1, 16, 1), 2),       # empty width
+])
+def test_downsample_validates_before_device(args, status):
+    lib = _abi.load()
+    dt, W, H, ip, f, op, B = args
+    dummy = ctypes.c_void_p(0x1000)
+    assert lib.mhfd_downsample(dummy, dt, W, H, ip, f, dummy, op, B, None) == status
+    assert lib.mhfd_downsample(None, 1, 16, 16, 16, 1, dummy, 16, 1, None) == 1
+    # batch 0 is a valid no-op that enqueues nothing
+    assert lib.mhfd_downsample(dummy, 1, 16, 16, 16, 2, dummy, 8, 0, None) == 0

@@ -469,3 +469,35 @@ def test_defocus_sweep_log_linear():
     fit = fit_log_linear(defocus, scores)
     assert fit.r <= -0.95 and fit.slope < 0, fit
     np.testing.assert_allclose(fit.deviation(fit.predict(defocus)), defocus, atol=1e-9)
+
+
+@pytest.mark.parametrize("dtype", [torch.uint8, torch.uint16])
+def test_downsample_bit_exact(dtype):
+    """mhfd_downsample (f4 pre-step) vs the oracle's f64 bilinear: integer outputs,
+    bit-exact, on ragged shapes, factors 1-5 and 8, a batch of 3 (each image vs its own
+    oracle call); then the downsampled tile feeds the detector."""
+    rng = np.random.default_rng(77)
+    hi = 256 if dtype == torch.uint8 else 65536
+    npd = np.uint8 if dtype == torch.uint8 else np.uint16
+    for (H, W) in ((1000, 777), (64, 64), (257, 1031), (255, 128)):   # (64, 64), (255, 128): factor-2 fast path
+        a = rng.integers(0, hi, size=(3, H, W)).astype(npd)
+        t = torch.from_numpy(a.astype(np.int32)).to(torch.int32).cuda().to(dtype) if dtype == torch.uint16 \
+            else torch.from_numpy(a).cuda()
+        for f in (1, 2, 3, 4, 5, 8):
+            out = mhfd.downsample(t, f)
+            torch.cuda.synchronize()
+            assert out.shape == (3, -(-H // f), -(-W // f)) and out.dtype == dtype
+            o = out.cpu()
+            o = o.numpy() if dtype == torch.uint8 else o.to(torch.int32).numpy().astype(np.uint16)
+            for b in range(3):
+                assert np.array_equal(o[b], oracle.downsample(a[b], f)), (H, W, f, b)
+    with pytest.raises(mhfd.MHFDError):
+        mhfd.downsample(torch.zeros((1, 8, 8), dtype=dtype, device="cuda"), 9)
+    # the pre-step in front of the detector: a 2048^2 synthetic tile -> 1024^2
+    img = synth.em_tile(2048, 2048, 1000, defocus=0.0, dose=300.0, device="cuda")
+    if dtype == torch.uint8:
+        small = mhfd.downsample(img, 2)[0]
+        det = mhfd.Detector(1024, 1024, 1.0, 10.0, 10, threshold=0.09, overlap=0.5)
+        s = float(det.focus_score(small)[0])
+        ref = oracle.detect(small.cpu().numpy(), 1.0, 10.0, 10, 0.09, 0.5)["count"]
+        assert abs(s - ref) <= 1e-3 * ref

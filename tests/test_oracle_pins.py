@@ -472,3 +472,61 @@ def test_bright_disk_detected_only_with_bright_polarity(r):
     assert abs(tmin + int(b["scale"]) * dt + dt / 2 - r / math.sqrt(2)) <= 0.61 + 1e-9
     res_dark = oracle.detect(bright, tmin, tmax, n, 0.1 * dt, 0.5, polarity="dark")
     assert (48, 48) not in {(int(q["x"]), int(q["y"])) for q in res_dark["blobs"]}
+
+
+# ---------------------------------------------------------------- downsampling (f4)
+# PAPER.md:401 ("downsampling, by bilinear interpolation"); reading R22.
+
+def test_downsample_identity_and_constant():
+    rng = np.random.default_rng(3)
+    for dt in (np.uint8, np.uint16):
+        a = rng.integers(0, np.iinfo(dt).max + 1, size=(13, 17), dtype=dt)
+        assert np.array_equal(oracle.downsample(a, 1), a)                     # SPEC.md:52 factor 1
+    c = np.full((4, 4), 128, np.uint8)
+    assert np.array_equal(oracle.downsample(c, 2), np.full((2, 2), 128, np.uint8))
+
+
+def test_downsample_ramp_hand_values():
+    # 4x4 ramp, factor 2, evaluated by hand at the sample centres x = 2X + 1/2:
+    # each output is the mean of one 2x2 block, e.g. (0 + 10 + 40 + 50) / 4 = 25
+    a = (np.arange(16).reshape(4, 4) * 10).astype(np.uint8)
+    assert oracle.downsample(a, 2).tolist() == [[25, 45], [105, 125]]
+    # factor 3 on 4x4: ceil -> 2x2; samples at x = 1, 4 -> columns 1, 3 (clamped)
+    assert oracle.downsample(a, 3).tolist() == [[50, 70], [130, 150]]
+    # a half-way value rounds up: (1 + 2 + 1 + 2) / 4 = 1.5 -> 2
+    assert oracle.downsample(np.array([[1, 2], [1, 2]], np.uint8), 2).tolist() == [[2]]
+
+
+@pytest.mark.parametrize("f", [2, 3, 4, 5])
+def test_downsample_matches_torch_bilinear(f):
+    # library routine: torch bilinear, align_corners=False (half-pixel centres, edge clamp)
+    # on divisible shapes, in f64, rounded half up
+    rng = np.random.default_rng(10 + f)
+    a = rng.integers(0, 65536, size=(6 * f, 7 * f), dtype=np.uint16)
+    t = torch.nn.functional.interpolate(torch.from_numpy(a.astype(np.float64))[None, None], scale_factor=1.0 / f,
+                                        mode="bilinear", align_corners=False, recompute_scale_factor=False)
+    ref = np.floor(t[0, 0].numpy() + 0.5).astype(np.uint16)
+    assert np.array_equal(oracle.downsample(a, f), ref)
+
+
+@pytest.mark.parametrize("shape,f", [((13, 17), 2), ((13, 17), 3), ((9, 20), 4), ((31, 29), 5), ((8, 8), 8)])
+def test_downsample_closed_form_integer_factor(shape, f):
+    # for an integer factor the sample x = X f + (f - 1)/2 is a pixel (odd f) or the
+    # midpoint of two (even f): output = that pixel, or the rounded-half-up mean of the
+    # 2 x 2 block, indices clamped to the image (brute force over a ragged shape)
+    rng = np.random.default_rng(sum(shape) + f)
+    a = rng.integers(0, 256, size=shape, dtype=np.uint8)
+    H, W = shape
+    out = oracle.downsample(a, f)
+    assert out.shape == (-(-H // f), -(-W // f))
+    for Y in range(out.shape[0]):
+        for X in range(out.shape[1]):
+            if f % 2:
+                y, x = min(Y * f + (f - 1) // 2, H - 1), min(X * f + (f - 1) // 2, W - 1)
+                want = int(a[y, x])
+            else:
+                y0, x0 = min(Y * f + f // 2 - 1, H - 1), min(X * f + f // 2 - 1, W - 1)
+                y1, x1 = min(y0 + 1, H - 1), min(x0 + 1, W - 1)
+                s = int(a[y0, x0]) + int(a[y0, x1]) + int(a[y1, x0]) + int(a[y1, x1])
+                want = (s + 2) // 4
+            assert int(out[Y, X]) == want, (Y, X)
