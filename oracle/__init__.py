@@ -77,6 +77,10 @@ def _load():
                 "oracle_detect_pol": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
                                             P, i64, P, P, P, P, P, P]),
                 "oracle_downsample": (i32, [P, i32, i32, i32, i32, P]),
+                "oracle_log_taps": (None, [f64, i32, P, P]),
+                "oracle_log_stack_rows": (None, [P, i32, i32, f64, f64, i32, i32, i32, P]),
+                "oracle_detect_resp": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
+                                             i32, P, i64, P, P, P, P, P, P]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(lib, name)
@@ -171,6 +175,28 @@ def dog_stack(f: np.ndarray, min_t: float, max_t: float, n: int,
     return D
 
 
+def log_taps(t: float, R: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """(w, w2): renormalised Gaussian taps and the zero-sum second-derivative taps
+    w2(d) = w(d)(d^2 - m2)/t^4, m2 = sum w d^2 (reading R23)."""
+    R = radius(t) if R is None else int(R)
+    w = np.empty(2 * R + 1, np.float64)
+    w2 = np.empty(2 * R + 1, np.float64)
+    _load().oracle_log_taps(float(t), R, _ptr(w), _ptr(w2))
+    return w, w2
+
+
+def log_stack(f: np.ndarray, min_t: float, max_t: float, n: int,
+              rows: tuple[int, int] | None = None) -> np.ndarray:
+    """Scale-normalised Laplacian planes t_i^2 (d_xx + d_yy) L(., t_i), i = 1..n
+    (Eq. 1; reading R23)."""
+    f = np.ascontiguousarray(f, np.float64)
+    H, W = f.shape
+    y0, y1 = (0, H) if rows is None else rows
+    D = np.empty((n, y1 - y0, W), np.float64)
+    _load().oracle_log_stack_rows(_ptr(f), H, W, min_t, max_t, n, y0, y1, _ptr(D))
+    return D
+
+
 def dog_at(f: np.ndarray, min_t: float, max_t: float, n: int, y: int, x: int) -> np.ndarray:
     """Eq. 2 at one pixel from the 2-D definition (for sampled full-size checks)."""
     f = np.ascontiguousarray(f, np.float64)
@@ -224,9 +250,10 @@ def prune(blobs: np.ndarray, min_t: float, max_t: float, n: int, overlap: float)
 
 def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, overlap: float,
            sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
-           strict: bool = False, dump: bool = False, polarity: str = "dark") -> dict:
+           strict: bool = False, dump: bool = False, polarity: str = "dark", response: str = "dog") -> dict:
     """Algorithm 1 + threshold + pruning; returns blobs, count, candidates.
-    polarity "bright" negates the Eq. 2 response (not in the paper)."""
+    polarity "bright" negates the response (not in the paper); response
+    "log" replaces Eq. 2 by the scale-normalised Laplacian t_i^2 lap L(t_i) (reading R23)."""
     img, bpp = _img(img)
     H, W = img.shape
     mode = {"paper": 0, "26": 1}[str(nms)]
@@ -238,9 +265,10 @@ def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, over
     v = np.empty((H, W), np.float64) if (dump and mode == 0) else None
     idx = np.empty((H, W), np.int32) if (dump and mode == 0) else None
     pol = {"dark": 0, "bright": 1}[str(polarity)]
-    k = _load().oracle_detect_pol(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
-                                  mode, int(strict), pol, _ptr(out), cap, ctypes.byref(ncand),
-                                  _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
+    resp = {"dog": 0, "log": 1}[str(response)]
+    k = _load().oracle_detect_resp(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
+                                   mode, int(strict), pol, resp, _ptr(out), cap, ctypes.byref(ncand),
+                                   _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
     if k < 0:
         raise MemoryError("oracle_detect failed")
     res = {"blobs": out[:k].copy(), "count": int(k), "n_candidates": int(ncand.value),

@@ -204,6 +204,67 @@ void oracle_dog_stack(const double* f, int H, int W, double min_t, double max_t,
   oracle_dog_stack_rows(f, H, W, min_t, max_t, n, 0, H, D);
 }
 
+/* Scale-normalised Laplacian response (SURVEY 8(f) f3 "true sigma^2 lap L"
+ * Eq. 1 and :163 "t^2 lap^2 L"; reading R23): LoG_i = t_i^2 (d_xx + d_yy) L(., t_i) for the
+ * n scales t_1..t_n of Eq. 2's planes.  Discrete second derivative of the sampled,
+ * renormalised Gaussian (taps w, support R): w2(d) = w(d) (d^2 - m2) / t^4 with
+ * m2 = sum_d w(d) d^2, so sum_d w2 = 0 (a constant image responds 0) and
+ * sum_d w2(d) d^2 / 2 = (sum w d^4 - m2^2) / (2 t^4) ~ 1; the 2-D operator is the sum
+ * of the two separable products w2 (x) w + w (x) w2, periodic boundary. */
+void oracle_log_taps(double t, int R, double* w /* 2R+1 */, double* w2 /* 2R+1 */) {
+  oracle_gaussian_taps(t, R, w);
+  double m2 = 0.0;
+  for (int d = -R; d <= R; ++d) m2 += w[d + R] * (double)d * d;
+  const double t4 = t * t * t * t;
+  for (int d = -R; d <= R; ++d) w2[d + R] = w[d + R] * ((double)d * d - m2) / t4;
+}
+
+void oracle_log_stack_rows(const double* f, int H, int W, double min_t, double max_t, int n,
+                           int y0, int y1, double* D) {
+  double* t = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+  oracle_scale_grid(min_t, max_t, n, t);
+  const int64_t plane = (int64_t)(y1 - y0) * W;
+  for (int i = 0; i < n; ++i) {
+    const int R = oracle_radius(t[i]);
+    double* w = (double*)malloc(sizeof(double) * (size_t)(2 * R + 1));
+    double* w2 = (double*)malloc(sizeof(double) * (size_t)(2 * R + 1));
+    oracle_log_taps(t[i], R, w, w2);
+    const int nrow = (y1 - y0) + 2 * R;   /* input rows y0-R .. y1+R-1 */
+    double* A = (double*)malloc(sizeof(double) * (size_t)nrow * (size_t)W);    /* w  along x */
+    double* Bx = (double*)malloc(sizeof(double) * (size_t)nrow * (size_t)W);   /* w2 along x */
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < nrow; ++r) {
+      const double* src = f + wrap((int64_t)(y0 - R + r), H) * W;
+      for (int x = 0; x < W; ++x) {
+        double a = 0.0, bb = 0.0;
+        for (int b = -R; b <= R; ++b) {
+          const double v = src[wrap((int64_t)x + b, W)];
+          a += w[b + R] * v;
+          bb += w2[b + R] * v;
+        }
+        A[(int64_t)r * W + x] = a;
+        Bx[(int64_t)r * W + x] = bb;
+      }
+    }
+    double* Di = D + (int64_t)i * plane;
+    const double t2 = t[i] * t[i];
+#pragma omp parallel for schedule(static)
+    for (int y = y0; y < y1; ++y) {
+      for (int x = 0; x < W; ++x) {
+        double yy = 0.0, xx = 0.0;   /* d_yy L: w2 along y of A;  d_xx L: w along y of Bx */
+        for (int a = -R; a <= R; ++a) {
+          const int64_t r = (int64_t)(y - y0 + R + a) * W + x;
+          yy += w2[a + R] * A[r];
+          xx += w[a + R] * Bx[r];
+        }
+        Di[(int64_t)(y - y0) * W + x] = t2 * (xx + yy);
+      }
+    }
+    free(A); free(Bx); free(w); free(w2);
+  }
+  free(t);
+}
+
 /* DoG at one pixel, evaluated straight from the 2-D definition
  * (sum over the (2R+1)^2 window of G * I', periodic) — used to check
  * sampled outputs of full-size images.  Dvec receives n values.          */
@@ -390,12 +451,12 @@ int64_t oracle_prune(const oracle_blob* c, int64_t nc, double min_t, double max_
  * order; *n_cand receives the candidate count before pruning; D_dump
  * (nullable) receives the n DoG planes; v_dump/idx_dump (nullable) the
  * Eq. 3 inner argmax.  Returns -1 on allocation failure.                 */
-int64_t oracle_detect_pol(const void* img, int bytes_per_px, int H, int W,
-                          double min_t, double max_t, int n, double tau, double overlap,
-                          double sat_low, double sat_high, int nms, int strict, int polarity,
-                          oracle_blob* out, int64_t cap, int64_t* n_cand,
-                          double* D_dump, double* v_dump, int32_t* idx_dump,
-                          int64_t* lo_out, int64_t* hi_out) {
+int64_t oracle_detect_resp(const void* img, int bytes_per_px, int H, int W,
+                           double min_t, double max_t, int n, double tau, double overlap,
+                           double sat_low, double sat_high, int nms, int strict, int polarity, int response,
+                           oracle_blob* out, int64_t cap, int64_t* n_cand,
+                           double* D_dump, double* v_dump, int32_t* idx_dump,
+                           int64_t* lo_out, int64_t* hi_out) {
   int64_t plane = (int64_t)H * W;
   int64_t lo, hi;
   if (oracle_percentiles(img, bytes_per_px, plane, sat_low, sat_high, &lo, &hi) != 0) return -1;
@@ -405,7 +466,8 @@ int64_t oracle_detect_pol(const void* img, int bytes_per_px, int H, int W,
   double* D = D_dump ? D_dump : (double*)malloc(sizeof(double) * (size_t)plane * (size_t)n);
   if (!f || !D) return -1;
   oracle_stretch(img, bytes_per_px, plane, lo, hi, f);
-  oracle_dog_stack(f, H, W, min_t, max_t, n, D);
+  if (response == 1) oracle_log_stack_rows(f, H, W, min_t, max_t, n, 0, H, D);   /* reading R23 */
+  else oracle_dog_stack(f, H, W, min_t, max_t, n, D);
   /* polarity (not in the paper): bright features use the negated
    * Eq. 2 response D_i = -t_i (L_{i+1} - L_i) */
   if (polarity)
@@ -432,6 +494,16 @@ int64_t oracle_detect_pol(const void* img, int bytes_per_px, int H, int W,
   free(keep); free(cand); free(f);
   if (!D_dump) free(D);
   return nk;
+}
+
+int64_t oracle_detect_pol(const void* img, int bytes_per_px, int H, int W,
+                          double min_t, double max_t, int n, double tau, double overlap,
+                          double sat_low, double sat_high, int nms, int strict, int polarity,
+                          oracle_blob* out, int64_t cap, int64_t* n_cand,
+                          double* D_dump, double* v_dump, int32_t* idx_dump,
+                          int64_t* lo_out, int64_t* hi_out) {
+  return oracle_detect_resp(img, bytes_per_px, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high, nms, strict,
+                            polarity, 0, out, cap, n_cand, D_dump, v_dump, idx_dump, lo_out, hi_out);
 }
 
 /* Algorithm 1 as written (dark features, Eq. 2). */

@@ -530,3 +530,80 @@ def test_downsample_closed_form_integer_factor(shape, f):
                 s = int(a[y0, x0]) + int(a[y0, x1]) + int(a[y1, x0]) + int(a[y1, x1])
                 want = (s + 2) // 4
             assert int(out[Y, X]) == want, (Y, X)
+
+
+# ---------------------------------------------------------------- LoG response (f3)
+# PAPER.md:156-163 (Eq. 1, "t^2 lap L"); reading R23.
+
+def test_log_taps_moments():
+    for t in (1.0, 1.9, 4.3, 10.0):
+        w, w2 = oracle.log_taps(t)
+        R = (len(w) - 1) // 2
+        d = np.arange(-R, R + 1, dtype=np.float64)
+        assert abs(w2.sum()) < 1e-15                        # zero sum: constants respond 0
+        assert abs((w2 * d * d).sum() / 2 - 1.0) < 1e-5     # second-moment normalisation
+        assert np.allclose(w2, w2[::-1], atol=0)            # symmetric
+        assert w2[R] < 0 and w2[0] > 0                      # negative centre lobe, positive tails
+
+
+def test_log_constant_image_is_zero():
+    f = np.full((48, 40), 0.37)
+    assert np.abs(oracle.log_stack(f, 1.0, 5.0, 5)).max() < 1e-14
+
+
+@pytest.mark.parametrize("s", [2.0, 3.5, 5.0])
+def test_log_gaussian_blob_closed_form(s):
+    # dark Gaussian blob 1 - A exp(-r^2 / 2 s^2): the blurred image is
+    # 1 - A s^2/(s^2+t^2) exp(-r^2 / 2(s^2+t^2)), so at the centre
+    # t^2 lap L = 2 A t^2 s^2 / (s^2 + t^2)^2 (positive: dark blobs respond positively)
+    A, N = 0.6, 160
+    yy, xx = np.mgrid[0:N, 0:N].astype(np.float64)
+    r2 = (yy - N // 2) ** 2 + (xx - N // 2) ** 2
+    f = 1.0 - A * np.exp(-r2 / (2 * s * s))
+    mn, mx, n = 1.0, 10.0, 10
+    D = oracle.log_stack(f, mn, mx, n, rows=(N // 2, N // 2 + 1))[:, 0, N // 2]
+    t = oracle.scale_grid(mn, mx, n)[:n]
+    want = 2 * A * t ** 2 * s ** 2 / (s * s + t ** 2) ** 2
+    # sampled vs continuous: the discrete sums differ from the integrals by Poisson
+    # aliasing, whose leading term decays like exp(-2 pi^2 t^2 s^2 / (t^2 + s^2)) (the
+    # product of the two sampled Gaussians' spectra); 1e3 covers its polynomial prefactor
+    # (measured 2.2e-5 of the peak at t = 1, s = 2); the support ceil(6t) cuts the
+    # second-derivative taps' tails, t^2 x 2 int_{6t}^inf |g''| ~ 12 e^-18 / sqrt(2 pi)
+    # = 7.4e-8 (measured <= 7.2e-8 of the peak): 2e-7
+    alias = np.exp(-2 * np.pi ** 2 * t ** 2 * s ** 2 / (t ** 2 + s ** 2))
+    assert np.all(np.abs(D - want) <= (2e-7 + 1e3 * alias) * want.max())
+    assert int(np.argmax(D)) == int(np.argmax(want))       # scale selection: t ~ s
+
+
+def test_log_separable_equals_2d_definition():
+    # the 2-D operator sum_{a,b} (w2(a) w(b) + w(a) w2(b)) f(y+a, x+b), periodic,
+    # evaluated directly at a few pixels of a random image
+    rng = np.random.default_rng(8)
+    f = rng.random((22, 26))
+    mn, mx, n = 1.0, 2.0, 2
+    D = oracle.log_stack(f, mn, mx, n)
+    t = oracle.scale_grid(mn, mx, n)
+    for i in range(n):
+        w, w2 = oracle.log_taps(t[i])
+        R = (len(w) - 1) // 2
+        K = np.outer(w2, w) + np.outer(w, w2)      # K[a, b]: a along y, b along x
+        for (y, x) in ((0, 0), (5, 17), (21, 25), (11, 3)):
+            acc = 0.0
+            for a in range(-R, R + 1):
+                for b in range(-R, R + 1):
+                    acc += K[a + R, b + R] * f[(y + a) % 22, (x + b) % 26]
+            assert abs(D[i, y, x] - t[i] ** 2 * acc) < 1e-13
+
+
+def test_log_detect_single_disk():
+    # end to end with response="log": one dark disk -> exactly one blob at its centre,
+    # at the scale where t^2 lap L of the disk peaks (t ~ r / sqrt 2 for a disk)
+    N, r = 128, 8.0
+    yy, xx = np.mgrid[0:N, 0:N].astype(np.float64)
+    f = np.where((yy - 64) ** 2 + (xx - 64) ** 2 <= r * r, 60, 200).astype(np.uint8)
+    res = oracle.detect(f, 1.0, 10.0, 10, 0.05, 0.5, response="log")
+    assert res["count"] == 1
+    b = res["blobs"][0]
+    assert (int(b["x"]), int(b["y"])) == (64, 64)
+    t = oracle.scale_grid(1.0, 10.0, 10)
+    assert abs(t[int(b["scale"])] - r / np.sqrt(2)) <= 0.9 + 1e-9
