@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define MHFD_ABI_VERSION 2
+#define MHFD_ABI_VERSION 3
 
 typedef struct mhfd_ctx mhfd_ctx; /* opaque, immutable after mhfd_create */
 
@@ -76,6 +76,16 @@ typedef enum { MHFD_U8 = 1, MHFD_U16 = 2 } mhfd_dtype;
  * on a dark background; equivalent to MHFD_DARK on the inverted image 255 - I
  * (65535 - I for u16) up to rounding. */
 typedef enum { MHFD_DARK = 0, MHFD_BRIGHT = 1 } mhfd_polarity;
+
+/* Response whose scale argmax / NMS / pruning follow (ABI 3).  MHFD_RESPONSE_DOG: Eq. 2
+ * (PAPER.md:169-173), the paper's detector (default).  MHFD_RESPONSE_LOG: the
+ * scale-normalised Laplacian it approximates, LoG_i = t_i^2 (d_xx + d_yy) L(., t_i) at the
+ * n scales t_1..t_n (Eq. 1; reading R23):
+ * d_xx by zero-sum sampled second-derivative taps w2(d) = w(d)(d^2 - m2)/t^4,
+ * m2 = sum_d w(d) d^2, over the same support ceil(5 t) as the blur; same sign and
+ * polarity conventions as Eq. 2, responses on the LoG scale (about 1/dt times Eq. 2's).
+ * LOG runs the two-pass CUDA-core schedule: width % 256 == 0 and 2n <= 62 required. */
+typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
 
 typedef enum {
   MHFD_NMS_PAPER = 0, /* Eq. 3: global argmax over scale, 3x3 local max in space (default) */
@@ -106,6 +116,8 @@ typedef struct {
                              n*ceil(W/2)*ceil(H/2) (26 mode)                         */
   int32_t polarity;       /* mhfd_polarity (ABI 2; a struct_size without this field
                              reads as MHFD_DARK)                                     */
+  int32_t response;       /* mhfd_response (ABI 3; a struct_size without this field
+                             reads as MHFD_RESPONSE_DOG)                             */
 } mhfd_params;
 
 /* One detected feature (x^_j, y^_j, i^_j) of Eq. 3 and its DoG

@@ -16,6 +16,7 @@ STATUS = {0: "MHFD_OK", 1: "MHFD_ERR_INVALID_ARGUMENT", 2: "MHFD_ERR_SHAPE", 3: 
           4: "MHFD_ERR_WORKSPACE", 5: "MHFD_ERR_CUDA", 6: "MHFD_ERR_DEVICE"}
 MHFD_U8, MHFD_U16 = 1, 2
 MHFD_DARK, MHFD_BRIGHT = 0, 1
+MHFD_RESPONSE_DOG, MHFD_RESPONSE_LOG = 0, 1
 MHFD_NMS_PAPER, MHFD_NMS_26 = 0, 1
 
 # every symbol include/mhfd.h declares (checked by tests/test_abi.py)
@@ -32,7 +33,8 @@ class mhfd_params(ctypes.Structure):
                 ("min_sigma", ctypes.c_float), ("max_sigma", ctypes.c_float), ("num_scales", ctypes.c_int32),
                 ("threshold", ctypes.c_float), ("overlap", ctypes.c_float), ("sat_low", ctypes.c_float),
                 ("sat_high", ctypes.c_float), ("nms", ctypes.c_int32), ("strict", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("max_candidates", ctypes.c_int32), ("polarity", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("max_candidates", ctypes.c_int32), ("polarity", ctypes.c_int32),
+                ("response", ctypes.c_int32)]
 
 
 class mhfd_blob(ctypes.Structure):

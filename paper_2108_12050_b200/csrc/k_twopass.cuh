@@ -193,9 +193,15 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                : "memory");
 }
 
+// LOG (reading R23): tab holds 2n sub-levels, Rx of sub-level 2i = w_i along x and of
+// 2i + 1 = w2_i along x; the column taps of sub-level s are the row taps of s ^ 1, so
+// sub-level 2i gives d_yy L_i and 2i + 1 gives d_xx L_i, and plane i's response is
+// tdog[2i] (= +-t_i^2) x their sum; optional `dog` receives the n planes.
+template <bool LOG>
 __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __restrict__ rx_all, int W, int H, int B,
                                                              const __grid_constant__ LevelTable tab,
                                                              float* __restrict__ v, uint8_t* __restrict__ idx,
+                                                             float* __restrict__ dog,
                                                              const ImgPar* __restrict__ par) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* buf0 = reinterpret_cast<float*>(smem_raw);
@@ -216,18 +222,20 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
       if (y < 0) y += H;
       cp_async16(hb + r * kBandHP + 4 * c, src + (int64_t)y * W + 4 * c);
     }
-    const float* w = tab.w + tab.woff[lev] + tab.pre[lev];
+    const int cl = LOG ? (lev ^ 1) : lev;   // the level whose taps run along y
+    const float* w = tab.w + tab.woff[cl] + tab.pre[cl];
     for (int i = tid; i < c3_taps(R); i += kC3Threads) wc[i] = i < 2 * R + 1 ? w[i] : 0.f;
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const int cp = lane & 15;
   const int rg = 2 * warp + (lane >> 4);
-  float lprev[16], vbest[16];
+  float lprev[16], vbest[16], part[16];
   uint32_t ibest[4];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) { lprev[k] = 0.f; vbest[k] = -INFINITY; }
+  for (int k = 0; k < 16; ++k) { lprev[k] = 0.f; vbest[k] = -INFINITY; part[k] = 0.f; }
 #pragma unroll
   for (int k = 0; k < 4; ++k) ibest[k] = 0u;
+  const bool degen = par[b].degen != 0;
   stage(0, 0);
   for (int lev = 0; lev < tab.nlev; ++lev) {
     if (lev + 1 < tab.nlev) {
@@ -239,11 +247,42 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
     __syncthreads();   // level lev's window and taps are in
     const float* hb = buf0 + (lev & 1) * bufsz;
     const float* wc = hb + c3_rows(tab.rmax) * kBandHP;
-    col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, lev,
-                      lev > 0 ? tab.tdog[lev - 1] : 0.f, lprev, vbest, ibest);
+    if (!LOG) {
+      col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, lev,
+                        lev > 0 ? tab.tdog[lev - 1] : 0.f, lprev, vbest, ibest);
+    } else {
+      // lev = 0: col_pass only returns the 16 column sums in lprev
+      col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, 0, 0.f, lprev, vbest, ibest);
+      if ((lev & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) part[k] = lprev[k];
+      } else {
+        const int i = lev >> 1;
+        const float tf = tab.tdog[lev];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float D = degen ? 0.f : tf * (part[k] + lprev[k]);
+          if (D > vbest[k]) {
+            vbest[k] = D;
+            const int sh = (k & 3) * 8;
+            ibest[k >> 2] = (ibest[k >> 2] & ~(0xffu << sh)) | ((uint32_t)i << sh);
+          }
+          part[k] = D;
+        }
+        if (dog) {
+#pragma unroll
+          for (int o = 0; o < 8; ++o) {
+            const int y = Y0 + 8 * rg + o;
+            if (y < H)
+              *reinterpret_cast<float2*>(dog + ((int64_t)b * (tab.nlev / 2) + i) * plane + (int64_t)y * W + x0 +
+                                         2 * cp) = make_float2(part[2 * o], part[2 * o + 1]);
+          }
+        }
+      }
+    }
     __syncthreads();   // buffer lev & 1 is free for level lev + 2
   }
-  const bool degen = par[b].degen != 0;
+  if (!v) return;
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
     const int y = Y0 + 8 * rg + o;

@@ -38,6 +38,7 @@ using namespace mhfd;
 struct mhfd_ctx {
   mhfd_params p;
   LevelTable* tab;   // host copy, passed by value to k_scale_space
+  LevelTable* ltab;  // LoG response (reading R23): 2n sub-levels {w_i, w2_i} (k_rows_pair / k_cols_pair<true>)
   int n;             // DoG planes
   double dt;
   double t[kMaxLevels];
@@ -139,7 +140,9 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.counters = take(sizeof(int32_t) * 8);
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
-  L.rx = take(c->twopass ? sizeof(float) * plane * B * (c->n + 1) : 0);   // two-pass: Rx of every level
+  // two-pass: Rx of every level (LoG: of every one of the 2n sub-levels)
+  L.rx = take(c->ltab ? sizeof(float) * plane * B * (2 * c->n)
+                      : (c->twopass ? sizeof(float) * plane * B * (c->n + 1) : 0));
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
   L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
@@ -299,7 +302,8 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   const bool band = band_lo < band_hi;
   // k_tc also writes the DoG planes: for the 26-neighbour NMS and for debug dumps
   float* tc_dog = dog_dump ? dog_dump : (paper ? nullptr : reinterpret_cast<float*>(ws + L.dog));
-  if (bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
+  const bool dogr = c->p.response == MHFD_RESPONSE_DOG;
+  if (dogr && bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
       (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
@@ -325,7 +329,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   }
   if (band) return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
   // ---- a2-a6 on u8 images, two-CTA band schedule
-  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
+  if (dogr && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
       band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
     const size_t smem = band2_smem(c->tab->rmax, c->tab->ntaps_total);
     cudaError_t ea = cudaFuncSetAttribute(k_band2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -337,7 +341,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
   }
   // ---- a2-a6 on u8 images: band schedule (raw band staged once per CTA, no f32 prepass)
-  if (bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
+  if (dogr && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
       band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
     const size_t smem = band_smem(c->tab->rmax, c->tab->ntaps_total);
     cudaError_t ea = cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -373,6 +377,23 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // ---- a3-a6: fused blur + DoG + argmax
   float* dog = dog_dump ? dog_dump : reinterpret_cast<float*>(ws + L.dog);
   const bool write_dog = dog_dump != nullptr || !paper;
+  if (!dogr) {   // LoG response (reading R23): two passes over 2n sub-levels
+    const LevelTable& T = *c->ltab;
+    float* rx = reinterpret_cast<float*>(ws + L.rx);
+    const size_t sm_p = r3_smem(T.rmax, r3_taps_total(T)), sm_3 = c3_smem(T.rmax);
+    cudaError_t ea = cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
+    if (ea == cudaSuccess)
+      ea = cudaFuncSetAttribute(k_cols_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
+    if (ea != cudaSuccess) return cuda_fail(ea, "LoG two-pass attributes");
+    k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, B), kC3Threads, sm_p, st>>>(fimg, W, H, T, rx, B);
+    LAUNCH_CHECK("k_rows_pair");
+    const dim3 gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
+    k_cols_pair<true><<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
+                                                     write_dog ? dog : nullptr, par);
+    LAUNCH_CHECK("k_cols_pair");
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
+  }
   if (c->twopass && W % kR2Cols == 0) {   // large radii: two passes per level through HBM
     const LevelTable& T = *c->tab;
     const size_t sm_r = rows2_smem(T.rmax), sm_c = cols2_smem(T.rmax);
@@ -396,9 +417,9 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     }
     if (pair) {
       const size_t sm_3 = c3_smem(T.rmax);
-      ea = cudaFuncSetAttribute(k_cols_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
+      ea = cudaFuncSetAttribute(k_cols_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
       if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_pair attribute");
-      k_cols_pair<<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, v, idx, par);
+      k_cols_pair<false><<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, v, idx, nullptr, par);
       LAUNCH_CHECK("k_cols_pair");
     } else {
       ea = cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
@@ -583,6 +604,12 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   p = &pp;
   if (p->polarity != MHFD_DARK && p->polarity != MHFD_BRIGHT)
     return fail(MHFD_ERR_INVALID_ARGUMENT, "polarity %d", p->polarity);
+  if (p->response != MHFD_RESPONSE_DOG && p->response != MHFD_RESPONSE_LOG)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "response %d", p->response);
+  if (p->response == MHFD_RESPONSE_LOG && 2 * p->num_scales > kMaxLevels - 2)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "LoG response: 2 num_scales = %d > %d", 2 * p->num_scales, kMaxLevels - 2);
+  if (p->response == MHFD_RESPONSE_LOG && p->width % kR3Cols != 0)
+    return fail(MHFD_ERR_SHAPE, "LoG response: width %d is not a multiple of %d", p->width, kR3Cols);
   if (!(std::isfinite(p->min_sigma) && p->min_sigma > 0.f))
     return fail(MHFD_ERR_INVALID_ARGUMENT, "min_sigma must be > 0 (NonPositiveScale)");
   if (!(std::isfinite(p->max_sigma) && p->max_sigma > p->min_sigma))
@@ -670,6 +697,52 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     c->t[i] = t[i];
   }
   T.ntaps_total = off;
+  if (p->response == MHFD_RESPONSE_LOG) {   // reading R23: sub-levels 2i = w_i, 2i+1 = w2_i (row taps)
+    c->ltab = new (std::nothrow) LevelTable;
+    if (!c->ltab) {
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_INVALID_ARGUMENT, "out of host memory");
+    }
+    LevelTable& LT = *c->ltab;
+    memset(&LT, 0, sizeof(LT));
+    LT.nlev = 2 * n;
+    LT.rmax = 0;
+    int lo = 0;
+    for (int i = 0; i < n; ++i) {
+      const int Ri = R[i];
+      const int pre = (4 - Ri % 4) % 4;
+      const int ntap = ((pre + 2 * Ri + 1) + kTapUnroll - 1) / kTapUnroll * kTapUnroll;
+      std::vector<double> w(2 * Ri + 1), w2(2 * Ri + 1);
+      double sum = 0.0, m2 = 0.0;
+      for (int d = -Ri; d <= Ri; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
+      for (int d = -Ri; d <= Ri; ++d) {
+        w[d + Ri] = std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum;
+        m2 += w[d + Ri] * (double)d * d;
+      }
+      const double t4 = t[i] * t[i] * t[i] * t[i];
+      for (int d = -Ri; d <= Ri; ++d) w2[d + Ri] = w[d + Ri] * ((double)d * d - m2) / t4;
+      for (int k = 0; k < 2; ++k) {
+        const int sl = 2 * i + k;
+        if (lo + ntap + 8 > kMaxTaps) {
+          mhfd_destroy(c);
+          return fail(MHFD_ERR_INVALID_ARGUMENT, "LoG tap table exceeds %d floats", kMaxTaps);
+        }
+        for (int d = -Ri; d <= Ri; ++d) LT.w[lo + pre + d + Ri] = (float)(k ? w2[d + Ri] : w[d + Ri]);
+        LT.R[sl] = Ri;
+        LT.pre[sl] = pre;
+        LT.ntap[sl] = ntap;
+        LT.woff[sl] = lo;
+        LT.tdog[sl] = (float)((p->polarity == MHFD_BRIGHT ? -1.0 : 1.0) * t[i] * t[i]);   // t_i^2, signed
+        lo += ntap + 8;
+      }
+      LT.rmax = std::max(LT.rmax, Ri);
+    }
+    LT.ntaps_total = lo;
+    if (c3_smem(LT.rmax) > kSmemLimit || r3_smem(LT.rmax, r3_taps_total(LT)) > kSmemLimit) {
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_INVALID_ARGUMENT, "LoG response: radius %d too large for the two-pass kernels", LT.rmax);
+    }
+  }
   // tensor-core plan and its Toeplitz tables (device copy owned by the context)
   c->tc = new (std::nothrow) TcPlan;
   if (c->tc && tc_plan_build(*c->tc, n + 1, R, t)) {
@@ -829,6 +902,7 @@ void mhfd_destroy(mhfd_ctx* c) {
   if (c->d_thr) cudaFree(c->d_thr);
   delete c->tc;
   delete c->tab;
+  delete c->ltab;
   delete c;
 }
 
@@ -899,6 +973,7 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (!c) return "none";
   const int W = c->p.width, H = c->p.height;
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
+  if (c->p.response == MHFD_RESPONSE_LOG) return "k_rows_pair+k_cols_pair<log>";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
   if (dtype == MHFD_U8 && paper && c->band_enabled) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
@@ -921,6 +996,10 @@ double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {
     return 2.0 * macs / ((double)kTcTile * kTcTile);
   }
   double f = 0.0;   // direct separable blur at R_i: 2 passes x (2R_i+1) FMA per level, + DoG/max
+  if (c->ltab) {    // LoG: per plane 2 row convs (w, w2) + 2 column convs, + sum/scale/max
+    for (int i = 0; i < c->n; ++i) f += 2.0 * 4.0 * (2.0 * c->tab->R[i] + 1.0);
+    return f + 4.0 * c->n;
+  }
   for (int i = 0; i <= c->n; ++i) f += 2.0 * 2.0 * (2.0 * c->tab->R[i] + 1.0);
   return f + 3.0 * c->n;
 }

@@ -29,7 +29,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert not missing, missing
     for s in declared:
         assert hasattr(lib, s)
-    assert lib.mhfd_abi_version() == 2
+    assert lib.mhfd_abi_version() == 3
 
 
 def test_library_is_sm100a_only():
@@ -70,7 +70,7 @@ def test_abi1_struct_size_reads_polarity_as_dark():
     ("min_sigma", 0.0, 1), ("max_sigma", 0.5, 1), ("num_scales", 0, 1), ("num_scales", 63, 1),
     ("threshold", -1.0, 1), ("threshold", float("nan"), 1), ("overlap", 1.5, 1), ("sat_low", 0.6, 1),
     ("nms", 7, 1), ("strict", 2, 1), ("max_sigma", 40.0, 1), ("width", 50, 2), ("height", 70000, 2),
-    ("polarity", 2, 1), ("struct_size", 8, 1),
+    ("polarity", 2, 1), ("struct_size", 8, 1), ("response", 2, 1),
 ])
 def test_create_validates_before_device(field, value, status):
     lib = _abi.load()
@@ -125,3 +125,32 @@ def test_downsample_validates_before_device(args, status):
     assert lib.mhfd_downsample(None, 1, 16, 16, 16, 1, dummy, 16, 1, None) == 1
     # batch 0 is a valid no-op that enqueues nothing
     assert lib.mhfd_downsample(dummy, 1, 16, 16, 16, 2, dummy, 8, 0, None) == 0
+
+
+@pytest.mark.parametrize("W,n,status", [(300, 10, 2), (256, 32, 1)])
+def test_log_response_validates_before_device(W, n, status):
+    # the LoG response (reading R23) runs the two-pass kernels: width % 256 == 0 and
+    # 2n sub-levels within the level table
+    lib = _abi.load()
+    p = _abi.mhfd_params()
+    lib.mhfd_params_default(ctypes.byref(p))
+    p.width, p.height, p.max_sigma, p.num_scales = W, 256, 5.0, n
+    p.response = _abi.MHFD_RESPONSE_LOG
+    h = ctypes.c_void_p()
+    assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == status
+    assert "LoG" in lib.mhfd_last_error().decode()
+
+
+def test_abi2_struct_size_reads_response_as_dog():
+    # an ABI-2 caller's struct ends before `response`: the field beyond struct_size is not
+    # read (a garbage value there must not be validated)
+    lib = _abi.load()
+    p = _abi.mhfd_params()
+    lib.mhfd_params_default(ctypes.byref(p))
+    p.width, p.height, p.max_sigma = 256, 256, 5.0
+    p.struct_size = _abi.mhfd_params.response.offset
+    p.response = 9
+    p.min_sigma = 0.0
+    h = ctypes.c_void_p()
+    assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == 1
+    assert "min_sigma" in lib.mhfd_last_error().decode()

@@ -35,17 +35,18 @@ def _to_t(img):
     return t
 
 
-def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None, polarity="dark"):
+def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None, polarity="dark",
+                 response="dog"):
     """Full comparison on one image: percentiles, DoG stack, v/argmax, candidates,
     pruned blobs, counts and score."""
     H, W = img.shape
     tau = _tau(cfg) if tau is None else tau
     n = cfg["num_scales"]
     det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, schedule=schedule,
-                        polarity=polarity, **cfg)
+                        polarity=polarity, response=response, **cfg)
     dump = det.debug_dump(_to_t(img))
     ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True,
-                        polarity=polarity)
+                        polarity=polarity, response=response)
     # a1: percentiles, exact integers
     lo, hi = dump["lohi"][0].tolist()
     assert (lo, hi) == (ref["lo"], ref["hi"])
@@ -501,3 +502,39 @@ def test_downsample_bit_exact(dtype):
         s = float(det.focus_score(small)[0])
         ref = oracle.detect(small.cpu().numpy(), 1.0, 10.0, 10, 0.09, 0.5)["count"]
         assert abs(s - ref) <= 1e-3 * ref
+
+
+# ---------------------------------------------------------------- LoG response (f3)
+@pytest.mark.parametrize("nms", ["paper", "26"])
+def test_log_response_full_parity(c1_img, nms):
+    """response="log" (reading R23): t_i^2 lap L(t_i) through k_rows_pair / k_cols_pair<log>
+    against the oracle's LoG stack: responses within 1e-4 of the peak, argmax, candidates,
+    pruned blobs, counts and score under the same parity rules as Eq. 2."""
+    tau = 0.1   # C1's tau / dt: LoG responses are ~1/dt times Eq. 2's
+    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response="log")
+    assert s["n_oracle"] > 100
+    det = mhfd.Detector(256, 256, threshold=tau, response="log", **C1)
+    assert det.schedule("u8") == "k_rows_pair+k_cols_pair<log>"
+
+
+def test_log_response_u16_ragged_and_degenerate():
+    """LoG on u16, a ragged last row band (H = 200 with 256-row column tiles), a batch of
+    two with a constant (degenerate) image: parity of v / argmax with the oracle for the
+    real image, zeros and no blobs for the constant one."""
+    cfg = dict(min_sigma=1.0, max_sigma=6.0, num_scales=5)
+    a = synth.em_tile_np(200, 512, 1300, dose=300.0, bits=16)
+    imgs = np.stack([a, np.full_like(a, 4321)])
+    det = mhfd.Detector(512, 200, threshold=0.1, response="log", **cfg)
+    t = torch.from_numpy(imgs.astype(np.int32)).to(torch.int32).cuda().to(torch.uint16)
+    d = det.debug_dump(t, dog=True, cands=False)
+    blobs, cnt, _ = det.detect(t)
+    torch.cuda.synchronize()
+    ref = oracle.detect(a, 1.0, 6.0, 5, 0.1, 0.5, dump=True, response="log")
+    Pk = float(ref["D"].max())
+    eps = P.REL_EPS * Pk
+    assert float(np.abs(d["dog"][0].cpu().numpy() - ref["D"]).max()) <= eps
+    assert float(np.abs(d["v"][0].cpu().numpy() - ref["v"]).max()) <= eps
+    tie = P.scale_tie(ref["D"], eps)
+    assert np.array_equal(d["idx"][0].cpu().numpy()[~tie], ref["idx"][~tie])
+    assert float(d["dog"][1].abs().max()) == 0.0 and float(d["v"][1].abs().max()) == 0.0 and int(cnt[1]) == 0
+    P.assert_score(int(cnt[0]), ref["count"])
