@@ -279,6 +279,16 @@ def other_configs(dev) -> dict:
             "score": score}
     out["C3_bands_1gpu"] = band_times(dev)
     out["downsample_f2"] = downsample_times(dev)
+    # C3 with the LoG response (reading R23): 4 FP32 convolutions per plane
+    img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
+    det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=0.1, overlap=OVERLAP,
+                        device=dev.index, response="log")
+    dms, hms, score = timed(det, img.unsqueeze(0), img.unsqueeze(0).cpu().pin_memory())
+    fpp = det.schedule_flops_per_pixel("u8")
+    out["C3_log"] = {"size": SIZE, "dtype": "u8", "sigma": list(SIGMA), "scales": NSCALES, "response": "log",
+                     "schedule": det.schedule("u8"), "device_ms": dms, "host_visible_ms": hms,
+                     "MPix_per_s_device": SIZE * SIZE / dms / 1e3, "score": score,
+                     "fp32_tflops_direct": fpp * SIZE * SIZE / (dms * 1e-3) / 1e12}
     return out
 
 
