@@ -832,7 +832,9 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   {   // large radii: the two-pass generic schedule (no halo recompute) when the fused
       // band kernel would recompute more than ~1.5x of its row pass
     const char* nt = getenv("MHFD_NO_TWOPASS");
-    c->twopass = (rmax >= 96 && p->width % kR2Cols == 0 && !(nt && nt[0] == '1') &&
+    const char* mr = getenv("MHFD_TWOPASS_MIN_R");   // tuning knob: smallest R_max for the two-pass path
+    const int min_r = mr ? atoi(mr) : 96;
+    c->twopass = (rmax >= min_r && p->width % kR2Cols == 0 && !(nt && nt[0] == '1') &&
                   rows2_smem(rmax) <= kSmemLimit && cols2_smem(rmax) <= kSmemLimit) ? 1 : 0;
   }
   {
