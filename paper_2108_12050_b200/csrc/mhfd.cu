@@ -65,6 +65,7 @@ struct mhfd_ctx {
 namespace {
 
 constexpr size_t kSmemLimit = 227 * 1024;   // opt-in dynamic shared memory per CTA on sm_100
+constexpr int kRxBatch = 8;                   // images per two-pass chunk (Rx workspace)
 
 thread_local std::string g_err;
 thread_local int32_t g_launches = 0;
@@ -106,7 +107,7 @@ int64_t wl_cap_of(const mhfd_ctx* c, int B) {
 // k_rows2 / k_cols_all instead
 bool pair_ok(const mhfd_ctx* c) {
   const LevelTable& T = *c->tab;
-  return c->p.nms == MHFD_NMS_PAPER && c3_smem(T.rmax) <= kSmemLimit &&
+  return c->p.nms == MHFD_NMS_PAPER && c->band_enabled && c->p.width % kR3Cols == 0 && c3_smem(T.rmax) <= kSmemLimit &&
          r3_smem(T.rmax, r3_taps_total(T)) <= kSmemLimit && getenv("MHFD_NO_COLS_PAIR") == nullptr;
 }
 
@@ -140,9 +141,11 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.counters = take(sizeof(int32_t) * 8);
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
-  // two-pass: Rx of every level (LoG: of every one of the 2n sub-levels)
-  L.rx = take(c->ltab ? sizeof(float) * plane * B * (2 * c->n)
-                      : (c->twopass ? sizeof(float) * plane * B * (c->n + 1) : 0));
+  // two-pass schedules: Rx of every level (LoG: of each of the 2n sub-levels) for up to
+  // kRxBatch images (run_front chunks larger batches)
+  const int64_t rxb = std::min(B, kRxBatch);
+  const bool any2 = c->ltab || c->twopass || pair_ok(c);
+  L.rx = take(any2 ? sizeof(float) * plane * rxb * (c->ltab ? 2 * c->n : c->n + 1) : 0);
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
   L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
@@ -377,56 +380,53 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // ---- a3-a6: fused blur + DoG + argmax
   float* dog = dog_dump ? dog_dump : reinterpret_cast<float*>(ws + L.dog);
   const bool write_dog = dog_dump != nullptr || !paper;
-  if (!dogr) {   // LoG response (reading R23): two passes over 2n sub-levels
-    const LevelTable& T = *c->ltab;
-    float* rx = reinterpret_cast<float*>(ws + L.rx);
-    const size_t sm_p = r3_smem(T.rmax, r3_taps_total(T)), sm_3 = c3_smem(T.rmax);
-    cudaError_t ea = cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
-    if (ea == cudaSuccess)
-      ea = cudaFuncSetAttribute(k_cols_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
-    if (ea != cudaSuccess) return cuda_fail(ea, "LoG two-pass attributes");
-    k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, B), kC3Threads, sm_p, st>>>(fimg, W, H, T, rx, B);
-    LAUNCH_CHECK("k_rows_pair");
-    const dim3 gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
-    k_cols_pair<true><<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
-                                                     write_dog ? dog : nullptr, par);
-    LAUNCH_CHECK("k_cols_pair");
-    MARK(2);
-    return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
-  }
-  if (c->twopass && W % kR2Cols == 0) {   // large radii: two passes per level through HBM
-    const LevelTable& T = *c->tab;
-    const size_t sm_r = rows2_smem(T.rmax), sm_c = cols2_smem(T.rmax);
-    cudaError_t ea = cudaFuncSetAttribute(k_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_r);
-    if (ea != cudaSuccess) return cuda_fail(ea, "two-pass attributes");
+  // ---- two passes through an HBM row-blur intermediate (k_twopass.cuh): the LoG response
+  // (always), the paper-mode DoG pair kernels (any radius: 1.5x the fused generic kernel
+  // on u16 at sigma 1-10), and large radii with DoG planes
+  // (k_rows2 / k_cols_all).  Rx holds at most kRxBatch images: larger batches run in chunks.
+  const bool pair = dogr && paper && !write_dog && pair_ok(c);
+  const bool big = dogr && !pair && c->twopass && W % kR2Cols == 0;
+  if (!dogr || pair || big) {
+    const LevelTable& T = dogr ? *c->tab : *c->ltab;
     float* rx = reinterpret_cast<float*>(ws + L.rx);
     const int64_t plane = (int64_t)W * H;
-    const dim3 gr(W / kR2Cols, (H + 31) / 32, B), gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, B);
-    const bool pair = !write_dog && pair_ok(c);
-    if (pair) {   // paper mode: all levels' row blur in one launch
-      const size_t sm_p = r3_smem(T.rmax, r3_taps_total(T));
-      ea = cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
-      if (ea != cudaSuccess) return cuda_fail(ea, "k_rows_pair attribute");
-      k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, B), kC3Threads, sm_p, st>>>(fimg, W, H, T, rx, B);
-      LAUNCH_CHECK("k_rows_pair");
-    } else {
-      for (int lev = 0; lev < T.nlev; ++lev) {
-        k_rows2<<<gr, 256, sm_r, st>>>(fimg, W, H, T, lev, rx + (int64_t)lev * B * plane);
-        LAUNCH_CHECK("k_rows2");
+    const bool rows_pair = !big;
+    const size_t sm_p = rows_pair ? r3_smem(T.rmax, r3_taps_total(T)) : rows2_smem(T.rmax);
+    const size_t sm_c = rows_pair ? c3_smem(T.rmax) : cols2_smem(T.rmax);
+    cudaError_t ea = rows_pair ? cudaFuncSetAttribute(k_rows_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p)
+                               : cudaFuncSetAttribute(k_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_p);
+    if (ea == cudaSuccess)
+      ea = !dogr ? cudaFuncSetAttribute(k_cols_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c)
+           : pair ? cudaFuncSetAttribute(k_cols_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c)
+                  : cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
+    if (ea != cudaSuccess) return cuda_fail(ea, "two-pass attributes");
+    const int nplanes = c->n;   // DoG / LoG planes written for the 26 mode and dumps
+    for (int b0 = 0; b0 < B; b0 += kRxBatch) {
+      const int Bc = std::min(kRxBatch, B - b0);
+      const float* fi = fimg + (int64_t)b0 * plane;
+      const ImgPar* pc = par + b0;
+      float* vc = paper ? v + (int64_t)b0 * plane : nullptr;
+      uint8_t* ic = paper ? idx + (int64_t)b0 * plane : nullptr;
+      float* dc = write_dog ? dog + (int64_t)b0 * nplanes * plane : nullptr;
+      const dim3 gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, Bc);
+      if (rows_pair) {   // every level's row blur in one launch
+        k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, Bc), kC3Threads, sm_p, st>>>(fi, W, H, T, rx, Bc);
+        LAUNCH_CHECK("k_rows_pair");
+      } else {
+        for (int lev = 0; lev < T.nlev; ++lev) {
+          k_rows2<<<dim3(W / kR2Cols, (H + 31) / 32, Bc), 256, sm_p, st>>>(fi, W, H, T, lev,
+                                                                           rx + (int64_t)lev * Bc * plane);
+          LAUNCH_CHECK("k_rows2");
+        }
       }
-    }
-    if (pair) {
-      const size_t sm_3 = c3_smem(T.rmax);
-      ea = cudaFuncSetAttribute(k_cols_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_3);
-      if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_pair attribute");
-      k_cols_pair<false><<<gc, kC3Threads, sm_3, st>>>(rx, W, H, B, T, v, idx, nullptr, par);
-      LAUNCH_CHECK("k_cols_pair");
-    } else {
-      ea = cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
-      if (ea != cudaSuccess) return cuda_fail(ea, "k_cols_all attribute");
-      k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, B, T, paper ? v : nullptr, paper ? idx : nullptr,
-                                        write_dog ? dog : nullptr, par);
-      LAUNCH_CHECK("k_cols_all");
+      if (!dogr) {
+        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
+      } else if (pair) {
+        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, nullptr, pc);
+      } else {
+        k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
+      }
+      LAUNCH_CHECK("k_cols");
     }
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
@@ -832,9 +832,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   {   // large radii: the two-pass generic schedule (no halo recompute) when the fused
       // band kernel would recompute more than ~1.5x of its row pass
     const char* nt = getenv("MHFD_NO_TWOPASS");
-    const char* mr = getenv("MHFD_TWOPASS_MIN_R");   // tuning knob: smallest R_max for the two-pass path
-    const int min_r = mr ? atoi(mr) : 96;
-    c->twopass = (rmax >= min_r && p->width % kR2Cols == 0 && !(nt && nt[0] == '1') &&
+    c->twopass = (rmax >= 96 && p->width % kR2Cols == 0 && !(nt && nt[0] == '1') &&
                   rows2_smem(rmax) <= kSmemLimit && cols2_smem(rmax) <= kSmemLimit) ? 1 : 0;
   }
   {
@@ -981,7 +979,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
     if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
   }
-  if (c->twopass && W % kR2Cols == 0) return pair_ok(c) ? "k_rows_pair+k_cols_pair" : "k_rows2+k_cols_all";
+  if (pair_ok(c)) return "k_rows_pair+k_cols_pair";
+  if (c->twopass && W % kR2Cols == 0) return "k_rows2+k_cols_all";
   return "k_scale_space";
 }
 

@@ -155,7 +155,17 @@ def test_u8_schedule_is_tensor_core():
     assert mhfd.Detector(4096, 4096, threshold=0.09, **C3).schedule("u8") == "k_tc"
     assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u8") == "k_tc"
     assert mhfd.Detector(256, 256, threshold=0.08, **C1).schedule("u8") == "k_tc"
-    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u16") == "k_scale_space"
+    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u16") == "k_rows_pair+k_cols_pair"
+    assert mhfd.Detector(1000, 1000, threshold=0.09, **C3).schedule("u16") == "k_scale_space"   # W % 256 != 0
+
+
+def test_u16_generic_schedule_parity():
+    """The fused generic kernel (k_scale_space: u16 with MHFD_SCHEDULE=generic, widths that
+    are not multiples of 256, DoG dumps below R_max 96) against the oracle."""
+    img = synth.em_tile_np(1024, 1024, 1004, defocus=1.0, dose=300.0, bits=16)
+    det = mhfd.Detector(1024, 1024, threshold=0.09, schedule="generic", **C3)
+    assert det.schedule("u16") == "k_scale_space"
+    _full_parity(img, C3, schedule="generic")
 
 
 def test_c2_sharp_beats_defocused():
@@ -369,22 +379,22 @@ def test_twopass_matches_fused_generic_bitwise():
     img = torch.from_numpy(img.to(torch.int32).cpu().numpy().astype(np.uint16))
     cfg = dict(min_sigma=1.0, max_sigma=20.0, num_scales=12)
     outs = []
-    for flag in (None, "1"):
-        if flag:
-            os.environ["MHFD_NO_TWOPASS"] = flag
-        try:
-            det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, **cfg)
-        finally:
-            os.environ.pop("MHFD_NO_TWOPASS", None)
-        assert det.schedule("u16") == ("k_rows_pair+k_cols_pair" if flag is None else "k_scale_space")
-        d = det.debug_dump(img, dog=True, cands=True)
-        os.environ["MHFD_NO_COLS_PAIR"] = "1"   # paper mode: k_cols_all, not k_cols_pair
-        try:
+    os.environ["MHFD_NO_COLS_PAIR"] = "1"   # paper mode on k_rows2 / k_cols_all, not the pair kernels
+    try:
+        for flag in (None, "1"):
+            if flag:
+                os.environ["MHFD_NO_TWOPASS"] = flag
+            try:
+                det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, **cfg)
+            finally:
+                os.environ.pop("MHFD_NO_TWOPASS", None)
+            assert det.schedule("u16") == ("k_rows2+k_cols_all" if flag is None else "k_scale_space")
+            d = det.debug_dump(img, dog=True, cands=True)
             blobs, cnt, _ = det.detect(img)
             torch.cuda.synchronize()
-        finally:
-            os.environ.pop("MHFD_NO_COLS_PAIR", None)
-        outs.append((d, blobs, int(cnt[0])))
+            outs.append((d, blobs, int(cnt[0])))
+    finally:
+        os.environ.pop("MHFD_NO_COLS_PAIR", None)
     (a, ba, ka), (b, bb, kb) = outs
     for key in ("lohi", "dog", "v", "idx", "ncand"):
         assert torch.equal(a[key], b[key]), key
@@ -538,3 +548,24 @@ def test_log_response_u16_ragged_and_degenerate():
     assert np.array_equal(d["idx"][0].cpu().numpy()[~tie], ref["idx"][~tie])
     assert float(d["dog"][1].abs().max()) == 0.0 and float(d["v"][1].abs().max()) == 0.0 and int(cnt[1]) == 0
     P.assert_score(int(cnt[0]), ref["count"])
+
+
+@pytest.mark.parametrize("response", ["dog", "log"])
+def test_two_pass_batch_chunks(response):
+    """The two-pass schedules hold Rx for at most 8 images and run larger batches in
+    chunks: a batch of 11 u16 tiles (different content, one constant) gives, image by
+    image, the same kept blobs as 11 single-image calls."""
+    imgs = [synth.em_tile_np(256, 512, 1400 + k, defocus=0.4 * (k % 5), dose=300.0, bits=16) for k in range(10)]
+    imgs.append(np.full((256, 512), 900, np.uint16))
+    batch = torch.from_numpy(np.stack(imgs).astype(np.int32)).cuda().to(torch.uint16)
+    det = mhfd.Detector(512, 256, 1.0, 6.0, 5, threshold=0.1 if response == "log" else 0.1,
+                        response=response)
+    assert det.schedule("u16").startswith("k_rows_pair+k_cols_pair")
+    blobs, cnt, _ = det.detect(batch)
+    torch.cuda.synchronize()
+    assert int(cnt[10]) == 0
+    for k in range(11):
+        b1, c1, _ = det.detect(batch[k:k + 1])
+        torch.cuda.synchronize()
+        n = int(c1[0])
+        assert n == int(cnt[k]) and torch.equal(b1[0, :n], blobs[k, :n]), k

@@ -1,5 +1,6 @@
 """Device time of one focus_score call on u16 tiles (C2/C3 sizes, sigma 1-10, 10 scales)
-for the fused generic schedule vs the two-pass pair schedule (MHFD_TWOPASS_MIN_R=0)."""
+for the fused generic schedule (MHFD_SCHEDULE=generic) vs the default two-pass pair schedule.
+Measured (B200): 1024^2 0.381 vs 0.222 ms; 4096^2 2.31 vs 1.51 ms; 8 x 4096^2 15.3 vs 10.8 ms."""
 import os
 import statistics
 import sys
@@ -15,11 +16,8 @@ for n, B in ((1024, 1), (4096, 1), (4096, 8)):
     img = synth.em_tile(n, n, 1000, defocus=0.0, dose=300.0, bits=16, device="cuda")
     img = torch.from_numpy(img.to(torch.int32).cpu().numpy().astype(np.uint16)).cuda()
     imgs = img.unsqueeze(0).repeat(B, 1, 1).contiguous()
-    for knob in (None, "0"):
-        if knob is not None:
-            os.environ["MHFD_TWOPASS_MIN_R"] = knob
-        det = mhfd.Detector(n, n, 1.0, 10.0, 10, threshold=0.09, overlap=0.5)
-        os.environ.pop("MHFD_TWOPASS_MIN_R", None)
+    for sched in ("generic", None):
+        det = mhfd.Detector(n, n, 1.0, 10.0, 10, threshold=0.09, overlap=0.5, schedule=sched)
         for _ in range(3):
             det.focus_score(imgs)
         torch.cuda.synchronize()
