@@ -264,10 +264,11 @@ mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
  * for images of `dtype` in mhfd_detect_batch / mhfd_focus_score on this context:
  * "k_tc" (u8, Eq. 3 NMS, tensor-core banded blur; default when the staged tile
  * fits), "k_band" / "k_band2" (u8, CUDA-core band schedules), "k_scale_space"
- * (generic), or for large radii (ceil(5 max_sigma) >= 96, width % 256 == 0) the
- * two-pass schedule through an HBM row-blur intermediate: "k_rows_pair+k_cols_pair"
- * (Eq. 3 NMS; calls that dump DoG planes run "k_rows2+k_cols_all", which is also the
- * 3x3x3 mode's and MHFD_NO_COLS_PAIR=1's).  The environment variable
+ * (generic: widths that are not multiples of 256, MHFD_SCHEDULE=generic, and DoG-plane
+ * calls below R_max 96), or the two-pass schedule through an HBM row-blur intermediate:
+ * "k_rows_pair+k_cols_pair" (Eq. 3 NMS, width % 256 == 0, any radius; also every
+ * MHFD_RESPONSE_LOG context, named "k_rows_pair+k_cols_pair<log>"), "k_rows2+k_cols_all"
+ * (DoG planes at R_max >= 96: 3x3x3 mode, dumps, MHFD_NO_COLS_PAIR=1).  The environment variable
  * MHFD_SCHEDULE=tc|band|band2|generic, read at mhfd_create, selects among the
  * applicable ones.  Static string; "none" for a NULL context. */
 const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype);
