@@ -77,6 +77,8 @@ def _load():
                 "oracle_detect_pol": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
                                             P, i64, P, P, P, P, P, P]),
                 "oracle_downsample": (i32, [P, i32, i32, i32, i32, P]),
+                "oracle_percentiles_f32": (i32, [P, i64, f64, f64, P, P]),
+                "oracle_stretch_f32": (None, [P, i64, f64, f64, P]),
                 "oracle_log_taps": (None, [f64, i32, P, P]),
                 "oracle_log_stack_rows": (None, [P, i32, i32, f64, f64, i32, i32, i32, P]),
                 "oracle_detect_resp": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
@@ -100,7 +102,9 @@ def _img(img: np.ndarray):
         return img, 1
     if img.dtype == np.uint16:
         return img, 2
-    raise TypeError("oracle images are uint8 or uint16")
+    if img.dtype == np.float32:
+        return img, 4
+    raise TypeError("oracle images are uint8, uint16 or float32")
 
 
 def set_threads(n: int) -> None:
@@ -111,9 +115,16 @@ def get_threads() -> int:
     return int(_load().oracle_get_threads())
 
 
-def percentiles(img: np.ndarray, sat_low: float = 0.00175, sat_high: float = 0.00175) -> tuple[int, int]:
-    """Nearest-rank lo/hi of the histogram stretch."""
+def percentiles(img: np.ndarray, sat_low: float = 0.00175, sat_high: float = 0.00175):
+    """Nearest-rank lo/hi of the histogram stretch: ints for
+    u8/u16 images, floats for float32 images (reading R24)."""
     img, bpp = _img(img)
+    if bpp == 4:
+        flo, fhi = ctypes.c_double(), ctypes.c_double()
+        if _load().oracle_percentiles_f32(_ptr(img), img.size, sat_low, sat_high, ctypes.byref(flo),
+                                          ctypes.byref(fhi)) != 0:
+            raise ValueError("oracle_percentiles_f32 failed")
+        return float(flo.value), float(fhi.value)
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
     rc = _load().oracle_percentiles(_ptr(img), bpp, img.size, sat_low, sat_high,
                                     ctypes.byref(lo), ctypes.byref(hi))
@@ -126,7 +137,10 @@ def stretch(img: np.ndarray, lo: int, hi: int) -> np.ndarray:
     """I' = clamp((I - lo)/(hi - lo), 0, 1) in f64 (PAPER.md:257)."""
     img, bpp = _img(img)
     out = np.empty(img.shape, np.float64)
-    _load().oracle_stretch(_ptr(img), bpp, img.size, int(lo), int(hi), _ptr(out))
+    if bpp == 4:
+        _load().oracle_stretch_f32(_ptr(img), img.size, float(lo), float(hi), _ptr(out))
+    else:
+        _load().oracle_stretch(_ptr(img), bpp, img.size, int(lo), int(hi), _ptr(out))
     return out
 
 

@@ -112,6 +112,38 @@ void oracle_stretch(const void* img, int bytes_per_px, int64_t npx,
   }
 }
 
+/* f32 input (SURVEY 8(f) f3 "f32 input dtype with a float-quantile select"; reading R24):
+ * the same nearest-rank percentiles on the real values (finite inputs; -0.0 and +0.0
+ * are equal values) and the same stretch, in f64.  lo/hi are returned as doubles. */
+static int cmp_f64(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+int oracle_percentiles_f32(const float* img, int64_t npx, double sat_low, double sat_high, double* lo, double* hi) {
+  if (npx <= 0) return -1;
+  double* s = (double*)malloc(sizeof(double) * (size_t)npx);
+  if (!s) return -2;
+  for (int64_t i = 0; i < npx; ++i) s[i] = (double)img[i];
+  qsort(s, (size_t)npx, sizeof(double), cmp_f64);
+  int64_t klo = (int64_t)floor(sat_low * (double)npx);
+  int64_t khi = (int64_t)floor(sat_high * (double)npx);
+  if (klo > npx - 1) klo = npx - 1;
+  if (khi > npx - 1) khi = npx - 1;
+  *lo = s[klo];
+  *hi = s[npx - 1 - khi];
+  free(s);
+  return 0;
+}
+
+void oracle_stretch_f32(const float* img, int64_t npx, double lo, double hi, double* out) {
+  for (int64_t i = 0; i < npx; ++i) {
+    if (hi == lo) { out[i] = 0.0; continue; }
+    double v = ((double)img[i] - lo) / (hi - lo);
+    out[i] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }
+}
+
 /* 3. Scale grid — PAPER.md:167: dt = (max_t - min_t)/n,
  * t_i = min_t + (i-1) dt, i = 1..n+1 (n+1 levels, reading R2).          */
 void oracle_scale_grid(double min_t, double max_t, int n, double* t) {
@@ -458,14 +490,27 @@ int64_t oracle_detect_resp(const void* img, int bytes_per_px, int H, int W,
                            double* D_dump, double* v_dump, int32_t* idx_dump,
                            int64_t* lo_out, int64_t* hi_out) {
   int64_t plane = (int64_t)H * W;
-  int64_t lo, hi;
-  if (oracle_percentiles(img, bytes_per_px, plane, sat_low, sat_high, &lo, &hi) != 0) return -1;
-  if (lo_out) *lo_out = lo;
-  if (hi_out) *hi_out = hi;
   double* f = (double*)malloc(sizeof(double) * (size_t)plane);
+  if (!f) return -1;
+  if (bytes_per_px == 4) {   /* f32 input (reading R24); lo/hi reported as their float32 bit patterns */
+    double flo, fhi;
+    if (oracle_percentiles_f32((const float*)img, plane, sat_low, sat_high, &flo, &fhi) != 0) { free(f); return -1; }
+    float l32 = (float)flo, h32 = (float)fhi;
+    uint32_t lb, hb;
+    memcpy(&lb, &l32, 4);
+    memcpy(&hb, &h32, 4);
+    if (lo_out) *lo_out = (int64_t)lb;
+    if (hi_out) *hi_out = (int64_t)hb;
+    oracle_stretch_f32((const float*)img, plane, flo, fhi, f);
+  } else {
+    int64_t lo, hi;
+    if (oracle_percentiles(img, bytes_per_px, plane, sat_low, sat_high, &lo, &hi) != 0) { free(f); return -1; }
+    if (lo_out) *lo_out = lo;
+    if (hi_out) *hi_out = hi;
+    oracle_stretch(img, bytes_per_px, plane, lo, hi, f);
+  }
   double* D = D_dump ? D_dump : (double*)malloc(sizeof(double) * (size_t)plane * (size_t)n);
-  if (!f || !D) return -1;
-  oracle_stretch(img, bytes_per_px, plane, lo, hi, f);
+  if (!D) { free(f); return -1; }
   if (response == 1) oracle_log_stack_rows(f, H, W, min_t, max_t, n, 0, H, D);   /* reading R23 */
   else oracle_dog_stack(f, H, W, min_t, max_t, n, D);
   /* polarity (not in the paper): bright features use the negated

@@ -607,3 +607,34 @@ def test_log_detect_single_disk():
     assert (int(b["x"]), int(b["y"])) == (64, 64)
     t = oracle.scale_grid(1.0, 10.0, 10)
     assert abs(t[int(b["scale"])] - r / np.sqrt(2)) <= 0.9 + 1e-9
+
+
+# ---------------------------------------------------------------- f32 input (f3)
+# SURVEY §8(f) f3 "f32 input dtype with a float-quantile select"; reading R24.
+
+def test_f32_percentiles_nearest_rank_and_integer_agreement():
+    rng = np.random.default_rng(21)
+    a = rng.integers(0, 256, size=(40, 37), dtype=np.uint8)
+    # integer-valued floats: the same ranks and the same stretch as the u8 image
+    lo_i, hi_i = oracle.percentiles(a, 0.05, 0.05)
+    lo_f, hi_f = oracle.percentiles(a.astype(np.float32), 0.05, 0.05)
+    assert (lo_f, hi_f) == (float(lo_i), float(hi_i))
+    assert np.array_equal(oracle.stretch(a.astype(np.float32), lo_f, hi_f), oracle.stretch(a, lo_i, hi_i))
+    # real values: sort-based nearest rank written out, negatives included
+    x = rng.normal(0.0, 3.0, size=(33, 29)).astype(np.float32)
+    s = np.sort(x.ravel().astype(np.float64))
+    k = int(np.floor(0.00175 * x.size))
+    assert oracle.percentiles(x) == (s[k], s[x.size - 1 - k])
+    # affine invariance of the stretch on real values: a*x + b, a > 0
+    y = (2.0 * x.astype(np.float64) + 5.0).astype(np.float32)
+    ly, hy = oracle.percentiles(y)
+    lx, hx = oracle.percentiles(x)
+    assert np.allclose(oracle.stretch(y, ly, hy), oracle.stretch(x, lx, hx), atol=1e-6)
+
+
+def test_f32_detect_equals_u8_on_integer_floats():
+    img = synth.em_tile_np(96, 96, 1000, dose=300.0, bits=8)
+    a = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.5)
+    b = oracle.detect(img.astype(np.float32), 1.0, 5.0, 5, 0.08, 0.5)
+    assert a["count"] == b["count"] and np.array_equal(a["blobs"], b["blobs"])
+    assert np.frombuffer(np.uint32(b["lo"]).tobytes(), np.float32)[0] == float(a["lo"])
