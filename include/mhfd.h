@@ -68,7 +68,10 @@ typedef enum {
   MHFD_ERR_DEVICE = 6            /* no CUDA device, or device is not sm_100 (B200) */
 } mhfd_status;
 
-typedef enum { MHFD_U8 = 1, MHFD_U16 = 2 } mhfd_dtype;
+/* Pixel types.  MHFD_F32 (ABI 3): float32 images with the same nearest-rank percentiles
+ * on real values (radix select over order-preserving keys; finite values required,
+ * reading R24); they run the CUDA-core schedules (k_tc is u8 only). */
+typedef enum { MHFD_U8 = 1, MHFD_U16 = 2, MHFD_F32 = 3 } mhfd_dtype;
 
 /* Feature polarity (reading R5).  MHFD_DARK: Eq. 2 as written,
  * DoG_i = t_i (L_{i+1} - L_i), dark blobs on a bright background respond positively

@@ -108,7 +108,7 @@ class Detector:
         return (p + 255) & ~255
 
     def prepare(self, images: torch.Tensor) -> tuple[torch.Tensor, int, int, int]:
-        """(B,H,W) or (H,W) uint8/uint16 tensor -> device tensor with a 16-byte-multiple pitch."""
+        """(B,H,W) or (H,W) uint8/uint16/float32 tensor -> device tensor with a 16-byte-multiple pitch."""
         if images.dim() == 2:
             images = images.unsqueeze(0)
         if images.dim() != 3 or images.shape[1] != self.height or images.shape[2] != self.width:
@@ -117,8 +117,10 @@ class Detector:
             dt, bpp = _abi.MHFD_U8, 1
         elif images.dtype == torch.uint16:
             dt, bpp = _abi.MHFD_U16, 2
+        elif images.dtype == torch.float32:
+            dt, bpp = _abi.MHFD_F32, 4
         else:
-            raise TypeError("images must be torch.uint8 or torch.uint16")
+            raise TypeError("images must be torch.uint8, torch.uint16 or torch.float32")
         images = images.to(self.device, non_blocking=True)
         B = images.shape[0]
         wp = (self.width * bpp + 15) // 16 * 16 // bpp
@@ -180,7 +182,8 @@ class Detector:
             host_images = host_images.unsqueeze(0)
         if host_images.device.type != "cpu":
             raise ValueError("focus_score_host takes host tensors")
-        dt, bpp = ((_abi.MHFD_U8, 1) if host_images.dtype == torch.uint8 else (_abi.MHFD_U16, 2))
+        dt, bpp = {torch.uint8: (_abi.MHFD_U8, 1), torch.uint16: (_abi.MHFD_U16, 2),
+                   torch.float32: (_abi.MHFD_F32, 4)}[host_images.dtype]
         B, H, W = host_images.shape
         if (H, W) != (self.height, self.width) or (W * bpp) % 16 or not host_images.is_contiguous():
             raise ValueError("host images must be contiguous (B, H, W) with W*bytes % 16 == 0")
@@ -244,12 +247,12 @@ class Detector:
 
     def schedule(self, dtype: str = "u8") -> str:
         """Kernel that computes rows a2-a6 for `dtype` images (mhfd_schedule_name)."""
-        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16}[dtype]
+        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16, "f32": _abi.MHFD_F32}[dtype]
         return self._lib.mhfd_schedule_name(self._h, code).decode()
 
     def schedule_flops_per_pixel(self, dtype: str = "u8") -> float:
         """Flops per pixel the schedule's a2-a6 kernel executes (bench roofline)."""
-        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16}[dtype]
+        code = {"u8": _abi.MHFD_U8, "u16": _abi.MHFD_U16, "f32": _abi.MHFD_F32}[dtype]
         return float(self._lib.mhfd_schedule_flops_per_pixel(self._h, code))
 
     @staticmethod

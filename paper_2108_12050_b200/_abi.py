@@ -14,7 +14,7 @@ from . import _build
 MHFD_OK = 0
 STATUS = {0: "MHFD_OK", 1: "MHFD_ERR_INVALID_ARGUMENT", 2: "MHFD_ERR_SHAPE", 3: "MHFD_ERR_CAPACITY",
           4: "MHFD_ERR_WORKSPACE", 5: "MHFD_ERR_CUDA", 6: "MHFD_ERR_DEVICE"}
-MHFD_U8, MHFD_U16 = 1, 2
+MHFD_U8, MHFD_U16, MHFD_F32 = 1, 2, 3
 MHFD_DARK, MHFD_BRIGHT = 0, 1
 MHFD_RESPONSE_DOG, MHFD_RESPONSE_LOG = 0, 1
 MHFD_NMS_PAPER, MHFD_NMS_26 = 0, 1

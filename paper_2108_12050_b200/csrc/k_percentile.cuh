@@ -151,4 +151,96 @@ __global__ void k_select2(const uint32_t* __restrict__ hist2, const SelState* __
   if ((threadIdx.x & 31) == 0) finish(&par[b], lo, hi);
 }
 
+// ---------------------------------------------------------------------------------
+// f32 input (reading R24): the same nearest ranks on real values by a
+// radix select over order-preserving 32-bit keys (sign flipped for positives, all bits
+// inverted for negatives), 8 bits per pass, 4 passes.  Pass 0 histograms the top byte
+// of every key (one histogram serves both ranks); pass p >= 1 histograms byte 3 - p of
+// the keys whose higher bytes equal the prefix selected so far for lo (bins 0..255) and
+// for hi (256..511).  The select kernel zeroes the histogram it consumed for the next
+// pass.  HBM-bound: 4 B/px read per pass.
+__device__ __forceinline__ uint32_t f32_key(uint32_t u) { return (u & 0x80000000u) ? ~u : (u | 0x80000000u); }
+__device__ __forceinline__ uint32_t f32_unkey(uint32_t k) { return (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k; }
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_hist_f32(const uint8_t* __restrict__ images, Shape s, int rows_per_cta,
+                                                  uint32_t* __restrict__ hist, const SelState* __restrict__ sel) {
+  constexpr int NH = PASS == 0 ? 1 : 2;
+  constexpr int SH = 24 - 8 * PASS;
+  __shared__ uint32_t sh[8][NH * 256];
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 8 * NH * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  uint32_t pl = 0, ph = 0;
+  if (PASS > 0) { pl = (uint32_t)sel[b].bin_lo; ph = (uint32_t)sel[b].bin_hi; }
+  __syncthreads();
+  const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
+  const int y0 = blockIdx.x * rows_per_cta;
+  const int y1 = min(s.H, y0 + rows_per_cta);
+  const int nvec = (s.W + 3) >> 2;
+  for (int y = y0; y < y1; ++y) {
+    const uint4* row = reinterpret_cast<const uint4*>(img + (int64_t)y * s.pitch);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      const uint4 q = __ldg(row + v);
+      const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (4 * v + k < s.W) {
+          const uint32_t key = f32_key(wds[k]);
+          const uint32_t bin = (key >> SH) & 255u;
+          if (PASS == 0) {
+            atomicAdd(&sh[warp][bin], 1u);
+          } else {
+            const uint32_t pre = key >> ((SH + 8) & 31);   // PASS >= 1: SH + 8 <= 24
+            if (pre == pl) atomicAdd(&sh[warp][bin], 1u);
+            if (pre == ph) atomicAdd(&sh[warp][256 + bin], 1u);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NH * 256; i += blockDim.x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += sh[w][i];
+    if (c) atomicAdd(&hist[(int64_t)b * 512 + i], c);
+  }
+}
+
+// one warp per image: extend the lo / hi prefixes by one byte; the last pass writes ImgPar
+// (lo/hi as float32 bit patterns, inv = 1/(hi - lo) in f32)
+template <int PASS>
+__global__ void k_select_f32(uint32_t* __restrict__ hist, RankPar r, SelState* __restrict__ sel,
+                             ImgPar* __restrict__ par, int batch) {
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (b >= batch) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t* h = hist + (int64_t)b * 512;
+  int64_t rl, rh;
+  int bl, bh;
+  if (PASS == 0) {
+    bl = select_bin_warp(h, r.rank_lo, &rl);
+    bh = select_bin_warp(h, r.rank_hi, &rh);
+  } else {
+    bl = select_bin_warp(h, sel[b].rem_lo, &rl);
+    bh = select_bin_warp(h + 256, sel[b].rem_hi, &rh);
+  }
+  __syncwarp();
+  for (int i = lane; i < 512; i += 32) h[i] = 0u;   // clean for the next pass / call
+  if (lane != 0) return;
+  const uint32_t pl = PASS == 0 ? (uint32_t)bl : (((uint32_t)sel[b].bin_lo << 8) | (uint32_t)bl);
+  const uint32_t ph = PASS == 0 ? (uint32_t)bh : (((uint32_t)sel[b].bin_hi << 8) | (uint32_t)bh);
+  if (PASS < 3) {
+    sel[b].bin_lo = (int32_t)pl; sel[b].bin_hi = (int32_t)ph; sel[b].rem_lo = rl; sel[b].rem_hi = rh;
+  } else {
+    const uint32_t ulo = f32_unkey(pl), uhi = f32_unkey(ph);
+    const float lo = __uint_as_float(ulo), hi = __uint_as_float(uhi);
+    par[b].lo = (int32_t)ulo;
+    par[b].hi = (int32_t)uhi;
+    par[b].degen = (hi == lo) ? 1 : 0;
+    par[b].inv = (hi == lo) ? 0.0f : 1.0f / (hi - lo);
+  }
+}
+
 }  // namespace mhfd

@@ -116,6 +116,38 @@ __global__ void __launch_bounds__(256) k_normalize(const uint8_t* __restrict__ i
   }
 }
 
+// f32 input (reading R24): lo/hi are float32 bit patterns in ImgPar; 4 pixels per
+// 16-byte load when W % 4 == 0
+__global__ void __launch_bounds__(256) k_normalize_f32(const uint8_t* __restrict__ images, Shape s,
+                                                       const ImgPar* __restrict__ par, float* __restrict__ out) {
+  const int b = blockIdx.y;
+  const ImgPar ip = par[b];
+  const float lo = __int_as_float(ip.lo), inv = ip.inv;
+  const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
+  float* o = out + (int64_t)b * s.H * s.W;
+  if (s.W % 4 == 0) {
+    const int vpr = s.W / 4;
+    const int64_t total = (int64_t)s.H * vpr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int y = (int)(i / vpr), v = (int)(i - (int64_t)y * vpr);
+      const float4 q = __ldg(reinterpret_cast<const float4*>(img + (int64_t)y * s.pitch) + v);
+      float4 r;
+      r.x = fminf(fmaxf((q.x - lo) * inv, 0.f), 1.f) - 0.5f;
+      r.y = fminf(fmaxf((q.y - lo) * inv, 0.f), 1.f) - 0.5f;
+      r.z = fminf(fmaxf((q.z - lo) * inv, 0.f), 1.f) - 0.5f;
+      r.w = fminf(fmaxf((q.w - lo) * inv, 0.f), 1.f) - 0.5f;
+      reinterpret_cast<float4*>(o)[i] = r;
+    }
+  } else {
+    const int64_t total = (int64_t)s.H * s.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int y = (int)(i / s.W), x = (int)(i - (int64_t)y * s.W);
+      const float p = reinterpret_cast<const float*>(img + (int64_t)y * s.pitch)[x];
+      o[i] = fminf(fmaxf((p - lo) * inv, 0.f), 1.f) - 0.5f;
+    }
+  }
+}
+
 // vectorised variant: 16 input bytes per thread-iteration; needs W % 16 == 0 (u8) or
 // W % 8 == 0 (u16)
 template <int BPP>

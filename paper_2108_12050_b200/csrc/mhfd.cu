@@ -157,9 +157,10 @@ mhfd_status check_call(const mhfd_ctx* c, const void* d_images, int32_t dtype, i
                        const void* ws, size_t ws_bytes) {
   if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (!d_images) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_images is NULL");
-  if (dtype != MHFD_U8 && dtype != MHFD_U16) return fail(MHFD_ERR_INVALID_ARGUMENT, "dtype %d", dtype);
+  if (dtype != MHFD_U8 && dtype != MHFD_U16 && dtype != MHFD_F32)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "dtype %d", dtype);
   if (batch < 1) return fail(MHFD_ERR_SHAPE, "batch %d < 1", batch);
-  const int bpp = dtype == MHFD_U8 ? 1 : 2;
+  const int bpp = dtype == MHFD_U8 ? 1 : dtype == MHFD_U16 ? 2 : 4;
   if (pitch < (int64_t)c->p.width * bpp || pitch % 16 != 0)
     return fail(MHFD_ERR_SHAPE, "pitch_bytes %lld: need >= width*bpp and a multiple of 16", (long long)pitch);
   if (((uintptr_t)d_images) % 16 != 0) return fail(MHFD_ERR_SHAPE, "d_images not 16-byte aligned");
@@ -260,7 +261,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
                       int band_lo = 0, int band_hi = 0) {
   MARK(0);
   const int W = c->p.width, H = c->p.height;
-  const int bpp = dtype == MHFD_U8 ? 1 : 2;
+  const int bpp = dtype == MHFD_U8 ? 1 : dtype == MHFD_U16 ? 2 : 4;
   const Shape s{W, H, pitch, bpp};
   const uint8_t* img = static_cast<const uint8_t*>(d_images);
   ImgPar* par = reinterpret_cast<ImgPar*>(ws + L.par);
@@ -274,14 +275,25 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   rp.npx = N;
   rp.rank_lo = std::min<int64_t>((int64_t)std::floor((double)c->p.sat_low * (double)N), N - 1);
   rp.rank_hi = N - 1 - std::min<int64_t>((int64_t)std::floor((double)c->p.sat_high * (double)N), N - 1);
-  cudaError_t e = cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 256 * B, st);
-  if (e == cudaSuccess && bpp == 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
+  cudaError_t e = bpp == 4 ? cudaSuccess : cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 256 * B, st);
+  if (e == cudaSuccess && bpp >= 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset hist");
   // ~2 CTAs per SM of rows (fewer, fuller CTAs: each flushes 256 global atomics)
   int rows_per_cta = std::max(1, (int)(((int64_t)H * B + 2 * c->sms - 1) / (2 * c->sms)));
   rows_per_cta = std::min(rows_per_cta, 64);
   dim3 hg((H + rows_per_cta - 1) / rows_per_cta, B);
-  if (bpp == 1) {
+  if (bpp == 4) {   // f32 (reading R24): 4 radix-select passes of 8 key bits
+    k_hist_f32<0><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    k_select_f32<0><<<(B + 3) / 4, 128, 0, st>>>(h2, rp, sel, par, B);
+    k_hist_f32<1><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    k_select_f32<1><<<(B + 3) / 4, 128, 0, st>>>(h2, rp, sel, par, B);
+    k_hist_f32<2><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    k_select_f32<2><<<(B + 3) / 4, 128, 0, st>>>(h2, rp, sel, par, B);
+    k_hist_f32<3><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    k_select_f32<3><<<(B + 3) / 4, 128, 0, st>>>(h2, rp, sel, par, B);
+    LAUNCH_CHECK("k_hist_f32 / k_select_f32");
+    launches += 7;
+  } else if (bpp == 1) {
     k_hist<1, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
     LAUNCH_CHECK("k_hist");
     k_select1<1><<<(B + 3) / 4, 128, 0, st>>>(h1, rp, sel, par, B);
@@ -365,10 +377,12 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   float* fimg = reinterpret_cast<float*>(ws + L.fimg);
   {
     const int64_t plane = (int64_t)W * H;
-    const bool vec = (bpp == 1) ? (W % 16 == 0) : (W % 8 == 0);
+    const bool vec = (bpp == 1) ? (W % 16 == 0) : (bpp == 2) ? (W % 8 == 0) : (W % 4 == 0);
     const int64_t work = vec ? plane / (16 / bpp) : plane;
     dim3 gn((unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)c->sms * 8), B);
-    if (vec) {
+    if (bpp == 4) {
+      k_normalize_f32<<<gn, 256, 0, st>>>(img, s, par, fimg);
+    } else if (vec) {
       if (bpp == 1) k_normalize_vec<1><<<gn, 256, 0, st>>>(img, s, par, fimg);
       else k_normalize_vec<2><<<gn, 256, 0, st>>>(img, s, par, fimg);
     } else {

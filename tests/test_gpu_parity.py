@@ -49,6 +49,8 @@ def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, sch
                         polarity=polarity, response=response)
     # a1: percentiles, exact integers
     lo, hi = dump["lohi"][0].tolist()
+    if img.dtype == np.float32:   # float32 bit patterns (reading R24)
+        lo, hi = lo & 0xFFFFFFFF, hi & 0xFFFFFFFF
     assert (lo, hi) == (ref["lo"], ref["hi"])
     # a2-a5: responses within 1e-4 of the peak
     D = ref["D"]
@@ -569,3 +571,33 @@ def test_two_pass_batch_chunks(response):
         torch.cuda.synchronize()
         n = int(c1[0])
         assert n == int(cnt[k]) and torch.equal(b1[0, :n], blobs[k, :n]), k
+
+
+# ---------------------------------------------------------------- f32 input (f3)
+@pytest.mark.parametrize("size,cfg", [(256, C1), (1000, C3)])
+def test_f32_input_full_parity(size, cfg):
+    """float32 images (reading R24): radix-select percentiles on real values (negative and
+    positive, exact float32 bit patterns vs the oracle's sort), the stretch, and the rest of
+    the path on the CUDA-core schedules (pair kernels at W = 256, k_scale_space at 1000)."""
+    a = synth.em_tile_np(size, size, 1006, defocus=0.5, dose=300.0, bits=16).astype(np.float32)
+    img = (a * np.float32(0.37) - np.float32(7000.25)).astype(np.float32)   # real values, both signs
+    s = _full_parity(img, cfg)
+    assert s["n_oracle"] > 50
+    det = mhfd.Detector(size, size, threshold=_tau(cfg), **cfg)
+    assert det.schedule("f32") == ("k_rows_pair+k_cols_pair" if size == 256 else "k_scale_space")
+
+
+def test_f32_integer_valued_equals_u16():
+    """Integer-valued float32 input gives the u16 result: the same percentiles (as values),
+    the same stretch, hence the same blobs — a batch of two, one constant (degenerate)."""
+    a = synth.em_tile_np(512, 512, 1007, dose=300.0, bits=16)
+    imgs = np.stack([a, np.full_like(a, 1234)])
+    det = mhfd.Detector(512, 512, threshold=_tau(C3), **C3)
+    tu = torch.from_numpy(imgs.astype(np.int32)).cuda().to(torch.uint16)
+    tf = torch.from_numpy(imgs.astype(np.float32)).cuda()
+    bu, cu, _ = det.detect(tu)
+    bf, cf, _ = det.detect(tf)
+    torch.cuda.synchronize()
+    assert int(cf[1]) == 0 and int(cu[1]) == 0
+    n = int(cu[0])
+    assert int(cf[0]) == n and torch.equal(bf[0, :n], bu[0, :n])
