@@ -78,6 +78,8 @@ def _load():
                                             P, i64, P, P, P, P, P, P]),
                 "oracle_downsample": (i32, [P, i32, i32, i32, i32, P]),
                 "oracle_percentiles_f32": (i32, [P, i64, f64, f64, P, P]),
+                "oracle_set_boundary": (None, [i32]),
+                "oracle_get_boundary": (i32, []),
                 "oracle_stretch_f32": (None, [P, i64, f64, f64, P]),
                 "oracle_log_taps": (None, [f64, i32, P, P]),
                 "oracle_log_stack_rows": (None, [P, i32, i32, f64, f64, i32, i32, i32, P]),
@@ -90,6 +92,20 @@ def _load():
                 fn.argtypes = args
             _lib = lib
     return _lib
+
+
+class _boundary:
+    """Set the oracle's blur boundary for one call ("periodic", reading R7, or "reflect",
+    reading R25) and restore periodic afterwards."""
+
+    def __init__(self, boundary: str):
+        self.b = {"periodic": 0, "reflect": 1}[str(boundary)]
+
+    def __enter__(self):
+        _load().oracle_set_boundary(self.b)
+
+    def __exit__(self, *exc):
+        _load().oracle_set_boundary(0)
 
 
 def _ptr(a: np.ndarray | None):
@@ -168,24 +184,26 @@ def gaussian_taps(t: float, R: int | None = None) -> np.ndarray:
     return w
 
 
-def blur(f: np.ndarray, t: float, rows: tuple[int, int] | None = None) -> np.ndarray:
+def blur(f: np.ndarray, t: float, rows: tuple[int, int] | None = None, boundary: str = "periodic") -> np.ndarray:
     """Periodic L = G(t) * f, optionally only rows [y0, y1)."""
     f = np.ascontiguousarray(f, np.float64)
     H, W = f.shape
     y0, y1 = (0, H) if rows is None else rows
     out = np.empty((y1 - y0, W), np.float64)
-    _load().oracle_blur_rows(_ptr(f), H, W, t, y0, y1, _ptr(out))
+    with _boundary(boundary):
+        _load().oracle_blur_rows(_ptr(f), H, W, t, y0, y1, _ptr(out))
     return out
 
 
 def dog_stack(f: np.ndarray, min_t: float, max_t: float, n: int,
-              rows: tuple[int, int] | None = None) -> np.ndarray:
+              rows: tuple[int, int] | None = None, boundary: str = "periodic") -> np.ndarray:
     """Eq. 2 DoG planes D_i = t_i (L_{i+1} - L_i), i=1..n."""
     f = np.ascontiguousarray(f, np.float64)
     H, W = f.shape
     y0, y1 = (0, H) if rows is None else rows
     D = np.empty((n, y1 - y0, W), np.float64)
-    _load().oracle_dog_stack_rows(_ptr(f), H, W, min_t, max_t, n, y0, y1, _ptr(D))
+    with _boundary(boundary):
+        _load().oracle_dog_stack_rows(_ptr(f), H, W, min_t, max_t, n, y0, y1, _ptr(D))
     return D
 
 
@@ -200,23 +218,26 @@ def log_taps(t: float, R: int | None = None) -> tuple[np.ndarray, np.ndarray]:
 
 
 def log_stack(f: np.ndarray, min_t: float, max_t: float, n: int,
-              rows: tuple[int, int] | None = None) -> np.ndarray:
+              rows: tuple[int, int] | None = None, boundary: str = "periodic") -> np.ndarray:
     """Scale-normalised Laplacian planes t_i^2 (d_xx + d_yy) L(., t_i), i = 1..n
     (Eq. 1; reading R23)."""
     f = np.ascontiguousarray(f, np.float64)
     H, W = f.shape
     y0, y1 = (0, H) if rows is None else rows
     D = np.empty((n, y1 - y0, W), np.float64)
-    _load().oracle_log_stack_rows(_ptr(f), H, W, min_t, max_t, n, y0, y1, _ptr(D))
+    with _boundary(boundary):
+        _load().oracle_log_stack_rows(_ptr(f), H, W, min_t, max_t, n, y0, y1, _ptr(D))
     return D
 
 
-def dog_at(f: np.ndarray, min_t: float, max_t: float, n: int, y: int, x: int) -> np.ndarray:
+def dog_at(f: np.ndarray, min_t: float, max_t: float, n: int, y: int, x: int,
+           boundary: str = "periodic") -> np.ndarray:
     """Eq. 2 at one pixel from the 2-D definition (for sampled full-size checks)."""
     f = np.ascontiguousarray(f, np.float64)
     H, W = f.shape
     out = np.empty(n, np.float64)
-    _load().oracle_dog_at(_ptr(f), H, W, min_t, max_t, n, int(y), int(x), _ptr(out))
+    with _boundary(boundary):
+        _load().oracle_dog_at(_ptr(f), H, W, min_t, max_t, n, int(y), int(x), _ptr(out))
     return out
 
 
@@ -264,10 +285,12 @@ def prune(blobs: np.ndarray, min_t: float, max_t: float, n: int, overlap: float)
 
 def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, overlap: float,
            sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
-           strict: bool = False, dump: bool = False, polarity: str = "dark", response: str = "dog") -> dict:
+           strict: bool = False, dump: bool = False, polarity: str = "dark", response: str = "dog",
+           boundary: str = "periodic") -> dict:
     """Algorithm 1 + threshold + pruning; returns blobs, count, candidates.
     polarity "bright" negates the response (not in the paper); response
-    "log" replaces Eq. 2 by the scale-normalised Laplacian t_i^2 lap L(t_i) (reading R23)."""
+    "log" replaces Eq. 2 by the scale-normalised Laplacian t_i^2 lap L(t_i) (reading R23);
+    boundary "reflect" mirrors the image at its edges for the blur (reading R25)."""
     img, bpp = _img(img)
     H, W = img.shape
     mode = {"paper": 0, "26": 1}[str(nms)]
@@ -280,9 +303,10 @@ def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, over
     idx = np.empty((H, W), np.int32) if (dump and mode == 0) else None
     pol = {"dark": 0, "bright": 1}[str(polarity)]
     resp = {"dog": 0, "log": 1}[str(response)]
-    k = _load().oracle_detect_resp(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
-                                   mode, int(strict), pol, resp, _ptr(out), cap, ctypes.byref(ncand),
-                                   _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
+    with _boundary(boundary):
+        k = _load().oracle_detect_resp(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
+                                       mode, int(strict), pol, resp, _ptr(out), cap, ctypes.byref(ncand),
+                                       _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
     if k < 0:
         raise MemoryError("oracle_detect failed")
     res = {"blobs": out[:k].copy(), "count": int(k), "n_candidates": int(ncand.value),

@@ -171,7 +171,19 @@ void oracle_gaussian_taps(double t, int R, double* w /* 2R+1 */) {
   for (int d = -R; d <= R; ++d) w[d + R] /= s;
 }
 
+/* Image boundary of the blur: periodic (reading R7, the default) or half-sample
+ * symmetric reflection (SURVEY 8(f) f3 "reflect boundary", reading R25: ... c b a | a b c
+ * ... x y z | z y x ..., scipy.ndimage mode 'reflect').  A process-wide setting of this
+ * test oracle (oracle_set_boundary; the Python wrapper sets and restores it per call). */
+static int g_boundary = 0;
+void oracle_set_boundary(int b) { g_boundary = b ? 1 : 0; }
+int oracle_get_boundary(void) { return g_boundary; }
+
 static int64_t wrap(int64_t a, int64_t m) {
+  if (g_boundary) {
+    while (a < 0 || a >= m) a = a < 0 ? -a - 1 : 2 * m - 1 - a;
+    return a;
+  }
   int64_t r = a % m;
   return r < 0 ? r + m : r;
 }

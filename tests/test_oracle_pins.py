@@ -638,3 +638,46 @@ def test_f32_detect_equals_u8_on_integer_floats():
     b = oracle.detect(img.astype(np.float32), 1.0, 5.0, 5, 0.08, 0.5)
     assert a["count"] == b["count"] and np.array_equal(a["blobs"], b["blobs"])
     assert np.frombuffer(np.uint32(b["lo"]).tobytes(), np.float32)[0] == float(a["lo"])
+
+
+# ---------------------------------------------------------------- reflect boundary (f3)
+# SURVEY §8(f) f3 "reflect boundary"; reading R25 (half-sample symmetric, scipy 'reflect').
+
+@pytest.mark.parametrize("t", [1.0, 2.5, 4.0])
+def test_reflect_blur_matches_scipy(t):
+    rng = np.random.default_rng(31)
+    f = rng.random((57, 61))
+    R = oracle.radius(t)
+    ref = ndi.gaussian_filter(f, t, mode="reflect", radius=R)
+    assert np.abs(oracle.blur(f, t, boundary="reflect") - ref).max() < 1e-13
+
+
+def _mirror_tile(f):
+    # the half-sample-symmetric extension of f is the periodic extension of this 2H x 2W tile
+    top = np.concatenate([f, f[:, ::-1]], 1)
+    return np.concatenate([top, top[::-1, :]], 0)
+
+
+@pytest.mark.parametrize("stack", ["dog", "log"])
+def test_reflect_equals_periodic_on_mirror_tile(stack):
+    # reflect-boundary responses of f = periodic responses of the mirrored 2H x 2W tile
+    # restricted to f (a different formulation of the same boundary rule)
+    rng = np.random.default_rng(32)
+    f = rng.random((26, 30))
+    fn = oracle.dog_stack if stack == "dog" else oracle.log_stack
+    a = fn(f, 1.0, 2.0, 3, boundary="reflect")
+    b = fn(_mirror_tile(f), 1.0, 2.0, 3)[:, :26, :30]
+    assert np.abs(a - b).max() < 1e-13
+    # constant images respond 0 under either boundary
+    assert np.abs(fn(np.full((26, 30), 0.4), 1.0, 2.0, 3, boundary="reflect")).max() < 1e-14
+
+
+def test_reflect_boundary_changes_only_the_edges():
+    # far from the edges (> R_max) the two boundaries agree exactly
+    rng = np.random.default_rng(33)
+    f = rng.random((80, 84))
+    a = oracle.dog_stack(f, 1.0, 3.0, 2, boundary="reflect")
+    b = oracle.dog_stack(f, 1.0, 3.0, 2)
+    R = oracle.radius(3.0)
+    assert np.abs(a[:, R:-R, R:-R] - b[:, R:-R, R:-R]).max() < 1e-15
+    assert np.abs(a - b).max() > 1e-6
