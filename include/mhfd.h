@@ -90,6 +90,13 @@ typedef enum { MHFD_DARK = 0, MHFD_BRIGHT = 1 } mhfd_polarity;
  * LOG runs the two-pass CUDA-core schedule: width % 256 == 0 and 2n <= 62 required. */
 typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
 
+/* Image boundary of the blur (ABI 3).  MHFD_BOUNDARY_PERIODIC: what the paper's FFT
+ * computes (reading R7; default).  MHFD_BOUNDARY_REFLECT: half-sample
+ * symmetric extension (scipy.ndimage 'reflect', reading R25), run on
+ * the two-pass CUDA-core schedule: width % 256 == 0 required.  The NMS window keeps its
+ * -inf padding either way. */
+typedef enum { MHFD_BOUNDARY_PERIODIC = 0, MHFD_BOUNDARY_REFLECT = 1 } mhfd_boundary;
+
 typedef enum {
   MHFD_NMS_PAPER = 0, /* Eq. 3: global argmax over scale, 3x3 local max in space (default) */
   MHFD_NMS_26 = 1     /* conventional 3x3x3 scale-space maxima, 26 neighbours */
@@ -121,6 +128,7 @@ typedef struct {
                              reads as MHFD_DARK)                                     */
   int32_t response;       /* mhfd_response (ABI 3; a struct_size without this field
                              reads as MHFD_RESPONSE_DOG)                             */
+  int32_t boundary;       /* mhfd_boundary (ABI 3; absent -> MHFD_BOUNDARY_PERIODIC)  */
 } mhfd_params;
 
 /* One detected feature (x^_j, y^_j, i^_j) of Eq. 3 and its DoG

@@ -42,13 +42,15 @@ class Detector:
                  num_scales: int = 10, threshold: float | None = None, overlap: float = 0.5,
                  sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
                  strict: bool = False, device: int | None = None, max_candidates: int = 0,
-                 schedule: str | None = None, polarity: str = "dark", response: str = "dog"):
+                 schedule: str | None = None, polarity: str = "dark", response: str = "dog",
+                 boundary: str = "periodic"):
         """schedule: None (library default: k_tc for u8 where the tile fits) or one of
         "tc", "band", "band2", "generic" — forwarded as MHFD_SCHEDULE, which the library
         reads once in mhfd_create.  polarity: "dark" (Eq. 2 as written, the paper's EM
         sections) or "bright" (negated DoG: bright blobs on a dark background).  response:
         "dog" (Eq. 2, the paper's detector) or "log" (the scale-normalised Laplacian
-        t_i^2 lap L(t_i) that Eq. 2 approximates; reading R23)."""
+        t_i^2 lap L(t_i) that Eq. 2 approximates; reading R23).  boundary:
+        "periodic" (the paper's FFT) or "reflect" (mirrored edges; reading R25)."""
         lib = _abi.load()
         if device is None:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
@@ -60,7 +62,9 @@ class Detector:
                               nms={"paper": _abi.MHFD_NMS_PAPER, "26": _abi.MHFD_NMS_26}[str(nms)],
                               strict=int(bool(strict)), device=int(device), max_candidates=int(max_candidates),
                               polarity={"dark": _abi.MHFD_DARK, "bright": _abi.MHFD_BRIGHT}[str(polarity)],
-                              response={"dog": _abi.MHFD_RESPONSE_DOG, "log": _abi.MHFD_RESPONSE_LOG}[str(response)])
+                              response={"dog": _abi.MHFD_RESPONSE_DOG, "log": _abi.MHFD_RESPONSE_LOG}[str(response)],
+                              boundary={"periodic": _abi.MHFD_BOUNDARY_PERIODIC,
+                                        "reflect": _abi.MHFD_BOUNDARY_REFLECT}[str(boundary)])
         h = ctypes.c_void_p()
         if schedule is not None and schedule not in ("tc", "band", "band2", "generic"):
             raise ValueError(f"unknown schedule {schedule!r}")

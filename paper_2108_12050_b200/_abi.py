@@ -17,6 +17,7 @@ STATUS = {0: "MHFD_OK", 1: "MHFD_ERR_INVALID_ARGUMENT", 2: "MHFD_ERR_SHAPE", 3: 
 MHFD_U8, MHFD_U16, MHFD_F32 = 1, 2, 3
 MHFD_DARK, MHFD_BRIGHT = 0, 1
 MHFD_RESPONSE_DOG, MHFD_RESPONSE_LOG = 0, 1
+MHFD_BOUNDARY_PERIODIC, MHFD_BOUNDARY_REFLECT = 0, 1
 MHFD_NMS_PAPER, MHFD_NMS_26 = 0, 1
 
 # every symbol include/mhfd.h declares (checked by tests/test_abi.py)
@@ -34,7 +35,7 @@ class mhfd_params(ctypes.Structure):
                 ("threshold", ctypes.c_float), ("overlap", ctypes.c_float), ("sat_low", ctypes.c_float),
                 ("sat_high", ctypes.c_float), ("nms", ctypes.c_int32), ("strict", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("max_candidates", ctypes.c_int32), ("polarity", ctypes.c_int32),
-                ("response", ctypes.c_int32)]
+                ("response", ctypes.c_int32), ("boundary", ctypes.c_int32)]
 
 
 class mhfd_blob(ctypes.Structure):

@@ -187,6 +187,14 @@ __host__ __device__ inline int c3_rows(int R) { return kC2Rows + ((2 * R + 1 + 1
 __host__ __device__ inline int c3_buf_floats(int rmax) { return c3_rows(rmax) * kBandHP + c3_taps(rmax); }
 __host__ __device__ inline size_t c3_smem(int rmax) { return sizeof(float) * 2 * (size_t)c3_buf_floats(rmax) + 16; }
 
+// blur boundary index: periodic (reading R7) or half-sample symmetric reflection (R25);
+// |a| < 2m (one reflection: R_max < W, H)
+__device__ __forceinline__ int bidx(int a, int m, int reflect) {
+  if (reflect) return a < 0 ? -a - 1 : (a >= m ? 2 * m - 1 - a : a);
+  a %= m;
+  return a < 0 ? a + m : a;
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src)
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
                                                              const __grid_constant__ LevelTable tab,
                                                              float* __restrict__ v, uint8_t* __restrict__ idx,
                                                              float* __restrict__ dog,
-                                                             const ImgPar* __restrict__ par) {
+                                                             const ImgPar* __restrict__ par, int reflect) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* buf0 = reinterpret_cast<float*>(smem_raw);
   const int bufsz = c3_buf_floats(tab.rmax);
@@ -218,8 +226,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
     const int nr = c3_rows(R);
     for (int i = tid; i < nr * 8; i += kC3Threads) {
       const int r = i >> 3, c = i & 7;
-      int y = (Y0 - R + r) % H;
-      if (y < 0) y += H;
+      const int y = bidx(Y0 - R + r, H, reflect);
       cp_async16(hb + r * kBandHP + 4 * c, src + (int64_t)y * W + 4 * c);
     }
     const int cl = LOG ? (lev ^ 1) : lev;   // the level whose taps run along y
@@ -247,38 +254,40 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
     __syncthreads();   // level lev's window and taps are in
     const float* hb = buf0 + (lev & 1) * bufsz;
     const float* wc = hb + c3_rows(tab.rmax) * kBandHP;
-    if (!LOG) {
-      col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, lev,
-                        lev > 0 ? tab.tdog[lev - 1] : 0.f, lprev, vbest, ibest);
-    } else {
-      // lev = 0: col_pass only returns the 16 column sums in lprev
-      col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, 0, 0.f, lprev, vbest, ibest);
-      if ((lev & 1) == 0) {
+    // lev = 0: col_pass only returns the 16 column sums (in Lc)
+    float Lc[16];
+    col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, 0, 0.f, Lc, vbest, ibest);
+    // plane i gets its response now: DoG plane lev - 1 = tdog (L_lev - L_{lev-1}) (Eq. 2),
+    // LoG plane lev / 2 = tdog (d_yy + d_xx) at odd sub-levels (reading R23)
+    const bool emit = LOG ? (lev & 1) != 0 : lev > 0;
+    if (emit) {
+      const int i = LOG ? lev >> 1 : lev - 1;
+      const float tf = LOG ? tab.tdog[lev] : tab.tdog[lev - 1];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) part[k] = lprev[k];
-      } else {
-        const int i = lev >> 1;
-        const float tf = tab.tdog[lev];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float D = degen ? 0.f : tf * (part[k] + lprev[k]);
-          if (D > vbest[k]) {
-            vbest[k] = D;
-            const int sh = (k & 3) * 8;
-            ibest[k >> 2] = (ibest[k >> 2] & ~(0xffu << sh)) | ((uint32_t)i << sh);
-          }
-          part[k] = D;
+      for (int k = 0; k < 16; ++k) {
+        const float D = degen ? 0.f : (LOG ? tf * (part[k] + Lc[k]) : tf * (Lc[k] - part[k]));
+        if (D > vbest[k]) {
+          vbest[k] = D;
+          const int sh = (k & 3) * 8;
+          ibest[k >> 2] = (ibest[k >> 2] & ~(0xffu << sh)) | ((uint32_t)i << sh);
         }
-        if (dog) {
+        lprev[k] = D;
+      }
+      if (dog) {
+        const int nplanes = LOG ? tab.nlev / 2 : tab.nlev - 1;
 #pragma unroll
-          for (int o = 0; o < 8; ++o) {
-            const int y = Y0 + 8 * rg + o;
-            if (y < H)
-              *reinterpret_cast<float2*>(dog + ((int64_t)b * (tab.nlev / 2) + i) * plane + (int64_t)y * W + x0 +
-                                         2 * cp) = make_float2(part[2 * o], part[2 * o + 1]);
-          }
+        for (int o = 0; o < 8; ++o) {
+          const int y = Y0 + 8 * rg + o;
+          if (y < H)
+            *reinterpret_cast<float2*>(dog + ((int64_t)b * nplanes + i) * plane + (int64_t)y * W + x0 + 2 * cp) =
+                make_float2(lprev[2 * o], lprev[2 * o + 1]);
         }
       }
+    }
+    // DoG: the next level's difference needs L_lev; LoG: d_yy of the next plane
+    if (!LOG || (lev & 1) == 0) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) part[k] = Lc[k];
     }
     __syncthreads();   // buffer lev & 1 is free for level lev + 2
   }
@@ -317,7 +326,7 @@ __host__ __device__ inline size_t r3_smem(int rmax, int taps_total) {
 
 __global__ void __launch_bounds__(kC3Threads, 1) k_rows_pair(const float* __restrict__ fimg, int W, int H,
                                                              const __grid_constant__ LevelTable tab,
-                                                             float* __restrict__ rx_all, int B) {
+                                                             float* __restrict__ rx_all, int B, int reflect) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* T = reinterpret_cast<float*>(smem_raw);                 // r3_nx x kBandHP, T[xi][row]
   const int NX = r3_nx(tab.rmax);
@@ -331,12 +340,17 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_rows_pair(const float* __rest
     // lane = row (conflict-free transposed stores), 32 contiguous bytes of that row per chunk
     const float* row = fimg + (int64_t)b * plane + (int64_t)min(y0 + lane, H - 1) * W;
     for (int q = warp; q < NX / 8; q += kC3Threads / 32) {
-      int xa = (xs + 8 * q) % W;
-      if (xa < 0) xa += W;
-      int xb = xa + 4;
-      if (xb >= W) xb -= W;
-      const float4 a = __ldg(reinterpret_cast<const float4*>(row + xa));
-      const float4 c = __ldg(reinterpret_cast<const float4*>(row + xb));
+      const int xq = xs + 8 * q;
+      float4 a, c;
+      if (!reflect || (xq >= 0 && xq + 8 <= W)) {   // periodic (4-aligned, never straddles) or interior
+        const int xa = bidx(xq, W, 0), xb = bidx(xq + 4, W, 0);
+        a = __ldg(reinterpret_cast<const float4*>(row + xa));
+        c = __ldg(reinterpret_cast<const float4*>(row + xb));
+      } else {   // mirrored edge pieces, pixel by pixel
+        a = make_float4(row[bidx(xq, W, 1)], row[bidx(xq + 1, W, 1)], row[bidx(xq + 2, W, 1)], row[bidx(xq + 3, W, 1)]);
+        c = make_float4(row[bidx(xq + 4, W, 1)], row[bidx(xq + 5, W, 1)], row[bidx(xq + 6, W, 1)],
+                        row[bidx(xq + 7, W, 1)]);
+      }
       float* d = T + (8 * q) * kBandHP + lane;
       d[0 * kBandHP] = a.x; d[1 * kBandHP] = a.y; d[2 * kBandHP] = a.z; d[3 * kBandHP] = a.w;
       d[4 * kBandHP] = c.x; d[5 * kBandHP] = c.y; d[6 * kBandHP] = c.z; d[7 * kBandHP] = c.w;

@@ -105,10 +105,13 @@ int64_t wl_cap_of(const mhfd_ctx* c, int B) {
 
 // paper-mode two-pass kernels (k_rows_pair / k_cols_pair) fit; MHFD_NO_COLS_PAIR=1 selects
 // k_rows2 / k_cols_all instead
-bool pair_ok(const mhfd_ctx* c) {
+bool pair_fit(const mhfd_ctx* c) {
   const LevelTable& T = *c->tab;
-  return c->p.nms == MHFD_NMS_PAPER && c->band_enabled && c->p.width % kR3Cols == 0 && c3_smem(T.rmax) <= kSmemLimit &&
+  return c->band_enabled && c->p.width % kR3Cols == 0 && c3_smem(T.rmax) <= kSmemLimit &&
          r3_smem(T.rmax, r3_taps_total(T)) <= kSmemLimit && getenv("MHFD_NO_COLS_PAIR") == nullptr;
+}
+bool pair_ok(const mhfd_ctx* c) {
+  return (c->p.nms == MHFD_NMS_PAPER || c->p.boundary == MHFD_BOUNDARY_REFLECT) && pair_fit(c);
 }
 
 Layout layout(const mhfd_ctx* c, int B) {
@@ -144,7 +147,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   // two-pass schedules: Rx of every level (LoG: of each of the 2n sub-levels) for up to
   // kRxBatch images (run_front chunks larger batches)
   const int64_t rxb = std::min(B, kRxBatch);
-  const bool any2 = c->ltab || c->twopass || pair_ok(c);
+  const bool any2 = c->ltab || c->twopass || pair_fit(c);
   L.rx = take(any2 ? sizeof(float) * plane * rxb * (c->ltab ? 2 * c->n : c->n + 1) : 0);
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
@@ -318,7 +321,9 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // k_tc also writes the DoG planes: for the 26-neighbour NMS and for debug dumps
   float* tc_dog = dog_dump ? dog_dump : (paper ? nullptr : reinterpret_cast<float*>(ws + L.dog));
   const bool dogr = c->p.response == MHFD_RESPONSE_DOG;
-  if (dogr && bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
+  const int reflect = c->p.boundary == MHFD_BOUNDARY_REFLECT ? 1 : 0;   // reading R25: two-pass only
+  const bool fused_ok = dogr && !reflect;
+  if (fused_ok && bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
       (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
@@ -344,7 +349,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   }
   if (band) return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
   // ---- a2-a6 on u8 images, two-CTA band schedule
-  if (dogr && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
+  if (fused_ok && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
       band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
     const size_t smem = band2_smem(c->tab->rmax, c->tab->ntaps_total);
     cudaError_t ea = cudaFuncSetAttribute(k_band2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -356,7 +361,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
   }
   // ---- a2-a6 on u8 images: band schedule (raw band staged once per CTA, no f32 prepass)
-  if (dogr && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
+  if (fused_ok && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
       band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
     const size_t smem = band_smem(c->tab->rmax, c->tab->ntaps_total);
     cudaError_t ea = cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -398,8 +403,10 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // (always), the paper-mode DoG pair kernels (any radius: 1.5x the fused generic kernel
   // on u16 at sigma 1-10), and large radii with DoG planes
   // (k_rows2 / k_cols_all).  Rx holds at most kRxBatch images: larger batches run in chunks.
-  const bool pair = dogr && paper && !write_dog && pair_ok(c);
-  const bool big = dogr && !pair && c->twopass && W % kR2Cols == 0;
+  const bool pair = dogr && pair_fit(c) && (reflect || (paper && !write_dog));
+  const bool big = dogr && !pair && !reflect && c->twopass && W % kR2Cols == 0;
+  if (reflect && dogr && !pair)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "reflect boundary needs the two-pass schedule (MHFD_SCHEDULE/NO_COLS_PAIR)");
   if (!dogr || pair || big) {
     const LevelTable& T = dogr ? *c->tab : *c->ltab;
     float* rx = reinterpret_cast<float*>(ws + L.rx);
@@ -424,7 +431,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       float* dc = write_dog ? dog + (int64_t)b0 * nplanes * plane : nullptr;
       const dim3 gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, Bc);
       if (rows_pair) {   // every level's row blur in one launch
-        k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, Bc), kC3Threads, sm_p, st>>>(fi, W, H, T, rx, Bc);
+        k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, Bc), kC3Threads, sm_p, st>>>(fi, W, H, T, rx, Bc, reflect);
         LAUNCH_CHECK("k_rows_pair");
       } else {
         for (int lev = 0; lev < T.nlev; ++lev) {
@@ -434,9 +441,9 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
         }
       }
       if (!dogr) {
-        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
+        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect);
       } else if (pair) {
-        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, nullptr, pc);
+        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect);
       } else {
         k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
       }
@@ -624,6 +631,10 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     return fail(MHFD_ERR_INVALID_ARGUMENT, "LoG response: 2 num_scales = %d > %d", 2 * p->num_scales, kMaxLevels - 2);
   if (p->response == MHFD_RESPONSE_LOG && p->width % kR3Cols != 0)
     return fail(MHFD_ERR_SHAPE, "LoG response: width %d is not a multiple of %d", p->width, kR3Cols);
+  if (p->boundary != MHFD_BOUNDARY_PERIODIC && p->boundary != MHFD_BOUNDARY_REFLECT)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "boundary %d", p->boundary);
+  if (p->boundary == MHFD_BOUNDARY_REFLECT && p->width % kR3Cols != 0)
+    return fail(MHFD_ERR_SHAPE, "reflect boundary: width %d is not a multiple of %d", p->width, kR3Cols);
   if (!(std::isfinite(p->min_sigma) && p->min_sigma > 0.f))
     return fail(MHFD_ERR_INVALID_ARGUMENT, "min_sigma must be > 0 (NonPositiveScale)");
   if (!(std::isfinite(p->max_sigma) && p->max_sigma > p->min_sigma))
@@ -988,6 +999,7 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   const int W = c->p.width, H = c->p.height;
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   if (c->p.response == MHFD_RESPONSE_LOG) return "k_rows_pair+k_cols_pair<log>";
+  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
   if (dtype == MHFD_U8 && paper && c->band_enabled) {
     if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";

@@ -154,3 +154,16 @@ def test_abi2_struct_size_reads_response_as_dog():
     h = ctypes.c_void_p()
     assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == 1
     assert "min_sigma" in lib.mhfd_last_error().decode()
+
+
+@pytest.mark.parametrize("W,b,status", [(300, 1, 2), (256, 2, 1)])
+def test_boundary_validates_before_device(W, b, status):
+    # reflect (reading R25) runs the two-pass kernels: width % 256 == 0; unknown values rejected
+    lib = _abi.load()
+    p = _abi.mhfd_params()
+    lib.mhfd_params_default(ctypes.byref(p))
+    p.width, p.height, p.max_sigma = W, 256, 5.0
+    p.boundary = b
+    h = ctypes.c_void_p()
+    assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == status
+    assert "boundary" in lib.mhfd_last_error().decode()

@@ -36,17 +36,17 @@ def _to_t(img):
 
 
 def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, schedule=None, polarity="dark",
-                 response="dog"):
+                 response="dog", boundary="periodic"):
     """Full comparison on one image: percentiles, DoG stack, v/argmax, candidates,
     pruned blobs, counts and score."""
     H, W = img.shape
     tau = _tau(cfg) if tau is None else tau
     n = cfg["num_scales"]
     det = mhfd.Detector(W, H, threshold=tau, overlap=overlap, nms=nms, strict=strict, schedule=schedule,
-                        polarity=polarity, response=response, **cfg)
+                        polarity=polarity, response=response, boundary=boundary, **cfg)
     dump = det.debug_dump(_to_t(img))
     ref = oracle.detect(img, cfg["min_sigma"], cfg["max_sigma"], n, tau, overlap, nms=nms, strict=strict, dump=True,
-                        polarity=polarity, response=response)
+                        polarity=polarity, response=response, boundary=boundary)
     # a1: percentiles, exact integers
     lo, hi = dump["lohi"][0].tolist()
     if img.dtype == np.float32:   # float32 bit patterns (reading R24)
@@ -601,3 +601,34 @@ def test_f32_integer_valued_equals_u16():
     assert int(cf[1]) == 0 and int(cu[1]) == 0
     n = int(cu[0])
     assert int(cf[0]) == n and torch.equal(bf[0, :n], bu[0, :n])
+
+
+# ---------------------------------------------------------------- reflect boundary (f3)
+@pytest.mark.parametrize("nms,response", [("paper", "dog"), ("26", "dog"), ("paper", "log")])
+def test_reflect_boundary_full_parity(c1_img, nms, response):
+    """boundary="reflect" (reading R25) on the two-pass kernels: mirrored windows at all four
+    edges (row staging pixel by pixel at the left/right edges, mirrored rows top/bottom),
+    against the oracle's reflect blur; DoG in both NMS modes (the DoG variant writes its
+    planes for the 26-neighbour NMS) and the LoG response."""
+    tau = 0.1 if response == "log" else None
+    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response=response, boundary="reflect")
+    assert s["n_oracle"] > 100
+    det = mhfd.Detector(256, 256, threshold=0.08, boundary="reflect", **C1)
+    assert det.schedule("u8") == "k_rows_pair+k_cols_pair"
+
+
+def test_reflect_differs_from_periodic_only_near_edges():
+    """v under the two boundaries on the same pair kernels (u16): bit-identical farther
+    than R_max from every edge (same staged values, same sums), different near the edges
+    of a non-periodic image."""
+    a16 = synth.em_tile_np(256, 512, 1008, dose=300.0, bits=16)
+    img = torch.from_numpy(a16.astype(np.int32)).cuda().to(torch.uint16)
+    res = []
+    for bd in ("periodic", "reflect"):
+        det = mhfd.Detector(512, 256, threshold=0.08, boundary=bd, **C1)
+        assert det.schedule("u16") == "k_rows_pair+k_cols_pair"
+        res.append(det.debug_dump(img, dog=False, cands=False)["v"][0].cpu())
+    R = 25   # ceil(5 * 5)
+    a, b = res
+    assert torch.equal(a[R:-R, R:-R], b[R:-R, R:-R])
+    assert float((a - b).abs().max()) > 1e-4
