@@ -632,3 +632,28 @@ def test_reflect_differs_from_periodic_only_near_edges():
     a, b = res
     assert torch.equal(a[R:-R, R:-R], b[R:-R, R:-R])
     assert float((a - b).abs().max()) > 1e-4
+
+
+# ---------------------------------------------------------------- host-buffer path (e2e API)
+@pytest.mark.parametrize("kind", ["u8", "u16", "f32", "u8-log"])
+def test_focus_score_host_equals_device(kind):
+    """mhfd_focus_score_host (pinned host batch, chunked H2D copies on a second stream
+    overlapped with compute, ramped chunk sizes) returns exactly the device path's scores
+    and counts: batch 11 with chunk 4 (chunks of 1, 2, 4, 4)."""
+    B, n = 11, 512
+    a = np.stack([synth.em_tile_np(n, n, 1500 + k, defocus=0.3 * (k % 4), dose=300.0,
+                                   bits=8 if kind.startswith("u8") else 16) for k in range(B)])
+    if kind == "u16":
+        host = torch.from_numpy(a.astype(np.int32)).to(torch.uint16)
+    elif kind == "f32":
+        host = torch.from_numpy((a.astype(np.float32) * np.float32(0.5)) - np.float32(3.25))
+    else:
+        host = torch.from_numpy(a)
+    host = host.pin_memory()
+    det = mhfd.Detector(n, n, threshold=0.1 if kind == "u8-log" else _tau(C3),
+                        response="log" if kind == "u8-log" else "dog", **C3)
+    dev_scores, dev_counts = det.focus_score(host.cuda(), counts=True)
+    hs, hc = det.focus_score_host(host, chunk=4, counts=True)
+    torch.cuda.synchronize()
+    assert torch.equal(hs, dev_scores.cpu()) and torch.equal(hc, dev_counts.cpu())
+    assert float(hs.min()) > 0
