@@ -657,3 +657,30 @@ def test_focus_score_host_equals_device(kind):
     torch.cuda.synchronize()
     assert torch.equal(hs, dev_scores.cpu()) and torch.equal(hc, dev_counts.cpu())
     assert float(hs.min()) > 0
+
+
+def test_downsample_pitched_buffers():
+    """mhfd_downsample through the C ABI with row pitches wider than the rows (input and
+    output), u8 factor 2 (vector path off: odd width) and u16 factor 3: bit-exact, and the
+    padding bytes of the output rows are left untouched."""
+    from paper_2108_12050_b200 import _abi
+    lib = _abi.load()
+    rng = np.random.default_rng(78)
+    for dt, npd, code, bpp, f in ((torch.uint8, np.uint8, _abi.MHFD_U8, 1, 2), (torch.int16, np.uint16, _abi.MHFD_U16, 2, 3)):
+        H, W, B = 37, 45, 2
+        a = rng.integers(0, 256 if bpp == 1 else 65536, size=(B, H, W)).astype(npd)
+        ip, OW, OH = (W * bpp + 32 + 15) // 16 * 16, -(-W // f), -(-H // f)
+        op = (OW * bpp + 16 + 15) // 16 * 16
+        src = torch.zeros((B, H, ip), dtype=torch.uint8)
+        src.view(B, H, ip)[:, :, :W * bpp] = torch.from_numpy(a.view(np.uint8).reshape(B, H, W * bpp))
+        src = src.cuda()
+        dst = torch.full((B, OH, op), 0xAB, dtype=torch.uint8, device="cuda")
+        st = lib.mhfd_downsample(src.data_ptr(), code, W, H, ip, f, dst.data_ptr(), op, B,
+                                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert st == 0
+        d = dst.cpu().numpy()
+        for b in range(B):
+            got = d[b, :, :OW * bpp].copy().view(npd).reshape(OH, OW)
+            assert np.array_equal(got, oracle.downsample(a[b], f))
+        assert (d[:, :, OW * bpp:] == 0xAB).all()
