@@ -42,6 +42,20 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
       uint4 q = __ldg(row + v);
       uint32_t wds[4] = {q.x, q.y, q.z, q.w};
       const int base = v * 16;
+      if (!SECOND && base + 16 <= row_bytes) {   // whole vector inside the row: no per-pixel test
+        uint32_t* hw = sh[warp];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (BPP == 1) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicAdd(hw + ((wds[k] >> (8 * j)) & 255u), 1u);
+          } else {
+            atomicAdd(hw + ((wds[k] >> 8) & 255u), 1u);
+            atomicAdd(hw + (wds[k] >> 24), 1u);
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (BPP == 1) {
