@@ -278,6 +278,7 @@ def other_configs(dev) -> dict:
             f"u{bits}"), "device_ms": dms, "host_visible_ms": hms, "MPix_per_s_device": size * size / dms / 1e3,
             "score": score}
     out["C3_bands_1gpu"] = band_times(dev)
+    out["C5_bands_1gpu"] = band_times(dev, c5=True)
     out["downsample_f2"] = downsample_times(dev)
     # C3 with the LoG response (reading R23): 4 FP32 convolutions per plane
     img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
@@ -320,16 +321,24 @@ def downsample_times(dev) -> dict:
             "kernel": "k_downsample2<uint8_t>"}
 
 
-def band_times(dev) -> dict:
+def band_times(dev, c5: bool = False) -> dict:
     """Single-image sharding measured on one GPU: for G bands of one
-    4096^2 tile, the device time of each rank's mhfd_detect_band (max over bands) and of
-    mhfd_prune_candidates on the full list — the compute a G-GPU run does per image
+    4096^2 u8 tile (k_tc) or, with c5, one 8192^2 u16 tile at sigma 1-30, 20 scales (the
+    pair kernels), the device time of each rank's mhfd_detect_band (max over bands) and
+    of mhfd_prune_candidates on the full list — the compute a G-GPU run does per image
     (the broadcast and the two all-gathers are not included)."""
     import synth
     import paper_2108_12050_b200 as mhfd
     from paper_2108_12050_b200.dist import band_rows
-    img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
-    det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP, device=dev.index)
+    size = 8192 if c5 else SIZE
+    if c5:
+        img = synth.em_tile(size, size, 7, defocus=0.0, dose=300.0, bits=16, device=dev)
+        img = torch.from_numpy(img.to(torch.int32).cpu().numpy().astype(np.uint16)).to(dev)
+        det = mhfd.Detector(size, size, 1.0, 30.0, 20, threshold=0.145, overlap=OVERLAP, device=dev.index)
+    else:
+        img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
+        det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP,
+                            device=dev.index)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def t(fn):
@@ -345,11 +354,11 @@ def band_times(dev) -> dict:
             ms.append(e0.elapsed_time(e1))
         return statistics.median(ms)
 
-    res = {}
+    res = {"schedule": det.schedule("u16" if c5 else "u8")}
     for G in (1, 2, 4, 8):
         bands, parts = [], []
         for r in range(G):
-            y0, y1 = band_rows(SIZE, G, r)
+            y0, y1 = band_rows(size, G, r)
             bands.append(t(lambda: det.detect_band(img, y0, y1)))
             c, nn = det.detect_band(img, y0, y1)
             parts.append(c[:int(nn)].clone())

@@ -228,14 +228,15 @@ mhfd_status mhfd_debug_dump(mhfd_ctx* c, const void* d_images, int32_t dtype, in
  * (the only step that needs every band: overlaps cross band edges).
  *
  * mhfd_detect_band: candidates of rows [y0, y1) of ONE image.
- *  d_image        : height x pitch_bytes bytes (u8; the "k_tc" schedule, Eq. 3 NMS)
+ *  d_image        : height x pitch_bytes bytes (the "k_tc" schedule for u8, or the
+ *                   "k_rows_pair+k_cols_pair" schedule for u16/f32; Eq. 3 NMS)
  *  0 <= y0 < y1 <= height; width % 1024 == 0
  *  d_workspace    : >= mhfd_workspace_bytes(c, 1)
  *  d_cands        : cand_capacity records; the band's candidates in (y, x) order,
  *                   truncated to cand_capacity (the count is exact)
  *  d_ncand        : 1 int32, the band's exact candidate count
  * Errors: as mhfd_detect_batch; SHAPE for the band/width; INVALID_ARGUMENT when the
- * context's u8 schedule is not "k_tc". */
+ * context's schedule for dtype is neither of those two. */
 mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, int64_t pitch_bytes, int32_t y0,
                              int32_t y1, void* d_workspace, size_t workspace_bytes, mhfd_blob* d_cands,
                              int32_t cand_capacity, int32_t* d_ncand, void* stream);

@@ -210,11 +210,13 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
                                                              const __grid_constant__ LevelTable tab,
                                                              float* __restrict__ v, uint8_t* __restrict__ idx,
                                                              float* __restrict__ dog,
-                                                             const ImgPar* __restrict__ par, int reflect) {
+                                                             const ImgPar* __restrict__ par, int reflect,
+                                                             int ty0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* buf0 = reinterpret_cast<float*>(smem_raw);
   const int bufsz = c3_buf_floats(tab.rmax);
-  const int b = blockIdx.z, Y0 = blockIdx.y * kC2Rows, x0 = blockIdx.x * kStripW;
+  // ty0: first 256-row output tile (single-image bands compute a sub-range of tiles)
+  const int b = blockIdx.z, Y0 = (blockIdx.y + ty0) * kC2Rows, x0 = blockIdx.x * kStripW;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t plane = (int64_t)H * W;
   // stage level `lev` into buffer `k`: rows Y0 - R .. (c3_rows), wrapped; taps 0..2R
@@ -326,12 +328,14 @@ __host__ __device__ inline size_t r3_smem(int rmax, int taps_total) {
 
 __global__ void __launch_bounds__(kC3Threads, 1) k_rows_pair(const float* __restrict__ fimg, int W, int H,
                                                              const __grid_constant__ LevelTable tab,
-                                                             float* __restrict__ rx_all, int B, int reflect) {
+                                                             float* __restrict__ rx_all, int B, int reflect,
+                                                             int ry0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* T = reinterpret_cast<float*>(smem_raw);                 // r3_nx x kBandHP, T[xi][row]
   const int NX = r3_nx(tab.rmax);
   float* wc_all = T + NX * kBandHP;
-  const int b = blockIdx.z, y0 = blockIdx.y * 32, x0 = blockIdx.x * kR3Cols;
+  // ry0: first 32-row tile (single-image bands compute the Rx rows their columns need)
+  const int b = blockIdx.z, y0 = (blockIdx.y + ry0) * 32, x0 = blockIdx.x * kR3Cols;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t plane = (int64_t)H * W;
   const int pm = r3_pre(tab.rmax);

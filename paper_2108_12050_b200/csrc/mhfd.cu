@@ -347,7 +347,8 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
   }
-  if (band) return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
+  if (band && !(c->p.response == MHFD_RESPONSE_DOG && paper && dog_dump == nullptr && pair_fit(c)))
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc or the two-pass pair schedule (Eq. 3 NMS)");
   // ---- a2-a6 on u8 images, two-CTA band schedule
   if (fused_ok && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
       band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
@@ -422,6 +423,23 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
                   : cudaFuncSetAttribute(k_cols_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_c);
     if (ea != cudaSuccess) return cuda_fail(ea, "two-pass attributes");
     const int nplanes = c->n;   // DoG / LoG planes written for the 26 mode and dumps
+    // single-image band (f2): output tiles covering rows [band_lo - 1, band_hi + 1) on the
+    // whole image's 256-row grid (same sums as the whole-image run), and only the Rx rows
+    // their windows read, as at most two row ranges (the periodic wrap)
+    int ct0 = 0, nct = (H + kC2Rows - 1) / kC2Rows;
+    int rr[2][2] = {{0, H}, {0, 0}};   // Rx row ranges [start, end)
+    if (band) {
+      const int o_lo = std::max(0, band_lo - 1), o_hi = std::min(H, band_hi + 1);
+      ct0 = o_lo / kC2Rows;
+      nct = (o_hi + kC2Rows - 1) / kC2Rows - ct0;
+      const int lo = ct0 * kC2Rows - T.rmax, hi = std::min(H, (ct0 + nct) * kC2Rows) + T.rmax;
+      if (hi - lo < H) {
+        rr[0][0] = std::max(0, lo);
+        rr[0][1] = std::min(H, hi);
+        if (lo < 0) { rr[1][0] = H + lo; rr[1][1] = H; }
+        if (hi > H) { rr[1][0] = 0; rr[1][1] = hi - H; }
+      }
+    }
     for (int b0 = 0; b0 < B; b0 += kRxBatch) {
       const int Bc = std::min(kRxBatch, B - b0);
       const float* fi = fimg + (int64_t)b0 * plane;
@@ -429,10 +447,14 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       float* vc = paper ? v + (int64_t)b0 * plane : nullptr;
       uint8_t* ic = paper ? idx + (int64_t)b0 * plane : nullptr;
       float* dc = write_dog ? dog + (int64_t)b0 * nplanes * plane : nullptr;
-      const dim3 gc((W + kStripW - 1) / kStripW, (H + kC2Rows - 1) / kC2Rows, Bc);
-      if (rows_pair) {   // every level's row blur in one launch
-        k_rows_pair<<<dim3(W / kR3Cols, (H + 31) / 32, Bc), kC3Threads, sm_p, st>>>(fi, W, H, T, rx, Bc, reflect);
-        LAUNCH_CHECK("k_rows_pair");
+      const dim3 gc((W + kStripW - 1) / kStripW, nct, Bc);
+      if (rows_pair) {   // every level's row blur in one launch (per Rx row range)
+        for (int k = 0; k < 2; ++k) {
+          if (rr[k][1] <= rr[k][0]) continue;
+          const int t0 = rr[k][0] / 32, t1 = (rr[k][1] + 31) / 32;
+          k_rows_pair<<<dim3(W / kR3Cols, t1 - t0, Bc), kC3Threads, sm_p, st>>>(fi, W, H, T, rx, Bc, reflect, t0);
+          LAUNCH_CHECK("k_rows_pair");
+        }
       } else {
         for (int lev = 0; lev < T.nlev; ++lev) {
           k_rows2<<<dim3(W / kR2Cols, (H + 31) / 32, Bc), 256, sm_p, st>>>(fi, W, H, T, lev,
@@ -441,16 +463,16 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
         }
       }
       if (!dogr) {
-        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect);
+        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0);
       } else if (pair) {
-        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect);
+        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0);
       } else {
         k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
       }
       LAUNCH_CHECK("k_cols");
     }
     MARK(2);
-    return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev);
+    return run_nms(c, W, H, B, ws, L, v, idx, dog, st, launches, ev, band_lo, band_hi);
   }
   const int strips = (W + kStripW - 1) / kStripW;
   // band height: 256 rows when that still gives >= 4 waves of 2 CTAs/SM, else 128
@@ -1043,8 +1065,9 @@ mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, in
   const int W = c->p.width, H = c->p.height;
   if (!(0 <= y0 && y0 < y1 && y1 <= H)) return fail(MHFD_ERR_SHAPE, "band rows [%d, %d) not inside [0, %d)", y0, y1, H);
   if (W % kSeg != 0) return fail(MHFD_ERR_SHAPE, "band mode needs width %% %d == 0", kSeg);
-  if (strcmp(mhfd_schedule_name(c, dtype), "k_tc") != 0)
-    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc schedule (u8, Eq. 3 NMS)");
+  const char* sch = mhfd_schedule_name(c, dtype);
+  if (strcmp(sch, "k_tc") != 0 && strcmp(sch, "k_rows_pair+k_cols_pair") != 0)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc or the two-pass pair schedule (Eq. 3 NMS)");
   if (!d_ncand || (!d_cands && cand_capacity > 0) || cand_capacity < 0)
     return fail(MHFD_ERR_INVALID_ARGUMENT, "d_ncand / d_cands / cand_capacity");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
