@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
                                                              float* __restrict__ v, uint8_t* __restrict__ idx,
                                                              float* __restrict__ dog,
                                                              const ImgPar* __restrict__ par, int reflect,
-                                                             int ty0) {
+                                                             int ty0, int need_lo, int need_hi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* buf0 = reinterpret_cast<float*>(smem_raw);
   const int bufsz = c3_buf_floats(tab.rmax);
@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
 #pragma unroll
   for (int k = 0; k < 4; ++k) ibest[k] = 0u;
   const bool degen = par[b].degen != 0;
+  // single-image bands: rows outside [need_lo, need_hi) need no response (whole 8-row
+  // groups skip the column convolution)
+  const bool active = Y0 + 8 * rg < need_hi && Y0 + 8 * rg + 8 > need_lo;
   stage(0, 0);
   for (int lev = 0; lev < tab.nlev; ++lev) {
     if (lev + 1 < tab.nlev) {
@@ -256,6 +259,9 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
     __syncthreads();   // level lev's window and taps are in
     const float* hb = buf0 + (lev & 1) * bufsz;
     const float* wc = hb + c3_rows(tab.rmax) * kBandHP;
+    // threads whose 8 rows are outside [need_lo, need_hi) only stage and take the barriers
+    // (both __syncthreads stay outside the branch: the groups of one warp can differ)
+    if (active) {
     // lev = 0: col_pass only returns the 16 column sums (in Lc)
     float Lc[16];
     col_pass<kBandHP>(hb + 8 * rg * kBandHP + 2 * cp, wc, 2 * tab.R[lev] + 1, 0, 0.f, Lc, vbest, ibest);
@@ -291,9 +297,10 @@ __global__ void __launch_bounds__(kC3Threads, 1) k_cols_pair(const float* __rest
 #pragma unroll
       for (int k = 0; k < 16; ++k) part[k] = Lc[k];
     }
+    }   // active
     __syncthreads();   // buffer lev & 1 is free for level lev + 2
   }
-  if (!v) return;
+  if (!v || !active) return;
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
     const int y = Y0 + 8 * rg + o;

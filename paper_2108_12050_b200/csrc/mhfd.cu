@@ -426,13 +426,15 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     // single-image band (f2): output tiles covering rows [band_lo - 1, band_hi + 1) on the
     // whole image's 256-row grid (same sums as the whole-image run), and only the Rx rows
     // their windows read, as at most two row ranges (the periodic wrap)
-    int ct0 = 0, nct = (H + kC2Rows - 1) / kC2Rows;
+    int ct0 = 0, nct = (H + kC2Rows - 1) / kC2Rows, need_lo = 0, need_hi = H;
     int rr[2][2] = {{0, H}, {0, 0}};   // Rx row ranges [start, end)
     if (band) {
       const int o_lo = std::max(0, band_lo - 1), o_hi = std::min(H, band_hi + 1);
       ct0 = o_lo / kC2Rows;
       nct = (o_hi + kC2Rows - 1) / kC2Rows - ct0;
-      const int lo = ct0 * kC2Rows - T.rmax, hi = std::min(H, (ct0 + nct) * kC2Rows) + T.rmax;
+      need_lo = o_lo;   // k_cols_pair skips 8-row groups outside [o_lo, o_hi)
+      need_hi = o_hi;
+      const int lo = o_lo / 8 * 8 - T.rmax, hi = std::min(H, (o_hi + 7) / 8 * 8) + T.rmax;
       if (hi - lo < H) {
         rr[0][0] = std::max(0, lo);
         rr[0][1] = std::min(H, hi);
@@ -463,9 +465,11 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
         }
       }
       if (!dogr) {
-        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0);
+        k_cols_pair<true><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0, need_lo,
+                                                         need_hi);
       } else if (pair) {
-        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0);
+        k_cols_pair<false><<<gc, kC3Threads, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc, reflect, ct0, need_lo,
+                                                          need_hi);
       } else {
         k_cols_all<<<gc, 256, sm_c, st>>>(rx, W, H, Bc, T, vc, ic, dc, pc);
       }
