@@ -181,7 +181,9 @@ class Detector:
 
     def focus_score_host(self, host_images: torch.Tensor, chunk: int = 8, counts: bool = False):
         """End-to-end call with HOST buffers (mhfd_focus_score_host): chunked H2D copies
-        from (pinned) host memory overlapped with compute; returns host float64 scores."""
+        from (pinned) host memory overlapped with compute; returns host float64 scores.
+        The results are views of this detector's pinned buffers, valid after the current
+        stream is synchronised and until the next call (copy them to keep them)."""
         if host_images.dim() == 2:
             host_images = host_images.unsqueeze(0)
         if host_images.device.type != "cpu":
