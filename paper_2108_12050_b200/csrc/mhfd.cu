@@ -381,19 +381,40 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   }
   // ---- a2: stretch on load -> centred f32 image
   float* fimg = reinterpret_cast<float*>(ws + L.fimg);
-  {
-    const int64_t plane = (int64_t)W * H;
+  // single-image bands (pair schedule): only the rows the band's Rx ranges read, by
+  // offsetting the image and the output (B = 1)
+  int nr[2][2] = {{0, H}, {0, 0}};
+  if (band) {
+    const LevelTable& T = *c->tab;
+    const int o_lo = std::max(0, band_lo - 1), o_hi = std::min(H, band_hi + 1);
+    const int lo = o_lo / 8 * 8 - T.rmax, hi = std::min(H, (o_hi + 7) / 8 * 8) + T.rmax;
+    if (hi - lo < H) {
+      nr[0][0] = std::max(0, lo);
+      nr[0][1] = std::min(H, hi);
+      if (lo < 0) { nr[1][0] = H + lo; nr[1][1] = H; }
+      if (hi > H) { nr[1][0] = 0; nr[1][1] = hi - H; }
+      for (int k = 0; k < 2; ++k)   // whole 32-row tiles of the row pass
+        if (nr[k][1] > nr[k][0]) { nr[k][0] = nr[k][0] / 32 * 32; nr[k][1] = std::min(H, (nr[k][1] + 31) / 32 * 32); }
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (nr[k][1] <= nr[k][0]) continue;
+    const int Hk = nr[k][1] - nr[k][0];
+    const Shape sk{W, Hk, pitch, bpp};
+    const uint8_t* ik = img + (int64_t)nr[k][0] * pitch;
+    float* fk = fimg + (int64_t)nr[k][0] * W;
+    const int64_t plane = (int64_t)W * Hk;
     const bool vec = (bpp == 1) ? (W % 16 == 0) : (bpp == 2) ? (W % 8 == 0) : (W % 4 == 0);
     const int64_t work = vec ? plane / (16 / bpp) : plane;
     dim3 gn((unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)c->sms * 8), B);
     if (bpp == 4) {
-      k_normalize_f32<<<gn, 256, 0, st>>>(img, s, par, fimg);
+      k_normalize_f32<<<gn, 256, 0, st>>>(ik, sk, par, fk);
     } else if (vec) {
-      if (bpp == 1) k_normalize_vec<1><<<gn, 256, 0, st>>>(img, s, par, fimg);
-      else k_normalize_vec<2><<<gn, 256, 0, st>>>(img, s, par, fimg);
+      if (bpp == 1) k_normalize_vec<1><<<gn, 256, 0, st>>>(ik, sk, par, fk);
+      else k_normalize_vec<2><<<gn, 256, 0, st>>>(ik, sk, par, fk);
     } else {
-      if (bpp == 1) k_normalize<1><<<gn, 256, 0, st>>>(img, s, par, fimg);
-      else k_normalize<2><<<gn, 256, 0, st>>>(img, s, par, fimg);
+      if (bpp == 1) k_normalize<1><<<gn, 256, 0, st>>>(ik, sk, par, fk);
+      else k_normalize<2><<<gn, 256, 0, st>>>(ik, sk, par, fk);
     }
     LAUNCH_CHECK("k_normalize");
   }
