@@ -235,7 +235,15 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   dim3 gn((nseg + 7) / 8, B);
   const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
   const dim3 gr((((row1 - row0 + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // kNmsRows segments per warp
-  if (rows_fast) {
+  // k_nms_roll<8> is the default count pass (NMS stage 1.695 -> 1.551 ms per 64 tiles
+  // against k_nms_rows; <4> 1.603); MHFD_NMS_ROLL=0/4/8 selects for A/B runs
+  static const int roll = [] { const char* e = getenv("MHFD_NMS_ROLL"); return e ? atoi(e) : 8; }();
+  if (rows_fast && (roll == 8 || roll == 4)) {
+    const int nr = roll;
+    const dim3 g8((((row1 - row0 + nr - 1) / nr) * (W / kSeg) + 7) / 8, B);
+    if (nr == 8) k_nms_roll<8><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
+    else k_nms_roll<4><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
+  } else if (rows_fast) {
     k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1, slab);
   } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
