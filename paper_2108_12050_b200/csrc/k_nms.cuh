@@ -520,4 +520,53 @@ __global__ void __launch_bounds__(256) k_nms_gather(NmsArgs a, int nseg, const i
   }
 }
 
+// The same gather with four segments per warp (eight lanes per segment; a segment parks
+// ~5 records on the C4 tiles, so a warp per segment left most lanes idle): parked
+// records are copied by the segment's eight lanes; each overflowing segment is then
+// re-evaluated by the whole warp as in k_nms_gather.
+__global__ void __launch_bounds__(256) k_nms_gather4(NmsArgs a, int nseg, const int32_t* __restrict__ segcnt,
+                                                     const int32_t* __restrict__ segoff,
+                                                     const mhfd_blob* __restrict__ slab, mhfd_blob* __restrict__ cand,
+                                                     int64_t cap, int row0) {
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int seg_base = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 4;
+  if (seg_base >= nseg) return;
+  const int seg = seg_base + (lane >> 3), j = lane & 7;
+  const bool in = seg < nseg;
+  const int cnt = in ? segcnt[(int64_t)b * nseg + seg] : 0;
+  const int64_t off0 = in ? segoff[(int64_t)b * nseg + seg] : 0;
+  mhfd_blob* out = cand + (int64_t)b * cap;
+  if (cnt <= kSlab) {
+    const mhfd_blob* sl = slab + ((int64_t)b * nseg + seg) * kSlab;
+    for (int r = j; r < cnt; r += 8)
+      if (off0 + r < cap) out[off0 + r] = sl[r];
+  }
+  uint32_t over = __ballot_sync(0xffffffffu, in && j == 0 && cnt > kSlab);
+  const int64_t plane = (int64_t)a.H * a.W;
+  while (over) {
+    const int src = __ffs(over) - 1;
+    over &= over - 1;
+    const int s2 = seg_base + (src >> 3);
+    int64_t off = __shfl_sync(0xffffffffu, off0, src);
+    const int64_t p0 = (int64_t)row0 * a.W + (int64_t)s2 * kSeg;
+    for (int k = 0; k < kSeg; k += 32) {
+      const int64_t p = p0 + k + lane;
+      const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);
+      float val = 0.f;
+      const bool c = paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val);
+      const uint32_t m = __ballot_sync(0xffffffffu, c);
+      if (c) {
+        const int64_t pos = off + __popc(m & ((1u << lane) - 1u));
+        if (pos < cap) {
+          mhfd_blob r;
+          r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
+          out[pos] = r;
+        }
+      }
+      off += __popc(m);
+    }
+  }
+}
+
 }  // namespace mhfd

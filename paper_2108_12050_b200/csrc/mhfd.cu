@@ -254,7 +254,9 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   k_seg_scan<<<B, 1024, 0, st>>>(segcnt, nseg, segoff, ncand);
   LAUNCH_CHECK("k_seg_scan");
   if (rows_fast) {   // parked records to their offsets (overflowing segments re-evaluated)
-    k_nms_gather<<<gn, 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
+    static const bool g1 = getenv("MHFD_NMS_GATHER1") != nullptr;   // A/B knob: one warp per segment
+    if (g1) k_nms_gather<<<gn, 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
+    else k_nms_gather4<<<dim3((nseg + 31) / 32, B), 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
   } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {
