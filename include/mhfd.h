@@ -43,6 +43,23 @@
  *    pitch_bytes >= width * bytes_per_pixel; d_images 16-byte aligned.
  *  - Coordinates in outputs are 0-based; `scale` is the 0-based DoG plane
  *    index s = i^ - 1, i.e. sigma = min_sigma + s * dt.
+ *
+ * Deliberate deviations from the boundary sketched in SURVEY.md §8(b):
+ *  - mhfd_workspace_bytes takes no blob_capacity: the workspace never holds the
+ *    caller's output list, and the internal candidate capacity is the context's
+ *    max_candidates (fixed at mhfd_create), so the size depends on the batch only.
+ *  - mhfd_last_error takes no context: the detail is thread-local (the failing call
+ *    may not have a context, e.g. mhfd_create or mhfd_downsample).
+ *  - A blob list longer than blob_capacity is not an error: the call returns MHFD_OK,
+ *    the counts stay exact and d_flags bit 1 marks the truncated images (bit 0 marks
+ *    candidate-capacity overflow).  An error status would force callers that only want
+ *    the leading blobs of a dense image to treat a complete, correct result as a
+ *    failure; MHFD_ERR_CAPACITY is kept for an invalid capacity argument.
+ *  - Defaults differ from SPEC.md's CPU program on purpose (readings R9, R11):
+ *    non-strict maxima (v == maxpool(v), the paper's primitive) and
+ *    threshold 0.1*dt instead of SPEC.md:254,278's strict dominance and min_response 0.
+ *    strict = 1 with threshold 0 selects SPEC.md's rule; counts then differ from the
+ *    defaults' on plateaus and near-zero responses.
  */
 #ifndef MHFD_H
 #define MHFD_H
@@ -54,7 +71,7 @@
 extern "C" {
 #endif
 
-#define MHFD_ABI_VERSION 3
+#define MHFD_ABI_VERSION 4
 
 typedef struct mhfd_ctx mhfd_ctx; /* opaque, immutable after mhfd_create */
 
@@ -97,6 +114,19 @@ typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
  * -inf padding either way. */
 typedef enum { MHFD_BOUNDARY_PERIODIC = 0, MHFD_BOUNDARY_REFLECT = 1 } mhfd_boundary;
 
+/* Schedule selection (ABI 4): which kernels compute rows a2-a6.  AUTO picks the fastest
+ * applicable one (mhfd_schedule_name reports it); TC / BAND / GENERIC force the tcgen05
+ * schedules, the u8 CUDA-core band kernel or the generic CUDA-core kernels where they
+ * apply (measurement and A/B use; every choice gives results within the parity
+ * tolerances of the oracle).  With AUTO the process-wide environment variable
+ * MHFD_SCHEDULE=tc|band|generic, read once in mhfd_create, is honoured (tools only). */
+typedef enum {
+  MHFD_SCHEDULE_AUTO = 0,
+  MHFD_SCHEDULE_TC = 1,
+  MHFD_SCHEDULE_BAND = 2,
+  MHFD_SCHEDULE_GENERIC = 3
+} mhfd_schedule;
+
 typedef enum {
   MHFD_NMS_PAPER = 0, /* Eq. 3: global argmax over scale, 3x3 local max in space (default) */
   MHFD_NMS_26 = 1     /* conventional 3x3x3 scale-space maxima, 26 neighbours */
@@ -129,6 +159,7 @@ typedef struct {
   int32_t response;       /* mhfd_response (ABI 3; a struct_size without this field
                              reads as MHFD_RESPONSE_DOG)                             */
   int32_t boundary;       /* mhfd_boundary (ABI 3; absent -> MHFD_BOUNDARY_PERIODIC)  */
+  int32_t schedule;       /* mhfd_schedule (ABI 4; absent -> MHFD_SCHEDULE_AUTO)      */
 } mhfd_params;
 
 /* One detected feature (x^_j, y^_j, i^_j) of Eq. 3 and its DoG
@@ -275,14 +306,15 @@ mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
 /* Name of the kernel that computes rows a2-a6 (stretch, blur, DoG, scale argmax)
  * for images of `dtype` in mhfd_detect_batch / mhfd_focus_score on this context:
  * "k_tc" (u8, Eq. 3 NMS, tensor-core banded blur; default when the staged tile
- * fits), "k_band" / "k_band2" (u8, CUDA-core band schedules), "k_scale_space"
+ * fits), "k_band" (u8, CUDA-core band schedule), "k_scale_space"
  * (generic: widths that are not multiples of 256, MHFD_SCHEDULE=generic, and DoG-plane
  * calls below R_max 96), or the two-pass schedule through an HBM row-blur intermediate:
  * "k_rows_pair+k_cols_pair" (Eq. 3 NMS, width % 256 == 0, any radius; also every
  * MHFD_RESPONSE_LOG context, named "k_rows_pair+k_cols_pair<log>"), "k_rows2+k_cols_all"
- * (DoG planes at R_max >= 96: 3x3x3 mode, dumps, MHFD_NO_COLS_PAIR=1).  The environment variable
- * MHFD_SCHEDULE=tc|band|band2|generic, read at mhfd_create, selects among the
- * applicable ones.  Static string; "none" for a NULL context. */
+ * (DoG planes at R_max >= 96: 3x3x3 mode, dumps, MHFD_NO_COLS_PAIR=1).  params.schedule
+ * (or, with MHFD_SCHEDULE_AUTO, the environment variable MHFD_SCHEDULE=tc|band|generic
+ * read at mhfd_create) selects among the applicable ones.  Static string; "none" for a
+ * NULL context. */
 const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype);
 
 /* Floating-point operations per output pixel that the kernel named by

@@ -72,6 +72,8 @@ def _load():
                 "oracle_nms_26": (i64, [P, i32, i32, i32, f64, i32, P, i64]),
                 "oracle_lens_fraction": (f64, [f64, f64, f64]),
                 "oracle_prune": (i64, [P, i64, f64, f64, i32, f64, P]),
+                "oracle_prune_grid": (i64, [P, i64, f64, f64, i32, f64, P]),
+                "oracle_set_prune_grid": (None, [i32]),
                 "oracle_detect": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32,
                                         P, i64, P, P, P, P, P, P]),
                 "oracle_detect_pol": (i64, [P, i32, i32, i32, f64, f64, i32, f64, f64, f64, f64, i32, i32, i32,
@@ -275,22 +277,37 @@ def lens_fraction(d: float, r1: float, r2: float) -> float:
     return float(_load().oracle_lens_fraction(d, r1, r2))
 
 
-def prune(blobs: np.ndarray, min_t: float, max_t: float, n: int, overlap: float) -> np.ndarray:
-    """Greedy overlap pruning in priority (scale desc, raster asc); returns keep flags."""
+def prune(blobs: np.ndarray, min_t: float, max_t: float, n: int, overlap: float,
+          grid: bool = False) -> np.ndarray:
+    """Greedy overlap pruning in priority (scale desc, raster asc); returns keep flags.
+    grid=True runs oracle_prune_grid: the same decisions with an exact distance early-out
+    (pairs farther apart than r1 + r2 have overlap fraction 0), for 10^5-blob lists."""
     blobs = np.ascontiguousarray(blobs, BLOB_DTYPE)
     keep = np.zeros(max(blobs.size, 1), np.uint8)
-    _load().oracle_prune(_ptr(blobs), blobs.size, min_t, max_t, n, overlap, _ptr(keep))
+    fn = _load().oracle_prune_grid if grid else _load().oracle_prune
+    fn(_ptr(blobs), blobs.size, min_t, max_t, n, overlap, _ptr(keep))
     return keep[:blobs.size].astype(bool)
+
+
+def blobs_from_records(rec: np.ndarray) -> np.ndarray:
+    """(k, 4) int32 records {x, y, scale, float32 response bits} (the C ABI's blob layout)
+    -> the oracle's blob array, e.g. to prune the CUDA path's candidate list exactly."""
+    rec = np.ascontiguousarray(rec, np.int32).reshape(-1, 4)
+    out = np.zeros(rec.shape[0], BLOB_DTYPE)
+    out["x"], out["y"], out["scale"] = rec[:, 0], rec[:, 1], rec[:, 2]
+    out["response"] = rec[:, 3].view(np.float32).astype(np.float64)
+    return out
 
 
 def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, overlap: float,
            sat_low: float = 0.00175, sat_high: float = 0.00175, nms: str = "paper",
            strict: bool = False, dump: bool = False, polarity: str = "dark", response: str = "dog",
-           boundary: str = "periodic") -> dict:
+           boundary: str = "periodic", grid_prune: bool = False) -> dict:
     """Algorithm 1 + threshold + pruning; returns blobs, count, candidates.
     polarity "bright" negates the response (not in the paper); response
     "log" replaces Eq. 2 by the scale-normalised Laplacian t_i^2 lap L(t_i) (reading R23);
-    boundary "reflect" mirrors the image at its edges for the blur (reading R25)."""
+    boundary "reflect" mirrors the image at its edges for the blur (reading R25).
+    grid_prune selects oracle_prune_grid (identical decisions, for full-size images)."""
     img, bpp = _img(img)
     H, W = img.shape
     mode = {"paper": 0, "26": 1}[str(nms)]
@@ -303,10 +320,14 @@ def detect(img: np.ndarray, min_t: float, max_t: float, n: int, tau: float, over
     idx = np.empty((H, W), np.int32) if (dump and mode == 0) else None
     pol = {"dark": 0, "bright": 1}[str(polarity)]
     resp = {"dog": 0, "log": 1}[str(response)]
-    with _boundary(boundary):
-        k = _load().oracle_detect_resp(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
-                                       mode, int(strict), pol, resp, _ptr(out), cap, ctypes.byref(ncand),
-                                       _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
+    _load().oracle_set_prune_grid(int(bool(grid_prune)))
+    try:
+        with _boundary(boundary):
+            k = _load().oracle_detect_resp(_ptr(img), bpp, H, W, min_t, max_t, n, tau, overlap, sat_low, sat_high,
+                                           mode, int(strict), pol, resp, _ptr(out), cap, ctypes.byref(ncand),
+                                           _ptr(D), _ptr(v), _ptr(idx), ctypes.byref(lo), ctypes.byref(hi))
+    finally:
+        _load().oracle_set_prune_grid(0)
     if k < 0:
         raise MemoryError("oracle_detect failed")
     res = {"blobs": out[:k].copy(), "count": int(k), "n_candidates": int(ncand.value),

@@ -9,7 +9,6 @@ without a CUDA device the context cannot be created and the calls raise.
 from __future__ import annotations
 
 import ctypes
-import os
 
 import torch
 
@@ -44,9 +43,9 @@ class Detector:
                  strict: bool = False, device: int | None = None, max_candidates: int = 0,
                  schedule: str | None = None, polarity: str = "dark", response: str = "dog",
                  boundary: str = "periodic"):
-        """schedule: None (library default: k_tc for u8 where the tile fits) or one of
-        "tc", "band", "band2", "generic" — forwarded as MHFD_SCHEDULE, which the library
-        reads once in mhfd_create.  polarity: "dark" (Eq. 2 as written, the paper's EM
+        """schedule: None / "auto" (library default: the tcgen05 schedules where they
+        apply) or one of "tc", "band", "generic" — the params.schedule field of
+        mhfd_create (no process-wide state is touched).  polarity: "dark" (Eq. 2 as written, the paper's EM
         sections) or "bright" (negated DoG: bright blobs on a dark background).  response:
         "dog" (Eq. 2, the paper's detector) or "log" (the scale-normalised Laplacian
         t_i^2 lap L(t_i) that Eq. 2 approximates; reading R23).  boundary:
@@ -65,20 +64,11 @@ class Detector:
                               response={"dog": _abi.MHFD_RESPONSE_DOG, "log": _abi.MHFD_RESPONSE_LOG}[str(response)],
                               boundary={"periodic": _abi.MHFD_BOUNDARY_PERIODIC,
                                         "reflect": _abi.MHFD_BOUNDARY_REFLECT}[str(boundary)])
-        h = ctypes.c_void_p()
-        if schedule is not None and schedule not in ("tc", "band", "band2", "generic"):
+        if schedule not in _abi.MHFD_SCHEDULE:
             raise ValueError(f"unknown schedule {schedule!r}")
-        saved = os.environ.get("MHFD_SCHEDULE")
-        try:
-            if schedule is not None:
-                os.environ["MHFD_SCHEDULE"] = schedule
-            _abi.check(lib.mhfd_create(ctypes.byref(self.params), ctypes.byref(h)))
-        finally:
-            if schedule is not None:
-                if saved is None:
-                    os.environ.pop("MHFD_SCHEDULE", None)
-                else:
-                    os.environ["MHFD_SCHEDULE"] = saved
+        self.params.schedule = _abi.MHFD_SCHEDULE[schedule]
+        h = ctypes.c_void_p()
+        _abi.check(lib.mhfd_create(ctypes.byref(self.params), ctypes.byref(h)))
         self._h = h
         self._lib = lib
         got = mhfd_params()

@@ -19,6 +19,7 @@ MHFD_DARK, MHFD_BRIGHT = 0, 1
 MHFD_RESPONSE_DOG, MHFD_RESPONSE_LOG = 0, 1
 MHFD_BOUNDARY_PERIODIC, MHFD_BOUNDARY_REFLECT = 0, 1
 MHFD_NMS_PAPER, MHFD_NMS_26 = 0, 1
+MHFD_SCHEDULE = {None: 0, "auto": 0, "tc": 1, "band": 2, "generic": 3}
 
 # every symbol include/mhfd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["mhfd_params_default", "mhfd_create", "mhfd_workspace_bytes", "mhfd_detect_batch",
@@ -35,7 +36,8 @@ class mhfd_params(ctypes.Structure):
                 ("threshold", ctypes.c_float), ("overlap", ctypes.c_float), ("sat_low", ctypes.c_float),
                 ("sat_high", ctypes.c_float), ("nms", ctypes.c_int32), ("strict", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("max_candidates", ctypes.c_int32), ("polarity", ctypes.c_int32),
-                ("response", ctypes.c_int32), ("boundary", ctypes.c_int32)]
+                ("response", ctypes.c_int32), ("boundary", ctypes.c_int32),
+                ("schedule", ctypes.c_int32)]
 
 
 class mhfd_blob(ctypes.Structure):

@@ -44,7 +44,11 @@ __device__ __forceinline__ bool paper_cand(const float* __restrict__ v, int W, i
       if (dy == 0 && dx == 0) continue;
       const int xx = x + dx;
       if (xx < 0 || xx >= W) continue;
-      if (!dominates(c, __ldg(v + (int64_t)yy * W + xx), strict)) return false;
+      // a NaN neighbour is skipped, as the count passes' fmaxf column-max chain skips it,
+      // so the count and the write/re-evaluation predicates agree for every input (v is
+      // NaN-free anyway: the stretch clamps, and a NaN centre fails c > tau in both)
+      const float q = __ldg(v + (int64_t)yy * W + xx);
+      if (q == q && !dominates(c, q, strict)) return false;
     }
   }
   return true;

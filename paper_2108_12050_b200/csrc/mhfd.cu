@@ -28,7 +28,6 @@
 #include "k_prune.cuh"
 #include "k_scale_space.cuh"
 #include "k_band.cuh"
-#include "k_band2.cuh"
 #include "k_tc.cuh"
 #include "k_twopass.cuh"
 #include "k_downsample.cuh"
@@ -48,7 +47,7 @@ struct mhfd_ctx {
   int prune_grid;    // cooperative grid size for k_prune
   int sms;
   int band_enabled;  // MHFD_NO_BAND=1 in the environment forces the generic schedule
-  int band_kind;     // 3 = k_tc (default), 1 = k_band, 2 = k_band2; MHFD_SCHEDULE=tc|band|band2|generic
+  int band_kind;     // 3 = k_tc (default), 1 = k_band (params.schedule, else MHFD_SCHEDULE=tc|band|generic)
   int twopass;       // generic path for large radii: k_rows2 / k_cols_all (MHFD_NO_TWOPASS=1 disables)
   TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
   uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
@@ -359,18 +358,6 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   }
   if (band && !(c->p.response == MHFD_RESPONSE_DOG && paper && dog_dump == nullptr && pair_fit(c)))
     return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc or the two-pass pair schedule (Eq. 3 NMS)");
-  // ---- a2-a6 on u8 images, two-CTA band schedule
-  if (fused_ok && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled && c->band_kind == 2 &&
-      band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
-    const size_t smem = band2_smem(c->tab->rmax, c->tab->ntaps_total);
-    cudaError_t ea = cudaFuncSetAttribute(k_band2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (ea != cudaSuccess) return cuda_fail(ea, "k_band2 attribute");
-    dim3 gb((W + kStripW - 1) / kStripW, (H + kBand2BH - 1) / kBand2BH, B);
-    k_band2<<<gb, kBand2Threads, smem, st>>>(img, s, par, *c->tab, v, idx);
-    LAUNCH_CHECK("k_band2");
-    MARK(2);
-    return run_nms(c, W, H, B, ws, L, v, idx, nullptr, st, launches, ev);
-  }
   // ---- a2-a6 on u8 images: band schedule (raw band staged once per CTA, no f32 prepass)
   if (fused_ok && bpp == 1 && paper && dog_dump == nullptr && c->band_enabled &&
       band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) {
@@ -666,6 +653,7 @@ void mhfd_params_default(mhfd_params* p) {
   p->device = 0;
   p->max_candidates = 0;
   p->polarity = MHFD_DARK;
+  p->schedule = MHFD_SCHEDULE_AUTO;
 }
 
 mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
@@ -707,6 +695,8 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   if (p->nms != MHFD_NMS_PAPER && p->nms != MHFD_NMS_26) return fail(MHFD_ERR_INVALID_ARGUMENT, "nms %d", p->nms);
   if (p->strict != 0 && p->strict != 1) return fail(MHFD_ERR_INVALID_ARGUMENT, "strict %d", p->strict);
   if (p->max_candidates < 0) return fail(MHFD_ERR_INVALID_ARGUMENT, "max_candidates < 0");
+  if (p->schedule < MHFD_SCHEDULE_AUTO || p->schedule > MHFD_SCHEDULE_GENERIC)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "schedule %d", p->schedule);
   const int n = p->num_scales;
   // scale grid in f64
   double t[kMaxLevels];
@@ -746,13 +736,19 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   c->dt = dt;
   c->sms = prop.multiProcessorCount;
   {
+    // schedule: the params field (ABI 4) wins; MHFD_SCHEDULE / MHFD_NO_BAND remain
+    // process-wide overrides for the measurement tools when the field is 0 (auto)
     const char* nb = getenv("MHFD_NO_BAND");
     c->band_enabled = !(nb && nb[0] == '1');
     const char* sch = getenv("MHFD_SCHEDULE");
-    c->band_kind = 3;
-    if (sch && strcmp(sch, "band2") == 0) c->band_kind = 2;
-    if (sch && strcmp(sch, "band") == 0) c->band_kind = 1;
-    if (sch && strcmp(sch, "generic") == 0) c->band_enabled = 0;
+    int choice = p->schedule;
+    if (choice == MHFD_SCHEDULE_AUTO && sch) {
+      if (strcmp(sch, "tc") == 0) choice = MHFD_SCHEDULE_TC;
+      if (strcmp(sch, "band") == 0) choice = MHFD_SCHEDULE_BAND;
+      if (strcmp(sch, "generic") == 0) choice = MHFD_SCHEDULE_GENERIC;
+    }
+    c->band_kind = choice == MHFD_SCHEDULE_BAND ? 1 : 3;
+    if (choice == MHFD_SCHEDULE_GENERIC) c->band_enabled = 0;
   }
   LevelTable& T = *c->tab;
   T.nlev = n + 1;
@@ -840,16 +836,15 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     tc_fill_tables(*c->tc, wv, tabh.data());
     int prev = 0;
     cudaGetDevice(&prev);
-    if (cudaSetDevice(p->device) == cudaSuccess &&
-        cudaMalloc(&c->d_tctab, tabh.size()) == cudaSuccess &&
-        cudaMemcpy(c->d_tctab, tabh.data(), tabh.size(), cudaMemcpyHostToDevice) == cudaSuccess) {
-    } else {
-      if (c->d_tctab) cudaFree(c->d_tctab);
-  if (c->d_thr) cudaFree(c->d_thr);
-      c->d_tctab = nullptr;
-      cudaGetLastError();
-    }
+    const bool ok = cudaSetDevice(p->device) == cudaSuccess &&
+                    cudaMalloc(&c->d_tctab, tabh.size()) == cudaSuccess &&
+                    cudaMemcpy(c->d_tctab, tabh.data(), tabh.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     cudaSetDevice(prev);
+    if (!ok) {   // fail loudly: no silent fallback to a slower schedule
+      cudaGetLastError();
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_CUDA, "Toeplitz table upload for k_tc failed");
+    }
   }
   c->radmax = 0.0;
   for (int s = 0; s < n; ++s) {
@@ -1061,10 +1056,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (c->p.response == MHFD_RESPONSE_LOG) return "k_rows_pair+k_cols_pair<log>";
   if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
-  if (dtype == MHFD_U8 && paper && c->band_enabled) {
-    if (c->band_kind == 2 && band2_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band2";
-    if (band_ok(W, H, c->tab->rmax, c->tab->ntaps_total)) return "k_band";
-  }
+  if (dtype == MHFD_U8 && paper && c->band_enabled && band_ok(W, H, c->tab->rmax, c->tab->ntaps_total))
+    return "k_band";
   if (pair_ok(c)) return "k_rows_pair+k_cols_pair";
   if (c->twopass && W % kR2Cols == 0) return "k_rows2+k_cols_all";
   return "k_scale_space";
@@ -1112,9 +1105,9 @@ mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, in
   s = run_front(c, d_image, dtype, 1, pitch_bytes, ws, L, nullptr, st, launches, nullptr, y0, y1);
   if (s != MHFD_OK) return s;
   const int32_t* nc = reinterpret_cast<const int32_t*>(ws + L.ncand);
-  if (cand_capacity > 0) {
-    k_copy_cands<<<c->sms * 4, 256, 0, st>>>(reinterpret_cast<const mhfd_blob*>(ws + L.cand), nc, cand_capacity,
-                                              d_cands);
+  if (cand_capacity > 0) {   // the workspace list holds at most c->cap records
+    k_copy_cands<<<c->sms * 4, 256, 0, st>>>(reinterpret_cast<const mhfd_blob*>(ws + L.cand), nc,
+                                              std::min<int64_t>(cand_capacity, c->cap), d_cands);
     ++launches;
   }
   cudaError_t e = cudaMemcpyAsync(d_ncand, nc, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);

@@ -46,33 +46,46 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def gather_candidates(cands: torch.Tensor, n: int | torch.Tensor) -> tuple[torch.Tensor, int]:
-    """All-gather every rank's first `n` candidate records (rows of `cands`) in rank
-    order -> (concatenated records, total).  Two collectives: the counts, then the
-    records padded to the largest count."""
+    """All-gather every rank's candidate records (rows of `cands`) in rank order ->
+    (concatenated records, exact total).  Two collectives: the counts, then the records
+    padded to the largest stored count.  A rank stores at most cands.shape[0] records
+    (mhfd_detect_band truncates its list but reports the exact count), so every rank
+    clamps the per-rank record count the same way before the second collective: the
+    concatenation is then the first records of the whole image's raster list, and the
+    returned total stays exact (callers compare it with the pruning capacity)."""
     world = dist.get_world_size()
     dev = cands.device
     n_t = (n.reshape(1) if isinstance(n, torch.Tensor) else torch.tensor([int(n)])).to(dev, torch.int64)
     counts = torch.empty(world, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(counts, n_t)
     counts_h = [int(c) for c in counts.cpu().tolist()]
-    m = max(max(counts_h), 1)
+    stored = [min(c, cands.shape[0]) for c in counts_h]   # identical on every rank
+    m = max(max(stored), 1)
     rec = cands.shape[1]
     local = torch.zeros((m, rec), dtype=cands.dtype, device=dev)
-    k = counts_h[dist.get_rank()]
+    k = stored[dist.get_rank()]
     local[:k] = cands[:k]
     allc = torch.empty((world * m, rec), dtype=cands.dtype, device=dev)
     dist.all_gather_into_tensor(allc, local)
-    parts = [allc[r * m: r * m + counts_h[r]] for r in range(world)]
+    parts = [allc[r * m: r * m + stored[r]] for r in range(world)]
     return torch.cat(parts, 0), sum(counts_h)
 
 
 def focus_score_single_image(det, image: torch.Tensor, src: int = 0):
     """Score ONE image on all ranks (each rank a row band; NCCL broadcast + all-gathers).
-    `image` is the (H, W) u8 tile on this rank's device (its content matters on `src`
+    `image` is the (H, W) tile on this rank's device (its content matters on `src`
     only).  Returns (blobs, count, score, flags) of mhfd_prune_candidates, identical on
-    every rank and bit-identical to det.detect / det.focus_score on the whole image."""
+    every rank and bit-identical to det.detect / det.focus_score on the whole image,
+    including candidate overflow: when the image has more than det.max_candidates
+    candidates, the first max_candidates in raster order are pruned and flags bit 0 is
+    set, as mhfd_detect_batch does."""
     dist.broadcast(image, src)
     y0, y1 = band_rows(det.height, dist.get_world_size(), dist.get_rank())
     cands, n = det.detect_band(image, y0, y1)
     allc, total = gather_candidates(cands, n)
-    return det.prune_candidates(allc, total)
+    cap = det.max_candidates
+    over = total > cap
+    blobs, cnt, score, flags = det.prune_candidates(allc[:cap] if over else allc, min(total, cap))
+    if over:
+        flags |= 1
+    return blobs, cnt, score, flags

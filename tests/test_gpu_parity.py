@@ -133,12 +133,12 @@ def test_c2_pair_parity(defocus, bits):
     _full_parity(img, C3)
 
 
-@pytest.mark.parametrize("schedule", ["band", "band2", "generic"])
+@pytest.mark.parametrize("schedule", ["band", "generic"])
 def test_c2_cuda_core_schedules(schedule):
     """The CUDA-core schedules (selectable fallbacks of k_tc) against the oracle."""
     img = synth.em_tile_np(1024, 1024, 1000, defocus=0.0, dose=300.0, bits=8)
     det = mhfd.Detector(1024, 1024, threshold=0.09, schedule=schedule, **C3)
-    assert det.schedule("u8") == {"band": "k_band", "band2": "k_band2", "generic": "k_scale_space"}[schedule]
+    assert det.schedule("u8") == {"band": "k_band", "generic": "k_scale_space"}[schedule]
     _full_parity(img, C3, schedule=schedule)
 
 

@@ -353,6 +353,37 @@ def test_prune_greedy_characterisation():
     assert oracle.prune(b, 1.0, 10.0, 10, 1.0).all()
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_prune_grid_equals_bruteforce(seed):
+    """oracle_prune_grid (exact distance early-out, cells >= 2 r_max) keeps exactly the
+    blobs the O(n^2) oracle_prune keeps: clustered lists with negative-offset coordinates
+    (cells anchored at the minimum), every overlap value, and the chain case."""
+    rng = np.random.default_rng(100 + seed)
+    centres = rng.integers(-40, 400, size=(30, 2))
+    rows = set()
+    for cx, cy in centres:   # dense clusters: many overlapping pairs, long suppression chains
+        for _ in range(60):
+            rows.add((int(cx + rng.normal(0, 9)), int(cy + rng.normal(0, 9)), int(rng.integers(0, 10))))
+    rows = sorted(rows)
+    b = _blobs(rows)
+    for o in (0.0, 0.1, 0.5, 0.9, 1.0):
+        brute = oracle.prune(b, 1.0, 10.0, 10, o)
+        grid = oracle.prune(b, 1.0, 10.0, 10, o, grid=True)
+        assert np.array_equal(brute, grid), o
+        if o < 1.0:
+            assert 0 < brute.sum() < len(rows)
+    A, B, C = (0, 0, 9), (11, 0, 6), (19, 0, 3)
+    assert oracle.prune(_blobs([C, A, B]), 1.0, 10.0, 10, 0.5, grid=True).tolist() == [True, True, False]
+    assert oracle.prune(_blobs([]), 1.0, 10.0, 10, 0.5, grid=True).size == 0
+
+
+def test_detect_grid_prune_equals_default():
+    img = synth.em_tile_np(128, 160, 1010, dose=300.0)
+    a = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.3)
+    g = oracle.detect(img, 1.0, 5.0, 5, 0.08, 0.3, grid_prune=True)
+    assert a["count"] == g["count"] > 0 and np.array_equal(a["blobs"], g["blobs"])
+
+
 # ---------------------------------------------------------------- end to end
 def test_detect_constant_is_zero():
     r = oracle.detect(synth.constant_image(64, 64, 200), 1.0, 5.0, 5, 0.0, 0.5)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Mutation check of the oracle pins: each plausible mistake below is applied to a
 # scratch copy of oracle/mhfd_oracle.c and the -m "not gpu" pin suite must fail.
-# Usage: tools/oracle_mutations.sh   (CPU only; ~1 min)
+# Usage: tools/oracle_mutations.sh   (CPU only; a few minutes)
 set -u
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 TMP=$(mktemp -d)
@@ -15,6 +15,8 @@ muts=(
  's/double rb = sqrt(2.0) \* t\[b->scale\];/double rb = sqrt(2.0) * t[b->scale + 1];/'                   # off-by-one radius
  's/if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue; \/\* -inf padding \*\//yy = (yy + H) % H; xx = (xx + W) % W;/'  # periodic NMS
  's/if (!(c > tau)) continue;/if (!(c >= tau)) continue;/'                                              # non-strict threshold
+ 's/const int64_t cell = (int64_t)ceil(2.0 \* rmax) + 1;/const int64_t cell = (int64_t)ceil(rmax);/'     # grid prune: cells < 2 r_max
+ 's/for (int64_t xx = cx - 1; xx <= cx + 1 \&\& ok; ++xx)/for (int64_t xx = cx; xx <= cx + 1 \&\& ok; ++xx)/'  # grid prune: missed cells
 )
 fail=0
 for m in "${muts[@]}"; do
