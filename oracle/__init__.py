@@ -263,6 +263,21 @@ def nms_paper(D: np.ndarray, tau: float, strict: bool = False) -> np.ndarray:
     return out[:c].copy()
 
 
+def nms_paper_v(v: np.ndarray, idx: np.ndarray, tau: float, strict: bool = False) -> np.ndarray:
+    """Eq. 3's outer step on a given inner argmax (v, i^): the
+    maxpool(3,3) comparison with -inf padding and the threshold."""
+    v = np.ascontiguousarray(v, np.float64)
+    idx = np.ascontiguousarray(idx, np.int32)
+    H, W = v.shape
+    cap = max(16, H * W // 2)
+    while True:
+        out = np.empty(cap, BLOB_DTYPE)
+        c = _load().oracle_nms_paper_v(_ptr(v), _ptr(idx), H, W, tau, int(strict), _ptr(out), out.size)
+        if c <= cap:
+            return out[:c].copy()
+        cap = int(c)
+
+
 def nms_26(D: np.ndarray, tau: float, strict: bool = False) -> np.ndarray:
     """Conventional 3x3x3 scale-space maxima."""
     D = np.ascontiguousarray(D, np.float64)

@@ -47,19 +47,23 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
 
 def gather_candidates(cands: torch.Tensor, n: int | torch.Tensor) -> tuple[torch.Tensor, int]:
     """All-gather every rank's candidate records (rows of `cands`) in rank order ->
-    (concatenated records, exact total).  Two collectives: the counts, then the records
-    padded to the largest stored count.  A rank stores at most cands.shape[0] records
-    (mhfd_detect_band truncates its list but reports the exact count), so every rank
-    clamps the per-rank record count the same way before the second collective: the
+    (concatenated records, exact total).  Two collectives: every rank's (count, capacity),
+    then the records padded to the largest stored count.  A rank stores at most
+    cands.shape[0] records (mhfd_detect_band truncates its list but reports the exact
+    count), so every rank clamps each rank's record count the same way from the gathered
+    (count, capacity) pairs before the second collective (no rank waits on a shape only
+    it knows): the
     concatenation is then the first records of the whole image's raster list, and the
     returned total stays exact (callers compare it with the pruning capacity)."""
     world = dist.get_world_size()
     dev = cands.device
     n_t = (n.reshape(1) if isinstance(n, torch.Tensor) else torch.tensor([int(n)])).to(dev, torch.int64)
-    counts = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(counts, n_t)
-    counts_h = [int(c) for c in counts.cpu().tolist()]
-    stored = [min(c, cands.shape[0]) for c in counts_h]   # identical on every rank
+    mine = torch.cat([n_t.reshape(1), torch.tensor([cands.shape[0]], dtype=torch.int64, device=dev)])
+    meta = torch.empty(2 * world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(meta, mine)   # (count, stored capacity) of every rank
+    meta_h = [int(c) for c in meta.cpu().tolist()]
+    counts_h = meta_h[0::2]
+    stored = [min(c, cap) for c, cap in zip(counts_h, meta_h[1::2])]   # identical on every rank
     m = max(max(stored), 1)
     rec = cands.shape[1]
     local = torch.zeros((m, rec), dtype=cands.dtype, device=dev)

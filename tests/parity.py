@@ -100,22 +100,46 @@ def compare_candidates(gpu, ora, amb_xy: set, tie_xy: set, eps: float, mode: str
 
 
 def compare_pruned(gpu, ora, amb_pts, rad_max: float, rad, mode: str):
-    """Kept sets equal outside A' = blobs within interaction range of an ambiguous
-    candidate (r_p + 2 r_max covers every direct interaction)."""
+    """Kept sets equal outside A' = A + {blobs within r_p + r_max of a member of A}
+    (SURVEY.md §8(c) parity rule 4: an ambiguous candidate can only change the greedy
+    decision of a blob it overlaps, i.e. one closer than r_p + r_a <= r_p + r_max).
+    Nearest-member distances come from a k-d tree (full-size images have ~10^5 blobs)."""
     if not amb_pts:
         assert blob_set(gpu) == blob_set(ora), "pruned sets differ with no ambiguous candidate"
         return {"excluded": 0}
-    pts = np.array([(p[0], p[1]) for p in amb_pts], np.float64)
+    from scipy.spatial import cKDTree
+    tree = cKDTree(np.array([(p[0], p[1]) for p in amb_pts], np.float64))
+    rad = np.asarray(rad, np.float64)
 
-    def near(r):
-        d = np.hypot(pts[:, 0] - r[0], pts[:, 1] - r[1])
-        return bool((d <= rad[r[2]] + 2 * rad_max).any())
-    gk = {(r[0], r[1], r[2]) for r in gpu if not near(r)}
-    ok = {(r[0], r[1], r[2]) for r in ora if not near(r)}
+    def outside(rows):
+        if not rows:
+            return set()
+        a = np.array([(r[0], r[1], r[2]) for r in rows], np.int64)
+        d, _ = tree.query(a[:, :2].astype(np.float64), k=1)
+        far = d > rad[a[:, 2]] + rad_max
+        return {(int(x), int(y), int(s)) for (x, y, s) in a[far]}
+    gk, ok = outside(gpu), outside(ora)
     diff = gk ^ ok
     assert not diff, f"{len(diff)} pruned-set mismatches outside A', e.g. {sorted(diff)[:5]}"
     excluded = len(gpu) + len(ora) - len(gk) - len(ok)
     return {"excluded": excluded}
+
+
+def assert_prune_exact(gpu_cands, gpu_kept, cfg, overlap: float):
+    """The pruning step in isolation, exactly: the oracle's greedy rule (f64 geometry on
+    integer coordinates, grid early-out with identical decisions) applied to the CUDA
+    path's own candidate list keeps exactly the blobs the CUDA path kept."""
+    import oracle
+    if not gpu_cands:
+        assert not gpu_kept
+        return 0
+    rec = np.array([(r[0], r[1], r[2], 0) for r in gpu_cands], np.int32)
+    keep = oracle.prune(oracle.blobs_from_records(rec), cfg["min_sigma"], cfg["max_sigma"], cfg["num_scales"],
+                        overlap, grid=True)
+    ref = {(int(x), int(y), int(s)) for (x, y, s, _), k in zip(rec, keep) if k}
+    got = blob_set(gpu_kept)
+    assert got == ref, f"pruning differs on the GPU's own candidates: {len(got ^ ref)} blobs"
+    return len(ref)
 
 
 def assert_score(s_gpu: float, s_oracle: float):

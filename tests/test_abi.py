@@ -29,7 +29,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert not missing, missing
     for s in declared:
         assert hasattr(lib, s)
-    assert lib.mhfd_abi_version() == 3
+    assert lib.mhfd_abi_version() == 4
 
 
 def test_library_is_sm100a_only():
@@ -70,7 +70,7 @@ def test_abi1_struct_size_reads_polarity_as_dark():
     ("min_sigma", 0.0, 1), ("max_sigma", 0.5, 1), ("num_scales", 0, 1), ("num_scales", 63, 1),
     ("threshold", -1.0, 1), ("threshold", float("nan"), 1), ("overlap", 1.5, 1), ("sat_low", 0.6, 1),
     ("nms", 7, 1), ("strict", 2, 1), ("max_sigma", 40.0, 1), ("width", 50, 2), ("height", 70000, 2),
-    ("polarity", 2, 1), ("struct_size", 8, 1), ("response", 2, 1),
+    ("polarity", 2, 1), ("struct_size", 8, 1), ("response", 2, 1), ("schedule", 9, 1), ("schedule", -1, 1),
 ])
 def test_create_validates_before_device(field, value, status):
     lib = _abi.load()
@@ -167,3 +167,18 @@ def test_boundary_validates_before_device(W, b, status):
     h = ctypes.c_void_p()
     assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == status
     assert "boundary" in lib.mhfd_last_error().decode()
+
+
+def test_abi3_struct_size_reads_schedule_as_auto():
+    # an ABI-3 caller's struct ends before `schedule` (ABI 4): a garbage value there is not read
+    lib = _abi.load()
+    p = _abi.mhfd_params()
+    lib.mhfd_params_default(ctypes.byref(p))
+    assert p.schedule == 0
+    p.width, p.height, p.max_sigma = 256, 256, 5.0
+    p.struct_size = _abi.mhfd_params.schedule.offset
+    p.schedule = 9
+    p.min_sigma = 0.0
+    h = ctypes.c_void_p()
+    assert lib.mhfd_create(ctypes.byref(p), ctypes.byref(h)) == 1
+    assert "min_sigma" in lib.mhfd_last_error().decode()

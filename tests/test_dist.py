@@ -123,3 +123,42 @@ def test_band_sharding_world2_reassembles_raster_list():
     np.testing.assert_array_equal(got[:, 2], allc["scale"])
     keep = oracle.prune(allc, 1.0, 5.0, 5, 0.5)
     assert int(keep.sum()) == ref["count"]
+
+
+def _overflow_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2108_12050_b200.dist import gather_candidates
+    # rank 0 found 7 candidates but stored only 5 (its band list overflowed), rank 1
+    # found 3 and stores them in a larger buffer: no hang, exact total, the records are
+    # the first ones of the raster list
+    n = 7 if rank == 0 else 3
+    cap = 5 if rank == 0 else 9
+    rec = torch.full((cap, 4), -1, dtype=torch.int32)
+    for k in range(min(n, cap)):
+        rec[k] = torch.tensor([k, 10 * rank, 0, 0], dtype=torch.int32)
+    got, total = gather_candidates(rec, n)
+    q.put((rank, got.numpy(), total))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_candidates_overflow_world2():
+    """a band list truncated to its capacity must not desynchronise the
+    all-gathers (each rank learns every rank's stored count), and the total stays exact."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overflow_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, got, total in res:
+        assert total == 10
+        assert got.shape == (8, 4)
+        assert got[:5, 0].tolist() == [0, 1, 2, 3, 4] and (got[:5, 1] == 0).all()
+        assert got[5:, 0].tolist() == [0, 1, 2] and (got[5:, 1] == 10).all()
