@@ -19,11 +19,12 @@ Per-stage device times come from events the library records on the same stream
 the roofline (k_tc, the tcgen05 kernel, by default).  `e2e` repeats the measurement through mhfd_focus_score_host with the
 batch in pinned host memory (H2D copies and the D2H of scores inside the timed
 region).  `cpu_baseline` times the oracle (oracle/, f64, plain C) on rank 0 on a
-bounded sample (a band of rows of one tile).
+bounded sample (the tile's percentiles + a 512-row band, extrapolated to the tile) on
+all host cores and on 1 thread.
 
 `--impl reference`: the oracle IS the reference arm for this tier (there is no
 reference implementation to install): rank 0 times it on the host
-cores, each step a band of the same workload; other ranks exit 0.
+cores, each step the same sample as cpu_baseline; other ranks exit 0.
 """
 from __future__ import annotations
 
@@ -48,10 +49,11 @@ SIGMA = (1.0, 10.0)
 NSCALES = 10
 TAU = 0.1 * (SIGMA[1] - SIGMA[0]) / NSCALES
 OVERLAP = 0.5
-# Derived ALU peak (B200_PROFILING.md unit counts): 148 SMs x 128 FP32 FMA/clk x 2 FLOP
-# x 1.965 GHz (clocks.max.sm).  The FFMA microbenchmark measured 36.1 TFMA/s = 72.2
-# TFLOP/s sustained (profiles/r01_ubench_ffma.json).
-ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# FP32 peak (SURVEY.md §8(d) "P_fp32"): nominal 148 SMs x 128 FFMA/clk x 1.965 GHz
+# (clocks.max.sm) = 37.2 T FFMA/s; the FFMA microbenchmark measured 36.1 T FFMA/s
+# (profiles/r01_ubench_ffma.json), reported beside it.
+FP32_PEAK_TFFMA = 148 * 128 * 1.965e9 / 1e12
+FP32_UBENCH_TFFMA = 36.1
 
 
 def log(*a):
@@ -63,11 +65,22 @@ def radii():
     return [math.ceil(5.0 * (SIGMA[0] + i * dt)) for i in range(NSCALES + 1)]
 
 
-def alg_flops_per_px():
-    """Algorithmic FLOPs of the fused kernel per pixel: the direct
-    separable blur at the parity radius R_i = ceil(5 t_i) — 2 passes x (2R_i+1) FMA
-    x 2 FLOP per level — plus DoG (2 FLOP) and the running max (1) per plane."""
-    return sum(2 * (2 * R + 1) * 2 for R in radii()) + 3 * NSCALES
+def cascade_ffma_per_px(smin: float = SIGMA[0], smax: float = SIGMA[1], n: int = NSCALES) -> int:
+    """SURVEY.md §8(d) F_alg: FFMA per pixel of the cheapest exact separable schedule at
+    the parity radius k = 5 — level 1 direct (2 passes x (2R_1+1)), then each next level
+    as the cascade increment sigma_inc = sqrt(t_{i+1}^2 - t_i^2) (2 x (2R_inc+1)).
+    674 at C3 (sigma 1-10, n 10), 2,662 at C5 (sigma 1-30, n 20)."""
+    dt = (smax - smin) / n
+    t = [smin + i * dt for i in range(n + 1)]
+    f = 2 * (2 * math.ceil(5.0 * t[0]) + 1)
+    for i in range(1, n + 1):
+        f += 2 * (2 * math.ceil(5.0 * math.sqrt(t[i] ** 2 - t[i - 1] ** 2)) + 1)
+    return f
+
+
+def direct_ffma_per_px(smin: float = SIGMA[0], smax: float = SIGMA[1], n: int = NSCALES) -> int:
+    dt = (smax - smin) / n
+    return sum(2 * (2 * math.ceil(5.0 * (smin + i * dt)) + 1) for i in range(n + 1))
 
 
 class ClockSampler:
@@ -131,33 +144,68 @@ def make_batch(rank: int, B: int, device) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ oracle timing
-def oracle_band(img: np.ndarray, rows: int) -> tuple[float, dict]:
-    """The oracle as it stands on a band of `rows` rows of one tile: percentiles and
-    stretch of the tile, Eq. 2 DoG of the band, Eq. 3 NMS, pruning.  Returns seconds."""
+ORACLE_ROWS = 512   # band of one tile per oracle sample (both the cpu_baseline and the reference arm)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(img: np.ndarray, rows: int = ORACLE_ROWS) -> dict:
+    """The oracle as it stands on a bounded sample of one 4096^2 tile: percentiles and
+    stretch of the whole tile (t_tile), then Eq. 2 DoG / Eq. 3 NMS / pruning of a band
+    of `rows` rows (t_band).  The rate extrapolates to the whole tile,
+    T = t_tile + t_band * SIZE / rows, value = SIZE^2 / T (MPix/s): the tile-wide
+    percentile sort is charged once per tile, not once per band (the round-1 reference
+    arm charged it per band and understated the oracle ~4x)."""
     import oracle
     t0 = time.perf_counter()
     lo, hi = oracle.percentiles(img)
     f = oracle.stretch(img, lo, hi)
+    t1 = time.perf_counter()
     y0 = (SIZE - rows) // 2
     D = oracle.dog_stack(f, SIGMA[0], SIGMA[1], NSCALES, rows=(y0, y0 + rows))
     cand = oracle.nms_paper(D, TAU)
     keep = oracle.prune(cand, SIGMA[0], SIGMA[1], NSCALES, OVERLAP)
-    dt = time.perf_counter() - t0
-    return dt, {"candidates": int(len(cand)), "kept": int(keep.sum())}
+    t2 = time.perf_counter()
+    T = (t1 - t0) + (t2 - t1) * SIZE / rows
+    return {"value": SIZE * SIZE / T / 1e6, "t_tile_s": t1 - t0, "t_band_s": t2 - t1, "rows": rows,
+            "tile_s_extrapolated": T, "candidates": int(len(cand)), "kept": int(keep.sum())}
 
 
-def cpu_baseline(img: np.ndarray, rows: int = 2048) -> dict:
+def _sample_text(r: dict, threads: int) -> str:
+    return (f"tile 0 (4096^2 u8): percentiles+stretch of the tile ({r['t_tile_s']:.2f} s) + DoG/NMS/pruning "
+            f"of a {r['rows']}-row band ({r['t_band_s']:.2f} s), f64, {threads} thread(s); extrapolated to the "
+            f"tile: {r['tile_s_extrapolated']:.1f} s per 16.8 MPix")
+
+
+def cpu_baseline(img: np.ndarray) -> dict:
+    """the oracle on all host cores and on 1 thread, with the CPU model."""
     import oracle
-    oracle.set_threads(os.cpu_count() or 1)
-    dt, info = oracle_band(img, rows)
-    px = rows * SIZE
-    return {"value": px / dt / 1e6, "unit": "MPix/s", "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"{rows} rows x {SIZE} cols (= {px / 1e6:.2f} MPix) of tile 0 (4096^2 u8): percentiles+stretch "
-                      f"of the tile, DoG/NMS/pruning of the band, f64, {dt:.1f} s",
-            "seconds": dt, **info}
+    ncpu = os.cpu_count() or 1
+    oracle.set_threads(ncpu)
+    r = oracle_sample(img)
+    cores = oracle.get_threads()
+    oracle.set_threads(1)
+    r1 = oracle_sample(img, rows=256)
+    oracle.set_threads(ncpu)
+    return {"value": r["value"], "unit": "MPix/s", "cores": cores, "kind": "oracle", "sample": _sample_text(r, cores),
+            "cpu_model": cpu_model(), "one_thread": {"value": r1["value"], "unit": "MPix/s", "cores": 1,
+                                                     "sample": _sample_text(r1, 1)},
+            "candidates_in_band": r["candidates"], "kept_in_band": r["kept"]}
 
 
 def run_reference(args) -> None:
+    """The reference arm of this tier: the oracle as it stands on the host cores, each
+    step one oracle_sample of the same workload (same sample and rate definition as
+    cpu_baseline, so the two agree)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -165,27 +213,22 @@ def run_reference(args) -> None:
     import synth
     oracle.set_threads(os.cpu_count() or 1)
     img = synth.em_tile_np(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, bits=8)
-    # size the per-step band so the whole run stays within ~150 s of CPU time
-    probe, _ = oracle_band(img, 16)
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    rows = int(max(16, min(SIZE, 16 * budget / max(probe, 1e-3))))
-    rows = max(16, rows // 16 * 16)
-    times = []
+    vals, last = [], None
     for k in range(args.warmup + args.steps):
-        dt, info = oracle_band(img, rows)
+        last = oracle_sample(img)
         if k >= args.warmup:
-            times.append(dt)
-    ms = statistics.median(times) * 1e3
-    px = rows * SIZE
-    value = px / (ms * 1e-3) / 1e6
+            vals.append(last["value"])
+    value = statistics.median(vals)
+    ms = SIZE * SIZE / (value * 1e6) * 1e3   # per 4096^2 tile
+    cores = oracle.get_threads()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_image": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C4 tile (4096x4096 u8 synthetic EM, sigma 1-10, 10 scales, tau 0.09, "
-                                   "overlap 0.5); each step a band of rows of tile 0", "rows_per_step": rows,
-                       "parallelism": "host cores (OpenMP)"},
-            "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": oracle.get_threads(), "kind": "oracle",
-                             "sample": f"{rows} rows x {SIZE} cols per step"},
+                                   "overlap 0.5); each step one oracle sample of tile 0, rate extrapolated to the tile",
+                       "rows_per_step": ORACLE_ROWS, "parallelism": f"{cores} host threads (OpenMP)"},
+            "cpu_baseline": {"value": value, "unit": "MPix/s", "cores": cores, "kind": "oracle",
+                             "sample": _sample_text(last, cores), "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -200,40 +243,66 @@ def peaks() -> tuple[dict, str]:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "of fallback (B200_PROFILING.md)"
 
 
-def roofline_of(det, B: int, kern_ms: float, step_ms: float) -> dict:
-    """Roofline of the dominant kernel (DESIGN.md §6/§8).  k_tc is bound by the fp16
-    tensor pipe: achieved = the banded formulation's MMA flops per pixel
-    (mhfd_schedule_flops_per_pixel: 2 row-pass and 3 column-pass fp16 products per
-    level, K_i-wide Toeplitz windows) x pixels / launch time, against the sustained
-    cuBLAS bf16 peak (fp16 runs at the bf16 rate: 2.25 PF nominal for both) because the
-    kernel runs inside a long step.  The CUDA-core schedules are FP32-FMA bound.
-    `alu_equivalent` restates the same time against the direct separable blur's FMA
-    count on the FP32 pipe, i.e. how far the kernel is past the CUDA-core ceiling."""
+def _ncu_summary(name: str) -> dict:
+    p = os.path.join(ROOT, "profiles", f"ncu_{name}_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def roofline_of(det, B: int, kern_ms: float, step_ms: float, stage_ms: dict) -> dict:
+    """Roofline per SURVEY.md §8(d).  The path is FP32-ALU bound: the
+    binding work is F_alg = the cascade FFMA count of the cheapest exact separable
+    schedule (674 FFMA/px at C3), B_alg = 1 B/px.  For the dominant kernel (stage a2-a6,
+    timed live with the library's CUDA events on the launching stream):
+      achieved = F_alg x 2 FLOP x pixels per launch / kernel ms,
+      peak     = nominal FP32 (148 x 128 FFMA/clk x 1.965 GHz, x 2 FLOP),
+      frac     = achieved / peak = T_bound / T_meas (roofline_frac of §8(d) item 2).
+    Beside it: the whole step's roofline_frac, hbm_frac from the ncu DRAM bytes (per
+    kernel and for the step), and for k_tc the tensor pipe: the dense-equivalent banded
+    MMA flops it issues against the BURST cuBLAS peak (k_tc runs unthrottled) next to
+    ncu's tensor-active %."""
     pk, pk_note = peaks()
     name = det.schedule("u8")
     px = B * SIZE * SIZE
-    fpp = det.schedule_flops_per_pixel("u8")
-    achieved = fpp * px / (kern_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"ncu_{name}_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f)["dram_bytes_per_image"] * B
-    alg = alg_flops_per_px()
-    alu = {"alg_flops_per_px": alg, "achieved": alg * px / (kern_ms * 1e-3) / 1e12, "peak": ALU_PEAK_TFLOPS,
-           "unit": "TFLOP/s", "frac": alg * px / (kern_ms * 1e-3) / 1e12 / ALU_PEAK_TFLOPS,
-           "note": "direct separable blur at R_i = ceil(5 t_i) on the FP32 pipe: 148 SMs x 128 FFMA/clk x 2 x "
-                   "1.965 GHz (B200_PROFILING.md unit counts)"}
-    common = {"kernel": name, "traffic": traffic, "kernel_ms_per_launch": kern_ms, "share_of_step": kern_ms / step_ms,
-              "flops_per_px": fpp, "hbm_gbs": px * (1 + 5) / (kern_ms * 1e-3) / 1e9,
-              "hbm_note": f"{name} HBM bytes: 1 B/px read + 5 B/px (v f32 + argmax u8) written"}
+    f_alg = cascade_ffma_per_px()
+    t_bound_ms = f_alg * px / (FP32_PEAK_TFFMA * 1e12) * 1e3
+    achieved = 2 * f_alg * px / (kern_ms * 1e-3) / 1e12
+    peak = 2 * FP32_PEAK_TFFMA
+    ncu = _ncu_summary(name)
+    traffic = ncu.get("dram_bytes_per_image", None)
+    traffic = traffic * B if traffic is not None else None
+    hbm_bw = pk["hbm_gbs"]
+    step_bytes = ncu.get("step_dram_bytes_per_image")
+    line = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": name, "kernel_ms_per_launch": kern_ms, "px_per_launch": px,
+            "alg_ffma_per_px": f_alg, "alg_flops_per_px": 2 * f_alg,
+            "alg_note": "SURVEY 8(d) F_alg: cascade FFMA of the cheapest exact separable schedule (level 1 direct, "
+                        "then sigma_inc increments, k = 5), x 2 FLOP",
+            "peak_note": "nominal FP32: 148 SMs x 128 FFMA/clk x 2 x 1.965 GHz (B200_PROFILING.md unit counts)",
+            "frac_vs_ffma_ubench": achieved / (2 * FP32_UBENCH_TFFMA),
+            "roofline_frac": t_bound_ms / kern_ms, "T_bound_ms": t_bound_ms, "T_meas_ms": kern_ms,
+            "roofline_frac_step": t_bound_ms / step_ms, "step_ms": step_ms, "share_of_step": kern_ms / step_ms,
+            "direct_ffma_per_px": direct_ffma_per_px(),
+            "hbm": {"alg_bytes_per_px": 1, "peak_GBs": hbm_bw, "peak_note": pk_note,
+                    "kernel_GBs": traffic / (kern_ms * 1e-3) / 1e9 if traffic else None,
+                    "hbm_frac_kernel": traffic / (kern_ms * 1e-3) / 1e9 / hbm_bw if traffic else None,
+                    "step_GBs": step_bytes * B / (step_ms * 1e-3) / 1e9 if step_bytes else None,
+                    "hbm_frac_step": step_bytes * B / (step_ms * 1e-3) / 1e9 / hbm_bw if step_bytes else None,
+                    "alg_frac_step": px / (step_ms * 1e-3) / 1e9 / hbm_bw,
+                    "source": ncu.get("source")}}
     if name == "k_tc":
-        peak = pk["bf16_tflops_sustained"]
-        return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "peak_note": f"fp16 dense tensor = bf16 rate; sustained cuBLAS bf16 {pk_note}",
-                **common, "alu_equivalent": alu}
-    return {"bound": "alu", "achieved": achieved, "peak": ALU_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / ALU_PEAK_TFLOPS, "peak_note": alu["note"], **common}
+        fpp = det.schedule_flops_per_pixel("u8")
+        t_ach = fpp * px / (kern_ms * 1e-3) / 1e12
+        line["tensor"] = {"dense_equiv_flops_per_px": fpp, "achieved": t_ach, "unit": "TFLOP/s",
+                          "peak_burst": pk["bf16_tflops"], "frac_burst": t_ach / pk["bf16_tflops"],
+                          "peak_sustained": pk["bf16_tflops_sustained"],
+                          "frac_sustained": t_ach / pk["bf16_tflops_sustained"],
+                          "ncu_tensor_active_pct": ncu.get("tensor_active_pct"),
+                          "note": "banded Toeplitz MMA work as issued (zeros of the band included; 2 row-pass and 3 "
+                                  "column-pass fp16 products per level) vs the cuBLAS bf16 peak (fp16 = bf16 rate)"}
+    return line
 
 
 def other_configs(dev) -> dict:
@@ -472,7 +541,7 @@ def main() -> None:
     ss_ms = statistics.mean(s[1] for s in stages)
     stage_ms = {k: statistics.mean(s[i] for s in stages) for i, k in
                 enumerate(["percentiles_a1", "blur_dog_argmax_a2_a6", "nms_compact_a7_a8", "prune_score_a9_a10"])}
-    roofline = roofline_of(det, B, ss_ms, ms)
+    roofline = roofline_of(det, B, ss_ms, ms, stage_ms)
 
     # e2e through the host-buffer C-ABI entry point
     e2e = None
@@ -517,7 +586,8 @@ def main() -> None:
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "ms_per_image": ms_max / B,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 (k_tc: fp16 hi/lo split operands, f32 accumulation)",
                 "data": "synthetic",
                 "config": {"workload": "C4: per GPU a batch of 64 synthetic EM tiles 4096x4096 u8 (seed 1000+g, "
                                        "defocus 0.5*(g mod 9) px, dose 300); sigma 1-10, 10 scales, tau 0.09, "
