@@ -29,6 +29,7 @@
 #include "k_scale_space.cuh"
 #include "k_band.cuh"
 #include "k_tc.cuh"
+#include "k_tc2.cuh"
 #include "k_twopass.cuh"
 #include "k_downsample.cuh"
 
@@ -51,6 +52,8 @@ struct mhfd_ctx {
   int twopass;       // generic path for large radii: k_rows2 / k_cols_all (MHFD_NO_TWOPASS=1 disables)
   TcPlan* tc;        // tensor-core geometry (host copy, passed by value to k_tc)
   uint8_t* d_tctab;  // device copy of the Toeplitz pair tables (context-owned, immutable)
+  Tc2Plan* tc2;      // two-pass tensor-core geometry (u16 / f32 / large radii), host copy
+  uint8_t* d_tc2tab; // its device pair tables (context-owned, immutable)
   float2* d_thr;     // pruning: n x n squared-distance bands (context-owned, immutable)
   int32_t dmax[kMaxLevels];
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
@@ -87,8 +90,18 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
-      chunkcnt, chunkpos, counters, scores, counts, rx, slab, wl, total;
+      chunkcnt, chunkpos, counters, scores, counts, rx, xtc, slab, wl, total;
 };
+
+// k_tc2 (two-pass tensor-core schedule) applies: Eq. 2 DoG, periodic, plan built, widths
+// in whole 128-column tiles, heights in whole 16-row slabs, one periodic wrap of the
+// staged row window
+bool tc2_fit(const mhfd_ctx* c) {
+  return c->tc2 && c->d_tc2tab && c->band_enabled && c->p.response == MHFD_RESPONSE_DOG &&
+         c->p.boundary == MHFD_BOUNDARY_PERIODIC && c->p.width % kT2Cols == 0 && c->p.height % kT2SlabRows == 0 &&
+         c->p.width >= c->tc2->S;
+}
+int tc2_nrt(const mhfd_ctx* c) { return (c->p.height + c->tc2->NR - 1) / c->tc2->NR; }
 
 int nseg_of(const mhfd_ctx* c) {
   const int64_t plane = (int64_t)c->p.width * c->p.height;
@@ -147,7 +160,9 @@ Layout layout(const mhfd_ctx* c, int B) {
   // kRxBatch images (run_front chunks larger batches)
   const int64_t rxb = std::min(B, kRxBatch);
   const bool any2 = c->ltab || c->twopass || pair_fit(c);
-  L.rx = take(any2 ? sizeof(float) * plane * rxb * (c->ltab ? 2 * c->n : c->n + 1) : 0);
+  L.rx = take(any2 || tc2_fit(c) ? sizeof(float) * plane * rxb * (c->ltab ? 2 * c->n : c->n + 1) : 0);
+  // k_tc2: the stretched image as tiled fp16 hi/lo planes (rows padded to whole NR tiles)
+  L.xtc = take(tc2_fit(c) ? 2 * t2_x_plane_bytes(c->p.width, tc2_nrt(c), c->tc2->NR) * rxb : 0);
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
   L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
@@ -353,6 +368,63 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     kern<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, paper ? v : nullptr,
                                             paper ? idx : nullptr, tc_dog, B, r_lo, r_hi, nullptr);
     LAUNCH_CHECK("k_tc");
+    MARK(2);
+    return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
+  }
+  // ---- a2-a6 on the two-pass tensor-core schedule (u16 / f32 images, u8 beyond k_tc's tile)
+  if (tc2_fit(c) && c->band_kind == 3 && (!band || (paper && dog_dump == nullptr))) {
+    const Tc2Plan& P = *c->tc2;
+    const int nrt = tc2_nrt(c);
+    // row tiles of k_tc2_rows and output row tiles of k_tc2_cols: everything, or in band
+    // mode (f2) only the 256-row output tiles that cover [band_lo - 1, band_hi + 1) on the
+    // whole image's grid and the NR-row tiles holding the Rx rows their windows read (at
+    // most two ranges: the periodic wrap), so every response equals the whole-image run's
+    int yt0 = 0, nyt = (H + kT2ColRows - 1) / kT2ColRows;
+    int rr[2][2] = {{0, nrt}, {0, 0}};
+    if (band) {
+      const int o_lo = std::max(0, band_lo - 1), o_hi = std::min(H, band_hi + 1);
+      yt0 = o_lo / kT2ColRows;
+      nyt = (o_hi + kT2ColRows - 1) / kT2ColRows - yt0;
+      const int lo = yt0 * kT2ColRows - P.rmax - kT2SlabRows, hi = (yt0 + nyt) * kT2ColRows + P.rmax + kT2SlabRows;
+      if (hi - lo < H) {
+        auto tiles = [&](int a, int z, int (&r)[2]) { r[0] = a / P.NR; r[1] = (z + P.NR - 1) / P.NR; };
+        tiles(std::max(0, lo), std::min(H, hi), rr[0]);
+        rr[1][0] = rr[1][1] = 0;
+        if (lo < 0) tiles(H + lo, H, rr[1]);
+        if (hi > H) tiles(0, hi - H, rr[1]);
+      }
+    }
+    const size_t sm1 = tc2_rows_smem(P), sm2 = tc2_cols_smem(P);
+    auto kc = tc_dog ? k_tc2_cols<true> : k_tc2_cols<false>;
+    cudaError_t ea = cudaFuncSetAttribute(k_tc2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    if (ea == cudaSuccess) ea = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    if (ea != cudaSuccess) return cuda_fail(ea, "k_tc2 attributes");
+    uint8_t* xt = reinterpret_cast<uint8_t*>(ws + L.xtc);
+    uint8_t* rx = reinterpret_cast<uint8_t*>(ws + L.rx);
+    const int64_t plane = (int64_t)W * H;
+    for (int b0 = 0; b0 < B; b0 += kRxBatch) {
+      const int Bc = std::min(kRxBatch, B - b0);
+      const uint8_t* ic = img + (int64_t)b0 * H * pitch;
+      const ImgPar* pc = par + b0;
+      const int64_t work = (int64_t)Bc * nrt * P.NR * (W / 8);
+      const dim3 gp((unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)c->sms * 16));
+      if (bpp == 1) k_tc2_prep<1><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
+      else if (bpp == 2) k_tc2_prep<2><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
+      else k_tc2_prep<4><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
+      LAUNCH_CHECK("k_tc2_prep");
+      for (int k = 0; k < 2; ++k) {
+        if (rr[k][1] <= rr[k][0]) continue;
+        const int64_t t1 = (int64_t)(W / kT2Cols) * (rr[k][1] - rr[k][0]) * Bc;
+        k_tc2_rows<<<(unsigned)std::min<int64_t>(t1, c->sms), kT2Threads, sm1, st>>>(
+            xt, P, c->d_tc2tab, rx, W, H, Bc, nrt, rr[k][0], rr[k][1] - rr[k][0]);
+        LAUNCH_CHECK("k_tc2_rows");
+      }
+      const int64_t t2 = (int64_t)(W / kT2Cols) * nyt * Bc;
+      kc<<<(unsigned)std::min<int64_t>(t2, c->sms), kT2Threads, sm2, st>>>(
+          rx, pc, P, c->d_tc2tab, paper ? v + (int64_t)b0 * plane : nullptr, paper ? idx + (int64_t)b0 * plane : nullptr,
+          tc_dog ? tc_dog + (int64_t)b0 * c->n * plane : nullptr, W, H, Bc, yt0, nyt);
+      LAUNCH_CHECK("k_tc2_cols");
+    }
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
   }
@@ -846,6 +918,34 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
       return fail(MHFD_ERR_CUDA, "Toeplitz table upload for k_tc failed");
     }
   }
+  // two-pass tensor-core plan (k_tc2) and its tables
+  c->tc2 = new (std::nothrow) Tc2Plan;
+  if (c->tc2 && tc2_plan_build(*c->tc2, n + 1, R, t)) {
+    if (p->polarity == MHFD_BRIGHT)
+      for (int i = 0; i <= n; ++i) c->tc2->lev[i].tdog = -c->tc2->lev[i].tdog;
+    std::vector<std::vector<double>> wv(n + 1);
+    for (int i = 0; i <= n; ++i) {
+      double sum = 0.0;
+      for (int d = -R[i]; d <= R[i]; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
+      for (int d = -R[i]; d <= R[i]; ++d) wv[i].push_back(std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum);
+    }
+    std::vector<uint8_t> tabh((size_t)c->tc2->tab_bytes);
+    tc2_fill_tables(*c->tc2, wv, tabh.data());
+    int prev = 0;
+    cudaGetDevice(&prev);
+    const bool ok = cudaSetDevice(p->device) == cudaSuccess &&
+                    cudaMalloc(&c->d_tc2tab, tabh.size()) == cudaSuccess &&
+                    cudaMemcpy(c->d_tc2tab, tabh.data(), tabh.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    cudaSetDevice(prev);
+    if (!ok) {
+      cudaGetLastError();
+      mhfd_destroy(c);
+      return fail(MHFD_ERR_CUDA, "Toeplitz table upload for k_tc2 failed");
+    }
+  } else {
+    delete c->tc2;
+    c->tc2 = nullptr;
+  }
   c->radmax = 0.0;
   for (int s = 0; s < n; ++s) {
     c->rad[s] = std::sqrt(2.0) * t[s];
@@ -976,8 +1076,10 @@ void mhfd_destroy(mhfd_ctx* c) {
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
   }
   if (c->d_tctab) cudaFree(c->d_tctab);
+  if (c->d_tc2tab) cudaFree(c->d_tc2tab);
   if (c->d_thr) cudaFree(c->d_thr);
   delete c->tc;
+  delete c->tc2;
   delete c->tab;
   delete c->ltab;
   delete c;
@@ -1056,6 +1158,7 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (c->p.response == MHFD_RESPONSE_LOG) return "k_rows_pair+k_cols_pair<log>";
   if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
+  if (c->band_kind == 3 && tc2_fit(c)) return "k_tc2";
   if (dtype == MHFD_U8 && paper && c->band_enabled && band_ok(W, H, c->tab->rmax, c->tab->ntaps_total))
     return "k_band";
   if (pair_ok(c)) return "k_rows_pair+k_cols_pair";
@@ -1074,6 +1177,12 @@ double mhfd_schedule_flops_per_pixel(const mhfd_ctx* c, int32_t dtype) {
       macs += 2.0 * kTcTile * K * K + 3.0 * kTcTile * kTcTile * K;
     }
     return 2.0 * macs / ((double)kTcTile * kTcTile);
+  }
+  if (strcmp(name, "k_tc2") == 0) {   // per pixel: 3 products x K_i (row pass) + 3 x K2_i (column pass)
+    const Tc2Plan& P = *c->tc2;
+    double macs = 0.0;
+    for (int i = 0; i < P.nlev; ++i) macs += 3.0 * P.lev[i].K + 3.0 * P.lev[i].K2;
+    return 2.0 * macs;
   }
   double f = 0.0;   // direct separable blur at R_i: 2 passes x (2R_i+1) FMA per level, + DoG/max
   if (c->ltab) {    // LoG: per plane 2 row convs (w, w2) + 2 column convs, + sum/scale/max
@@ -1094,8 +1203,8 @@ mhfd_status mhfd_detect_band(mhfd_ctx* c, const void* d_image, int32_t dtype, in
   if (!(0 <= y0 && y0 < y1 && y1 <= H)) return fail(MHFD_ERR_SHAPE, "band rows [%d, %d) not inside [0, %d)", y0, y1, H);
   if (W % kSeg != 0) return fail(MHFD_ERR_SHAPE, "band mode needs width %% %d == 0", kSeg);
   const char* sch = mhfd_schedule_name(c, dtype);
-  if (strcmp(sch, "k_tc") != 0 && strcmp(sch, "k_rows_pair+k_cols_pair") != 0)
-    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc or the two-pass pair schedule (Eq. 3 NMS)");
+  if (strcmp(sch, "k_tc") != 0 && strcmp(sch, "k_tc2") != 0 && strcmp(sch, "k_rows_pair+k_cols_pair") != 0)
+    return fail(MHFD_ERR_INVALID_ARGUMENT, "band mode needs the k_tc, k_tc2 or two-pass pair schedule (Eq. 3 NMS)");
   if (!d_ncand || (!d_cands && cand_capacity > 0) || cand_capacity < 0)
     return fail(MHFD_ERR_INVALID_ARGUMENT, "d_ncand / d_cands / cand_capacity");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -142,7 +142,8 @@ def test_c2_cuda_core_schedules(schedule):
     _full_parity(img, C3, schedule=schedule)
 
 
-@pytest.mark.parametrize("nms,bits,size", [("paper", 8, 256), ("paper", 8, 1024), ("26", 8, 256), ("paper", 16, 256)])
+@pytest.mark.parametrize("nms,bits,size", [("paper", 8, 256), ("paper", 8, 1024), ("26", 8, 256), ("paper", 16, 256),
+                                           ("26", 16, 256)])
 def test_bright_polarity_parity(nms, bits, size):
     """Bright features (negated Eq. 2) on every schedule kind: k_tc (u8),
     26-mode and u16 (generic)."""
@@ -157,8 +158,11 @@ def test_u8_schedule_is_tensor_core():
     assert mhfd.Detector(4096, 4096, threshold=0.09, **C3).schedule("u8") == "k_tc"
     assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u8") == "k_tc"
     assert mhfd.Detector(256, 256, threshold=0.08, **C1).schedule("u8") == "k_tc"
-    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u16") == "k_rows_pair+k_cols_pair"
-    assert mhfd.Detector(1000, 1000, threshold=0.09, **C3).schedule("u16") == "k_scale_space"   # W % 256 != 0
+    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("u16") == "k_tc2"
+    assert mhfd.Detector(1024, 1024, threshold=0.09, **C3).schedule("f32") == "k_tc2"
+    assert mhfd.Detector(1024, 1024, 1.0, 20.0, 12, threshold=0.16).schedule("u8") == "k_tc2"   # R 100 > k_tc's tile
+    assert mhfd.Detector(1024, 1024, threshold=0.09, schedule="band", **C3).schedule("u16") == "k_rows_pair+k_cols_pair"
+    assert mhfd.Detector(1000, 1000, threshold=0.09, **C3).schedule("u16") == "k_scale_space"   # W % 128 != 0
 
 
 def test_u16_generic_schedule_parity():
@@ -383,7 +387,7 @@ def test_band_sharding_pair_schedule_u16(G):
     a = synth.em_tile_np(size, size, 1009, defocus=0.5, dose=300.0, bits=16)
     img = torch.from_numpy(a.astype(np.int32)).cuda().to(torch.uint16)
     det = mhfd.Detector(size, size, 1.0, 20.0, 12, threshold=0.1 * 19.0 / 12)
-    assert det.schedule("u16") == "k_rows_pair+k_cols_pair"
+    assert det.schedule("u16") == "k_tc2"
     full = det.debug_dump(img, dog=False, cands=True)
     nfull = int(full["ncand"][0])
     blobs_full, cnt_full, _ = det.detect(img)
@@ -418,8 +422,8 @@ def test_twopass_matches_fused_generic_bitwise():
         for flag in (None, "1"):
             if flag:
                 os.environ["MHFD_NO_TWOPASS"] = flag
-            try:
-                det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, **cfg)
+            try:   # "band": the CUDA-core schedules (no tensor-core kernel takes the u16 image)
+                det = mhfd.Detector(1024, 1024, threshold=0.1 * 19.0 / 12, schedule="band", **cfg)
             finally:
                 os.environ.pop("MHFD_NO_TWOPASS", None)
             assert det.schedule("u16") == ("k_rows2+k_cols_all" if flag is None else "k_scale_space")
@@ -447,7 +451,8 @@ def test_cols_pair_matches_cols_all():
     imgs = [synth.em_tile(1000, 1024, 1105 + k, defocus=0.5 * k, dose=300.0, bits=16, device="cuda") for k in range(2)]
     imgs.append(torch.full((1000, 1024), 777, dtype=torch.int32))
     img = torch.from_numpy(np.stack([t.to(torch.int32).cpu().numpy() for t in imgs]).astype(np.uint16))
-    det = mhfd.Detector(1024, 1000, min_sigma=1.0, max_sigma=20.0, num_scales=12, threshold=0.1 * 19.0 / 12)
+    det = mhfd.Detector(1024, 1000, min_sigma=1.0, max_sigma=20.0, num_scales=12, threshold=0.1 * 19.0 / 12,
+                        schedule="band")
     assert det.schedule("u16") == "k_rows_pair+k_cols_pair"
     res = []
     for flag in (None, "1"):
@@ -594,7 +599,7 @@ def test_two_pass_batch_chunks(response):
     batch = torch.from_numpy(np.stack(imgs).astype(np.int32)).cuda().to(torch.uint16)
     det = mhfd.Detector(512, 256, 1.0, 6.0, 5, threshold=0.1 if response == "log" else 0.1,
                         response=response)
-    assert det.schedule("u16").startswith("k_rows_pair+k_cols_pair")
+    assert det.schedule("u16") == ("k_tc2" if response == "dog" else "k_rows_pair+k_cols_pair<log>")
     blobs, cnt, _ = det.detect(batch)
     torch.cuda.synchronize()
     assert int(cnt[10]) == 0
@@ -616,7 +621,7 @@ def test_f32_input_full_parity(size, cfg):
     s = _full_parity(img, cfg)
     assert s["n_oracle"] > 50
     det = mhfd.Detector(size, size, threshold=_tau(cfg), **cfg)
-    assert det.schedule("f32") == ("k_rows_pair+k_cols_pair" if size == 256 else "k_scale_space")
+    assert det.schedule("f32") == ("k_tc2" if size == 256 else "k_scale_space")
 
 
 def test_f32_integer_valued_equals_u16():
@@ -657,7 +662,7 @@ def test_reflect_differs_from_periodic_only_near_edges():
     img = torch.from_numpy(a16.astype(np.int32)).cuda().to(torch.uint16)
     res = []
     for bd in ("periodic", "reflect"):
-        det = mhfd.Detector(512, 256, threshold=0.08, boundary=bd, **C1)
+        det = mhfd.Detector(512, 256, threshold=0.08, boundary=bd, schedule="band", **C1)   # both on the pair kernels
         assert det.schedule("u16") == "k_rows_pair+k_cols_pair"
         res.append(det.debug_dump(img, dog=False, cands=False)["v"][0].cpu())
     R = 25   # ceil(5 * 5)
@@ -716,3 +721,47 @@ def test_downsample_pitched_buffers():
             got = d[b, :, :OW * bpp].copy().view(npd).reshape(OH, OW)
             assert np.array_equal(got, oracle.downsample(a[b], f))
         assert (d[:, :, OW * bpp:] == 0xAB).all()
+
+
+# ---------------------------------------------------------------- k_tc2 (two-pass tensor cores)
+@pytest.mark.parametrize("bits,cfg,size", [(16, C3, 1024), (8, dict(min_sigma=1.0, max_sigma=20.0, num_scales=12), 1024),
+                                           (16, C1, 512)])
+def test_tc2_full_parity(bits, cfg, size):
+    """k_tc2 (u16, and u8 with R_max 100 > k_tc's tile) in full against the oracle; and the
+    CUDA-core pair kernels (schedule="band") on the same image agree with it within the
+    parity tolerance."""
+    img = synth.em_tile_np(size, size, 1011, defocus=0.5, dose=300.0, bits=bits)
+    det = mhfd.Detector(size, size, threshold=_tau(cfg), **cfg)
+    assert det.schedule(f"u{bits}") == "k_tc2"
+    s = _full_parity(img, cfg)
+    assert s["n_oracle"] > 500
+    alt = mhfd.Detector(size, size, threshold=_tau(cfg), schedule="band", **cfg)
+    t = _to_t(img) if bits == 8 else torch.from_numpy(img.astype(np.int32)).cuda().to(torch.uint16)
+    va = det.debug_dump(t, dog=False, cands=False)["v"]
+    vb = alt.debug_dump(t, dog=False, cands=False)["v"]
+    torch.cuda.synchronize()
+    assert float((va - vb).abs().max()) <= 2 * P.REL_EPS * float(vb.abs().max())
+
+
+def test_tc2_batch_ragged_rows_and_degenerate():
+    """k_tc2 with H not a multiple of its row tiles (NR) or of 256, a batch of 11 (> 8:
+    chunked Rx), a constant image inside: image by image equal to single-image calls, the
+    constant one all zero."""
+    imgs = [synth.em_tile_np(400, 512, 1600 + k, defocus=0.3 * (k % 4), dose=300.0, bits=16) for k in range(10)]
+    imgs.insert(4, np.full((400, 512), 1234, np.uint16))
+    batch = torch.from_numpy(np.stack(imgs).astype(np.int32)).cuda().to(torch.uint16)
+    det = mhfd.Detector(512, 400, 1.0, 6.0, 5, threshold=0.1)
+    assert det.schedule("u16") == "k_tc2"
+    blobs, cnt, _ = det.detect(batch)
+    d = det.debug_dump(batch, dog=True, cands=False)
+    torch.cuda.synchronize()
+    assert int(cnt[4]) == 0 and float(d["v"][4].abs().max()) == 0.0 and float(d["dog"][4].abs().max()) == 0.0
+    for k in range(11):
+        b1, c1, _ = det.detect(batch[k:k + 1])
+        torch.cuda.synchronize()
+        n = int(c1[0])
+        assert n == int(cnt[k]) and torch.equal(b1[0, :n], blobs[k, :n]), k
+    ref = oracle.detect(imgs[7], 1.0, 6.0, 5, 0.1, 0.5, dump=True)
+    eps = P.REL_EPS * float(ref["D"].max())
+    assert float(np.abs(d["dog"][7].cpu().numpy() - ref["D"]).max()) <= eps
+    P.assert_score(int(cnt[7]), ref["count"])
