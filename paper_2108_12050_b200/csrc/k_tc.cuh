@@ -149,7 +149,11 @@ __device__ __forceinline__ void split_half(const uint32_t (&r)[8], uint32_t (&h4
     l4[u] = *reinterpret_cast<const uint32_t*>(&ll);
   }
 }
+#ifndef TC_EXP
+#define TC_EXP 0   // performance experiments only (tools/tc_exp.py): 1 no DoG reads, 2 one DoG read, 3 no split, 4 = 1 + 3
+#endif
 __device__ __forceinline__ void tc_split_chunk(uint32_t tq, int j) {
+  if (TC_EXP == 3 || TC_EXP == 4) return;
   const uint32_t base = tq + 16 * j;
   uint32_t r[8], h4[4], l4a[4], l4b[4];
   umma::ld8(base, r);
@@ -204,7 +208,9 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
 #define TC_STAMP(g, slot) \
   do { if (tr && (g) < 64) tr[(g) * 16 + (slot)] = clock64(); } while (0)
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // warp index through a shuffle: the compiler can then prove the role branches below
+  // warp-uniform and keep the issuer's descriptors in uniform registers
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   // rows [row_lo, row_hi) of every image (the whole image, or one band: mhfd_detect_band)
   const int tx = (s.W + kTcTile - 1) / kTcTile, ty = (row_hi - row_lo + kTcTile - 1) / kTcTile;
   const int ntiles = tx * ty * batch;
@@ -226,62 +232,67 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
 
   if (warp == kTcThreads / 32) {
     // ================= MMA issuer =================
-    if (lane == 0) {
-      auto issue_table = [&](int gg) {
+    // The whole warp runs this loop (warp-uniform branch: `warp` comes through
+    // __shfl_sync), one elected lane issues each tcgen05 instruction (umma::*_w), so the
+    // descriptors live in uniform registers.
+    if (lane != 0) tr = nullptr;
+    auto issue_table = [&](int gg) {
+      if (lane == 0) {
         const int lev = gg % P.nlev;
         const int bytes = 2 * P.lev[lev].npairs * 256;
         uint64_t* tb = &bars[8 + (gg & 1)];
         mbar_arrive_expect_tx(tb, (uint32_t)bytes);
         bulk_g2s(tbuf + (size_t)(gg & 1) * P.max_level_bytes, tabs + P.lev[lev].tab_off, (uint32_t)bytes, tb);
-      };
-      issue_table(0);
-      if (G > 1) issue_table(1);
-      int tile_i = 0;
-      uint32_t sph = 0;   // phase bits of the split barriers (group 3 is not used on every level)
-      for (int g = 0; g < G; ++g) {
-        const int lev = g % P.nlev;
-        TC_STAMP(g, 0);
-        if (lev == 0) mbar_wait(&bars[7], (uint32_t)(tile_i++ & 1));
-        mbar_wait(&bars[8 + (g & 1)], (uint32_t)((g >> 1) & 1));
-        umma::fence_after();
-        TC_STAMP(g, 1);
-        const TcLevel& L = P.lev[lev];
-        const int K = L.K, E1 = K / 8 - 2, nj = K / 16;
-        const uint32_t thi = umma::smem_addr(tbuf + (size_t)(g & 1) * P.max_level_bytes);
-        const uint32_t tlo = thi + L.npairs * 256;
-        const uint32_t b1 = umma::smem_addr(B1) + (L.c0 / 8) * SBO1 + (L.c0 / 8) * 128;
-        const uint32_t idr = umma::idesc_f16(128, K), idc = umma::idesc_f16(128, 128);
-        // K-step j: B1 window +256 B (start field +16), Toeplitz pairs -512 B (field -32)
-        const uint64_t dB = umma::desc_kmajor(b1, 128, SBO1);
-        const uint64_t dH = umma::desc_kmajor(thi + E1 * 256, 128, 256);
-        const uint64_t dL = umma::desc_kmajor(tlo + E1 * 256, 128, 256);
-        // row pass of level g.  No wait for the previous column pass: tcgen05.mma from one
-        // thread execute in issue order, so these writes of D1 follow its reads of A2.
-        for (int j = 0; j < nj; ++j) {
-          umma::mma_ss(tmem, dH - 32u * j, dB + 16u * j, idr, j > 0);
-          umma::mma_ss(tmem, dL - 32u * j, dB + 16u * j, idr, 1);
-        }
-        umma::commit(&bars[1]);
-        TC_STAMP(g, 2);
-        if (g > 0) {
-          mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));   // column pass g-1 done: table buffer free
-          if (g + 1 < G) issue_table(g + 1);
-        }
-        const uint32_t d2 = tmem + 256 + 128 * (g & 1);
-        for (int grp = 0; 4 * grp < nj; ++grp) {
-          mbar_wait(&bars[3 + grp], (sph >> grp) & 1u);
-          sph ^= 1u << grp;
-          umma::fence_after();
-          TC_STAMP(g, 3 + grp);
-          for (int j = 4 * grp; j < nj && j < 4 * grp + 4; ++j) {
-            umma::mma_ts(d2, tmem + 16 * j, dH - 32u * j, idc, j > 0);
-            umma::mma_ts(d2, tmem + 16 * j, dL - 32u * j, idc, 1);
-            umma::mma_ts(d2, tmem + 16 * j + 8, dH - 32u * j, idc, 1);
-          }
-        }
-        umma::commit(&bars[2]);
-        TC_STAMP(g, 7);
       }
+      __syncwarp();
+    };
+    issue_table(0);
+    if (G > 1) issue_table(1);
+    int tile_i = 0;
+    uint32_t sph = 0;   // phase bits of the split barriers (group 3 is not used on every level)
+    for (int g = 0; g < G; ++g) {
+      const int lev = g % P.nlev;
+      TC_STAMP(g, 0);
+      if (lev == 0) mbar_wait(&bars[7], (uint32_t)(tile_i++ & 1));
+      mbar_wait(&bars[8 + (g & 1)], (uint32_t)((g >> 1) & 1));
+      umma::fence_after();
+      TC_STAMP(g, 1);
+      const TcLevel& L = P.lev[lev];
+      const int K = L.K, E1 = K / 8 - 2, nj = K / 16;
+      const uint32_t thi = umma::smem_addr(tbuf + (size_t)(g & 1) * P.max_level_bytes);
+      const uint32_t tlo = thi + L.npairs * 256;
+      const uint32_t b1 = umma::smem_addr(B1) + (L.c0 / 8) * SBO1 + (L.c0 / 8) * 128;
+      const uint32_t idr = umma::idesc_f16(128, K), idc = umma::idesc_f16(128, 128);
+      // K-step j: B1 window +256 B (start field +16), Toeplitz pairs -512 B (field -32)
+      const uint64_t dB = umma::desc_kmajor(b1, 128, SBO1);
+      const uint64_t dH = umma::desc_kmajor(thi + E1 * 256, 128, 256);
+      const uint64_t dL = umma::desc_kmajor(tlo + E1 * 256, 128, 256);
+      // row pass of level g.  No wait for the previous column pass: tcgen05.mma from one
+      // thread execute in issue order, so these writes of D1 follow its reads of A2.
+      for (int j = 0; j < nj; ++j) {
+        umma::mma_ss_w(tmem, dH - 32u * j, dB + 16u * j, idr, j > 0);
+        umma::mma_ss_w(tmem, dL - 32u * j, dB + 16u * j, idr, 1);
+      }
+      umma::commit_w(&bars[1]);
+      TC_STAMP(g, 2);
+      if (g > 0) {
+        mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));   // column pass g-1 done: table buffer free
+        if (g + 1 < G) issue_table(g + 1);
+      }
+      const uint32_t d2 = tmem + 256 + 128 * (g & 1);
+      for (int grp = 0; 4 * grp < nj; ++grp) {
+        mbar_wait(&bars[3 + grp], (sph >> grp) & 1u);
+        sph ^= 1u << grp;
+        umma::fence_after();
+        TC_STAMP(g, 3 + grp);
+        for (int j = 4 * grp; j < nj && j < 4 * grp + 4; ++j) {
+          umma::mma_ts_w(d2, tmem + 16 * j, dH - 32u * j, idc, j > 0);
+          umma::mma_ts_w(d2, tmem + 16 * j, dL - 32u * j, idc, 1);
+          umma::mma_ts_w(d2, tmem + 16 * j + 8, dH - 32u * j, idc, 1);
+        }
+      }
+      umma::commit_w(&bars[2]);
+      TC_STAMP(g, 7);
     }
     __syncwarp();
   } else {
@@ -307,9 +318,19 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {   // 8 rows at a time: fewer live registers (96 with 17 warps)
         uint32_t a[8], b[8];
-        umma::ld8(cur + 8 * qq, a);
-        umma::ld8(prv + 8 * qq, b);
-        umma::wait_ld();
+        if (TC_EXP == 1 || TC_EXP == 4) {
+#pragma unroll
+          for (int uu = 0; uu < 8; ++uu) a[uu] = b[uu] = __float_as_uint((float)uu);
+        } else if (TC_EXP == 2) {
+          umma::ld8(cur + 8 * qq, a);
+          umma::wait_ld();
+#pragma unroll
+          for (int uu = 0; uu < 8; ++uu) b[uu] = a[(uu + 1) & 7];
+        } else {
+          umma::ld8(cur + 8 * qq, a);
+          umma::ld8(prv + 8 * qq, b);
+          umma::wait_ld();
+        }
 #pragma unroll
         for (int uu = 0; uu < 8; ++uu) {
           const int u = 8 * qq + uu;
