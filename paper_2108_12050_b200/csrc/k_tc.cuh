@@ -32,6 +32,11 @@
 
 namespace mhfd {
 
+#ifndef TC_EXP
+#define TC_EXP 0   // performance experiments only (tools/tc_exp.py): 1 no DoG reads, 2 one DoG read, 3 no split, 4 = 1 + 3,
+                   // 5 no output writes, 6 no staging conversion
+#endif
+
 constexpr int kTcThreads = 512;
 
 __host__ __device__ inline int tc_off(const TcPlan& P) { return (16 - P.H0 % 16) % 16; }   // landing column offset
@@ -104,31 +109,44 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// raw window (land) -> B1: saturate to [lo, hi], centre on mid, exact fp16; chunk g of
-// 8 pixels lands at B1 + 16 g (canonical K-major: row group, column chunk, row)
+// raw window (land) -> B1: saturate to [lo, hi], centre on mid, exact fp16; chunk (r, kc)
+// of 8 pixels lands at B1 + ((r/8 * S/8 + kc) * 8 + r%8) * 16 (canonical K-major: row
+// group, column chunk, row).  Called by the 16 epilogue warps.  Each warp converts blocks
+// of 8 rows x 16 chunks; lane -> (r8 = lane & 7, kc = lane/8 + 4 ((r8 + i) & 3)) in its
+// i-th step, so the 8-byte loads hit 16 distinct bank pairs although every land row starts
+// at the same bank (LW = 256), and the 16-byte stores of the 8 rows fall in 8 distinct bank
+// groups: 2 and 4 wavefronts per instruction, the minimum (the raster mapping was 8-way
+// conflicted on the loads).
 __device__ __forceinline__ void tc_stage_b1(const uint8_t* land, uint8_t* B1, int S, int LW, int OFF, int lo, int hi,
                                             int mid) {
   const uint32_t lo2 = (uint32_t)lo * 0x10001u, hi2 = (uint32_t)hi * 0x10001u;
   const __half2 cm = __floats2half2_rn(1024.f + (float)mid, 1024.f + (float)mid);
-  const int nchunk = S * S / 8, kcs = S / 8;
-  for (int gch = threadIdx.x; gch < nchunk; gch += kTcThreads) {
-    const int cm8 = gch >> 3;
-    const int r = (cm8 / kcs) * 8 + (gch & 7), kc = cm8 % kcs;
-    const uint2 raw = *reinterpret_cast<const uint2*>(land + (size_t)r * LW + OFF + 8 * kc);
-    const uint32_t a = clamp_bytes(raw.x, lo2, hi2), bb = clamp_bytes(raw.y, lo2, hi2);
-    // 0x64pp = fp16 1024 + p exactly; subtracting 1024 + mid leaves the integer p - mid
-    const uint32_t p0 = __byte_perm(a, 0x64646464u, 0x4140u), p1 = __byte_perm(a, 0x64646464u, 0x4342u);
-    const uint32_t p2 = __byte_perm(bb, 0x64646464u, 0x4140u), p3 = __byte_perm(bb, 0x64646464u, 0x4342u);
-    __half2 x0 = __hsub2(*reinterpret_cast<const __half2*>(&p0), cm);
-    __half2 x1 = __hsub2(*reinterpret_cast<const __half2*>(&p1), cm);
-    __half2 x2 = __hsub2(*reinterpret_cast<const __half2*>(&p2), cm);
-    __half2 x3 = __hsub2(*reinterpret_cast<const __half2*>(&p3), cm);
-    uint4 o;
-    o.x = *reinterpret_cast<uint32_t*>(&x0);
-    o.y = *reinterpret_cast<uint32_t*>(&x1);
-    o.z = *reinterpret_cast<uint32_t*>(&x2);
-    o.w = *reinterpret_cast<uint32_t*>(&x3);
-    *reinterpret_cast<uint4*>(B1 + (size_t)gch * 16) = o;
+  const int kcs = S / 8, nkb = (kcs + 15) / 16, nblk = (S / 8) * nkb;
+  const int lane = threadIdx.x & 31, r8 = lane & 7;
+  if (TC_EXP == 6) return;
+  for (int blk = threadIdx.x >> 5; blk < nblk; blk += kTcThreads / 32) {
+    const int rg = blk / nkb, kb = blk - rg * nkb;
+    const int r = rg * 8 + r8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kc = kb * 16 + (lane >> 3) + 4 * ((r8 + i) & 3);
+      if (kc >= kcs) continue;
+      const uint2 raw = *reinterpret_cast<const uint2*>(land + (size_t)r * LW + OFF + 8 * kc);
+      const uint32_t a = clamp_bytes(raw.x, lo2, hi2), bb = clamp_bytes(raw.y, lo2, hi2);
+      // 0x64pp = fp16 1024 + p exactly; subtracting 1024 + mid leaves the integer p - mid
+      const uint32_t p0 = __byte_perm(a, 0x64646464u, 0x4140u), p1 = __byte_perm(a, 0x64646464u, 0x4342u);
+      const uint32_t p2 = __byte_perm(bb, 0x64646464u, 0x4140u), p3 = __byte_perm(bb, 0x64646464u, 0x4342u);
+      __half2 x0 = __hsub2(*reinterpret_cast<const __half2*>(&p0), cm);
+      __half2 x1 = __hsub2(*reinterpret_cast<const __half2*>(&p1), cm);
+      __half2 x2 = __hsub2(*reinterpret_cast<const __half2*>(&p2), cm);
+      __half2 x3 = __hsub2(*reinterpret_cast<const __half2*>(&p3), cm);
+      uint4 o;
+      o.x = *reinterpret_cast<uint32_t*>(&x0);
+      o.y = *reinterpret_cast<uint32_t*>(&x1);
+      o.z = *reinterpret_cast<uint32_t*>(&x2);
+      o.w = *reinterpret_cast<uint32_t*>(&x3);
+      *reinterpret_cast<uint4*>(B1 + ((size_t)(rg * kcs + kc) * 8 + r8) * 16) = o;
+    }
   }
 }
 
@@ -149,9 +167,6 @@ __device__ __forceinline__ void split_half(const uint32_t (&r)[8], uint32_t (&h4
     l4[u] = *reinterpret_cast<const uint32_t*>(&ll);
   }
 }
-#ifndef TC_EXP
-#define TC_EXP 0   // performance experiments only (tools/tc_exp.py): 1 no DoG reads, 2 one DoG read, 3 no split, 4 = 1 + 3
-#endif
 __device__ __forceinline__ void tc_split_chunk(uint32_t tq, int j) {
   if (TC_EXP == 3 || TC_EXP == 4) return;
   const uint32_t base = tq + 16 * j;
@@ -348,19 +363,22 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         }
       }
     };
-    auto write_out = [&]() {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
-      if (DOG && !v_out) return;
-      const int x = ot.x0 + 32 * q + lane;
+    auto write_out = [&](const TcTile& wt, int wdeg) {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
+      if ((DOG && !v_out) || TC_EXP == 5) return;
+      const int x = wt.x0 + 32 * q + lane;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
-        const int y = ot.y0 + 32 * wg + u;
+        const int y = wt.y0 + 32 * wg + u;
         if (x < s.W && y < row_hi) {
-          const int64_t pidx = (int64_t)ot.b * plane + (int64_t)y * s.W + x;
-          v_out[pidx] = odeg ? 0.f : vbest[u];
-          idx_out[pidx] = odeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+          const int64_t pidx = (int64_t)wt.b * plane + (int64_t)y * s.W + x;
+          v_out[pidx] = wdeg ? 0.f : vbest[u];
+          idx_out[pidx] = wdeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
         }
       }
     };
+    TcTile wt = tt;   // tile whose output is pending (written after the split of the next tile's level 0)
+    int wdeg = 0;
+    bool pending = false;
 
     if (tid != 0) tr = nullptr;
     for (int g = 0; g < G; ++g) {
@@ -382,20 +400,21 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         epi_sync();   // landing zone free
         const int tn = t + gridDim.x;
         if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty, row_lo), land, &bars[0], images, s, &tmap, use_tmap, P);
-        // ---- DoG of the previous tile's last level, then its output
+        // ---- DoG of the previous tile's last level (before this level's column pass
+        // overwrites D2[g & 1] = its L_{n-1}); its output is written after the split below,
+        // off the tensor pipe's critical path (level 0 has no DoG, so v/argmax stay put
+        // until the consume of level 1 at iteration g + 2)
         if (g > 0) {
           mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
           umma::fence_after();
           consume(g - 1);
-          write_out();
+          wt = ot;
+          wdeg = odeg;
+          pending = true;
         }
         ot = tt;
         oinv = ip.inv * (1.f / kTcWScale);
         odeg = ip.degen;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) vbest[u] = -INFINITY;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) ibest[u] = 0u;
         if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty, row_lo); }
       } else {
         mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
@@ -418,11 +437,19 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         if (lane == 0) mbar_arrive1(&bars[3 + grp]);
         TC_STAMP(g, 12 + grp);
       }
+      if (lev == 0) {
+        if (pending) write_out(wt, wdeg);
+        pending = false;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) vbest[u] = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ibest[u] = 0u;
+      }
     }
     mbar_wait(&bars[2], (uint32_t)((G - 1) & 1));
     umma::fence_after();
     consume(G - 1);
-    write_out();
+    write_out(ot, odeg);
   }
   umma::fence_before();
   __syncthreads();
