@@ -134,7 +134,7 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
   uint8_t* tbuf = xs + 2 * xplane;              // 2 x max_lev_bytes1
   uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * (size_t)P.max_lev_bytes1);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;   // warp-uniform roles
   const int ntx = W / kT2Cols;
   const int ntiles = ntx * rt_count * batch;   // row tiles [rt_first, rt_first + rt_count) (band mode: a subset)
   const int t0 = blockIdx.x;
@@ -161,8 +161,8 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
   };
 
   if (warp == kT2Epi / 32) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp, elected lane issues; umma::*_w) =================
+    {
       const uint32_t idesc = umma::idesc_f16(128, NR);
       for (int g = 0; g < G; ++g) {
         const int lev = g % nlev;
@@ -182,13 +182,13 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
         const uint32_t d1 = tmem + (uint32_t)((g & 1) * NR);
         const uint32_t stepx = 2u * NR;   // two column groups per K-step, in 16-byte units
         for (int j = 0; j < L.K / 16; ++j) {
-          umma::mma_ss(d1, dH - 32u * j, dXh + stepx * j, idesc, j > 0);
-          umma::mma_ss(d1, dL - 32u * j, dXh + stepx * j, idesc, 1);
-          umma::mma_ss(d1, dH - 32u * j, dXl + stepx * j, idesc, 1);
+          umma::mma_ss_w(d1, dH - 32u * j, dXh + stepx * j, idesc, j > 0);
+          umma::mma_ss_w(d1, dL - 32u * j, dXh + stepx * j, idesc, 1);
+          umma::mma_ss_w(d1, dH - 32u * j, dXl + stepx * j, idesc, 1);
         }
-        umma::commit(&bars[g & 1]);
-        umma::commit(&bars[6 + (g & 1)]);
-        if (lev == nlev - 1) umma::commit(&bars[9]);
+        umma::commit_w(&bars[g & 1]);
+        umma::commit_w(&bars[6 + (g & 1)]);
+        if (lev == nlev - 1) umma::commit_w(&bars[9]);
       }
     }
     __syncwarp();
@@ -277,7 +277,7 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
   uint8_t* tbuf = ring + (size_t)kT2Stages * 2 * kT2SlabBytes;     // 2 x max_lev_bytes2
   uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * (size_t)P.max_lev_bytes2);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kT2Stages);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;   // warp-uniform roles
   const int ntx = W / kT2Cols, nty = yt_count;   // output row tiles [yt_first, yt_first + yt_count)
   const int ntiles = ntx * nty * batch;
   const int t0 = blockIdx.x;
@@ -305,8 +305,8 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
   };
 
   if (warp == kT2Epi / 32) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp, elected lane issues; umma::*_w) =================
+    {
       const uint32_t idesc = umma::idesc_f16(128, kT2ColRows);
       const uint32_t ring0 = umma::smem_addr(ring);
       uint32_t cnt = 0;
@@ -327,13 +327,13 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
           umma::fence_after();
           const uint64_t aH = umma::desc_kmajor(ring0 + st * 2 * kT2SlabBytes, kT2SlabBytes / 2, 128);
           const uint64_t aL = umma::desc_kmajor(ring0 + st * 2 * kT2SlabBytes + kT2SlabBytes, kT2SlabBytes / 2, 128);
-          umma::mma_ss(d2, aH, dH - 32u * j, idesc, j > 0);
-          umma::mma_ss(d2, aH, dL - 32u * j, idesc, 1);
-          umma::mma_ss(d2, aL, dH - 32u * j, idesc, 1);
-          umma::commit(&bars[8 + kT2Stages + st]);
+          umma::mma_ss_w(d2, aH, dH - 32u * j, idesc, j > 0);
+          umma::mma_ss_w(d2, aH, dL - 32u * j, idesc, 1);
+          umma::mma_ss_w(d2, aL, dH - 32u * j, idesc, 1);
+          umma::commit_w(&bars[8 + kT2Stages + st]);
         }
-        umma::commit(&bars[g & 1]);
-        umma::commit(&bars[6 + (g & 1)]);
+        umma::commit_w(&bars[g & 1]);
+        umma::commit_w(&bars[6 + (g & 1)]);
       }
     }
     __syncwarp();
