@@ -252,9 +252,11 @@ def _ncu_summary(name: str) -> dict:
 
 
 def roofline_of(det, B: int, kern_ms: float, step_ms: float, stage_ms: dict) -> dict:
-    """Roofline per SURVEY.md §8(d).  The path is FP32-ALU bound: the
-    binding work is F_alg = the cascade FFMA count of the cheapest exact separable
-    schedule (674 FFMA/px at C3), B_alg = 1 B/px.  For the dominant kernel (stage a2-a6,
+    """Roofline per SURVEY.md §8(d).  On CUDA cores the path is FP32-ALU
+    bound: F_alg = the cascade FFMA count of the cheapest exact separable schedule (674
+    FFMA/px at C3), B_alg = 1 B/px.  The tcgen05 kernel k_tc beats that bound, so for it
+    the top-level roofline is the tensor pipe (issued banded-GEMM work vs the burst
+    cuBLAS peak) and the ALU figures move to `alu_cascade`.  For the dominant kernel (stage a2-a6,
     timed live with the library's CUDA events on the launching stream):
       achieved = F_alg x 2 FLOP x pixels per launch / kernel ms,
       peak     = nominal FP32 (148 x 128 FFMA/clk x 1.965 GHz, x 2 FLOP),
@@ -293,15 +295,24 @@ def roofline_of(det, B: int, kern_ms: float, step_ms: float, stage_ms: dict) -> 
                     "alg_frac_step": px / (step_ms * 1e-3) / 1e9 / hbm_bw,
                     "source": ncu.get("source")}}
     if name == "k_tc":
+        # The tensor-core kernel beats the FP32 cascade bound above (roofline_frac > 1), so
+        # the ALU roofline no longer bounds it: its roofline is the fp16 tensor pipe, with
+        # the banded-GEMM formulation's work per pixel (DESIGN.md §6.1 / §8) as F_alg.
         fpp = det.schedule_flops_per_pixel("u8")
         t_ach = fpp * px / (kern_ms * 1e-3) / 1e12
-        line["tensor"] = {"dense_equiv_flops_per_px": fpp, "achieved": t_ach, "unit": "TFLOP/s",
-                          "peak_burst": pk["bf16_tflops"], "frac_burst": t_ach / pk["bf16_tflops"],
-                          "peak_sustained": pk["bf16_tflops_sustained"],
+        floor_pf = 148 * 8192 * 1.965e9 / 1e12   # tcgen05 kind::f16 M128 floor: 8192 FLOP/clk/SM at 1.965 GHz
+        alu = {k: line.pop(k) for k in ("bound", "achieved", "peak", "unit", "frac")}
+        alu["note"] = "method-level ALU roofline (SURVEY 8(d)): frac > 1 = faster than any FP32 cascade schedule"
+        line.update({"bound": "tensor", "achieved": t_ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": t_ach / pk["bf16_tflops"]})
+        line["alu_cascade"] = alu
+        line["tensor"] = {"alg_flops_per_px": fpp, "peak_note": "burst cuBLAS bf16 " + pk_note + " (fp16 = bf16 rate; "
+                          "k_tc runs unthrottled)", "peak_sustained": pk["bf16_tflops_sustained"],
                           "frac_sustained": t_ach / pk["bf16_tflops_sustained"],
+                          "peak_tcgen05_floor": floor_pf, "frac_tcgen05_floor": t_ach / floor_pf,
                           "ncu_tensor_active_pct": ncu.get("tensor_active_pct"),
-                          "note": "banded Toeplitz MMA work as issued (zeros of the band included; 2 row-pass and 3 "
-                                  "column-pass fp16 products per level) vs the cuBLAS bf16 peak (fp16 = bf16 rate)"}
+                          "note": "F_alg = the banded Toeplitz MMA work the formulation issues per pixel (zeros of "
+                                  "the band included; 2 row-pass and 3 column-pass fp16 products per level)"}
     return line
 
 

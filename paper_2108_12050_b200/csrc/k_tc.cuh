@@ -365,14 +365,25 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     };
     auto write_out = [&](const TcTile& wt, int wdeg) {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
       if ((DOG && !v_out) || TC_EXP == 5) return;
-      const int x = wt.x0 + 32 * q + lane;
+      const int x = wt.x0 + 32 * q + lane, y0 = wt.y0 + 32 * wg;
+      const int64_t p0 = (int64_t)wt.b * plane + (int64_t)y0 * s.W + x;
+      float* vo = v_out + p0;
+      uint8_t* io = idx_out + p0;
+      if (x < s.W && y0 + 32 <= row_hi) {   // whole column piece inside: pointer walk, no checks
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int y = wt.y0 + 32 * wg + u;
-        if (x < s.W && y < row_hi) {
-          const int64_t pidx = (int64_t)wt.b * plane + (int64_t)y * s.W + x;
-          v_out[pidx] = wdeg ? 0.f : vbest[u];
-          idx_out[pidx] = wdeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+        for (int u = 0; u < 32; ++u) {
+          *vo = wdeg ? 0.f : vbest[u];
+          *io = wdeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+          vo += s.W;
+          io += s.W;
+        }
+      } else if (x < s.W) {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          if (y0 + u < row_hi) {
+            vo[(int64_t)u * s.W] = wdeg ? 0.f : vbest[u];
+            io[(int64_t)u * s.W] = wdeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+          }
         }
       }
     };
@@ -381,61 +392,70 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     bool pending = false;
 
     if (tid != 0) tr = nullptr;
-    for (int g = 0; g < G; ++g) {
-      const int lev = g % P.nlev;
+    // g == G is a tail step: the last level's DoG and the last tile's output only (one
+    // call site each for consume and the output, which keeps the kernel's code small)
+    for (int g = 0; g <= G; ++g) {
+      const bool last = g == G;
+      const int lev = last ? 0 : g % P.nlev;
       const uint32_t par_g = (uint32_t)(g & 1);
       TC_STAMP(g, 8);
-      if (lev == 0) {
+      ImgPar ip{};
+      int tn = 0;
+      if (lev == 0 && !last) {
         // ---- stage tile tt (rowDone of the previous tile's last level was waited below)
         if (mode) {
           mbar_wait(&bars[0], land_phase);
           land_phase ^= 1u;
         }
         epi_sync();
-        const ImgPar ip = par[tt.b];
+        ip = par[tt.b];
         tc_stage_b1(land, B1, S, LW, OFF, ip.lo, ip.hi, ip.lo + (ip.hi - ip.lo + 1) / 2);
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive1(&bars[7]);
         epi_sync();   // landing zone free
-        const int tn = t + gridDim.x;
+        tn = t + gridDim.x;
         if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty, row_lo), land, &bars[0], images, s, &tmap, use_tmap, P);
-        // ---- DoG of the previous tile's last level (before this level's column pass
-        // overwrites D2[g & 1] = its L_{n-1}); its output is written after the split below,
-        // off the tensor pipe's critical path (level 0 has no DoG, so v/argmax stay put
-        // until the consume of level 1 at iteration g + 2)
-        if (g > 0) {
-          mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
-          umma::fence_after();
-          consume(g - 1);
-          wt = ot;
-          wdeg = odeg;
-          pending = true;
-        }
-        ot = tt;
-        oinv = ip.inv * (1.f / kTcWScale);
-        odeg = ip.degen;
-        if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty, row_lo); }
-      } else {
+      }
+      // ---- DoG of level g-1.  At level 0 that is the previous tile's last level; it runs
+      // before this level's column pass overwrites D2[g & 1] (= its L_{n-1}), and the
+      // tile's output is written after the split below, off the tensor pipe's critical
+      // path (level 0 has no DoG, so v / argmax stay put until iteration g + 2)
+      if (g > 0) {
         mbar_wait(&bars[2], (uint32_t)((g - 1) & 1));
         umma::fence_after();
         TC_STAMP(g, 9);
         consume(g - 1);
       }
+      if (lev == 0) {
+        if (g > 0) {
+          wt = ot;
+          wdeg = odeg;
+          pending = true;
+        }
+        if (!last) {
+          ot = tt;
+          oinv = ip.inv * (1.f / kTcWScale);
+          odeg = ip.degen;
+          if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty, row_lo); }
+        }
+      }
       TC_STAMP(g, 10);
-      // ---- split D1 -> A2 group by group (chunk 4 grp + wg of this warp's lane quarter)
-      const int nj = P.lev[lev].K / 16;
-      mbar_wait(&bars[1], par_g);
-      umma::fence_after();
-      TC_STAMP(g, 11);
-      for (int grp = 0; 4 * grp < nj; ++grp) {
-        const int j = 4 * grp + wg;
-        if (j < nj) tc_split_chunk(tq, j);
-        umma::wait_st();
-        umma::fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive1(&bars[3 + grp]);
-        TC_STAMP(g, 12 + grp);
+      if (!last) {
+        // ---- split D1 -> A2 group by group (chunk 4 grp + wg of this warp's lane quarter)
+        const int nj = P.lev[lev].K / 16;
+        mbar_wait(&bars[1], par_g);
+        umma::fence_after();
+        TC_STAMP(g, 11);
+        for (int grp = 0; 4 * grp < nj; ++grp) {
+          const int j = 4 * grp + wg;
+          if (j < nj) tc_split_chunk(tq, j);
+          umma::wait_st();
+          umma::fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive1(&bars[3 + grp]);
+          TC_STAMP(g, 12 + grp);
+        }
       }
       if (lev == 0) {
         if (pending) write_out(wt, wdeg);
@@ -446,10 +466,6 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         for (int u = 0; u < 8; ++u) ibest[u] = 0u;
       }
     }
-    mbar_wait(&bars[2], (uint32_t)((G - 1) & 1));
-    umma::fence_after();
-    consume(G - 1);
-    write_out(ot, odeg);
   }
   umma::fence_before();
   __syncthreads();

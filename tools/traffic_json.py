@@ -37,8 +37,8 @@ for vals in rows[2:]:
         k = "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
         if k in d:
             res["tensor_active_pct"] = float(d[k])
-        res["duration_ms"] = num(d, u, "gpu__time_duration.sum") / 1e6 if u["gpu__time_duration.sum"] == "nsecond" \
-            else float(d["gpu__time_duration.sum"])
+        tsc = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
+        res["duration_ms"] = float(d["gpu__time_duration.sum"].replace(",", "")) * tsc[u["gpu__time_duration.sum"]]
 res["step_dram_bytes_per_image"] = step / images
 res["per_kernel_dram_bytes_per_image"] = {k: v / images for k, v in per_kernel.items()}
 print(json.dumps(res, indent=1))
