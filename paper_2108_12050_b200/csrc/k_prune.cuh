@@ -12,8 +12,12 @@
 // is final and equals the sequential one (induction on priority), and the highest-
 // priority undecided blob always decides, so the rounds terminate (<= 10
 // rounds on EM tiles).  One cooperative launch runs all rounds for the whole batch,
-// separated by grid-wide barriers; candidates are looked up through a per-row index
-// of the raster-sorted candidate list.
+// separated by grid-wide barriers.  Neighbours are found through a cell index: the
+// image is cut into bands of cs rows (cs = a power of two >= every search radius) and
+// each band's candidates (a contiguous range of the raster-sorted list) are counting-
+// sorted by their cs-wide column cell into `crec`; the 3 x 3 cells around a blob are then
+// three contiguous record ranges (cells cx-1..cx+1 of bands yb-1..yb+1), found with six
+// independent index loads instead of a chain of ~2 Dm dependent per-row lookups.
 //
 // Score: DOF = |C| after pruning.  The kept list is emitted in
 // (y, x, scale) order by a chunked scan (no atomics decide positions).
@@ -25,6 +29,10 @@
 namespace mhfd {
 
 namespace cg = cooperative_groups;
+
+#ifndef PRUNE_STAMPS
+#define PRUNE_STAMPS 0   // performance experiments: globaltimer after each grid barrier -> counters[16..],
+#endif                   // records scanned -> counters[8]
 
 constexpr uint8_t kUndecided = 0, kKept = 1, kRemoved = 2;
 constexpr int kChunk = 256;
@@ -43,8 +51,10 @@ struct PruneArgs {
   int n;                    // DoG planes
   uint8_t* st;              // B x cap
   int32_t* rowstart;        // B x (H + 1): first candidate of each row
-  int32_t* rbi;             // B x H x (nbx + 1): first candidate of row y with x >= 32 k
-  int nbx;                  // ceil(W / 32)
+  int cs_shift;             // cell edge cs = 1 << cs_shift (>= every dmax)
+  int ncx, nbands;          // ceil(W / cs) cells per band, ceil(H / cs) bands
+  int32_t* cellstart;       // B x nbands x (ncx + 1): first crec index of cell (band, cx)
+  int4* crec;               // B x cap: {x, y, scale, k} per candidate, band-major, cell-sorted
   int64_t* img_off;         // B + 1: prefix of effective candidate counts
   int64_t* chunk_off;       // B + 1: prefix of chunk counts
   int32_t* chunk_cnt;       // kept per chunk
@@ -85,50 +95,74 @@ __device__ __forceinline__ int image_of(const int64_t* off, int B, int64_t g) {
 
 constexpr int kNbMax = 6;   // neighbour indices kept per worklist record
 
+constexpr int kMaxCells = 2048;   // ncx + 1 per band (shared-memory counting sort)
+
 // Scan the candidates around blob k for higher-priority blobs that overlap it by more
-// than `overlap`; rows ylo + r0, ylo + r0 + rstep, ...  Returns true as soon as one of
-// them is KEPT (k is then REMOVED); otherwise sets *blocked if one is UNDECIDED and
-// passes every overlapping one to rec(q).
+// than `overlap`: the records of cells cx-1..cx+1 in bands yb-1..yb+1 (three contiguous
+// ranges), entries i0, i0 + istep, ... of each.  Returns true as soon as one of them is
+// KEPT (k is then REMOVED); otherwise sets *blocked if one is UNDECIDED and passes every
+// overlapping one to rec(q).
+// R: the image's cell-ordered records, or a shared-memory copy of a band window offset so
+// that R[i] is record i (k_prune round 0)
 template <class Rec>
-__device__ __forceinline__ bool scan_rows(const PruneArgs& a, int b, int64_t k, int r0, int rstep, bool* blocked,
-                                          Rec rec) {
-  const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+__device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4 me4, const int4* R0p, const int4* R1p,
+                                           const int4* R2p, int i0, int istep, bool* blocked, Rec rec) {
   const uint8_t* st = a.st + (int64_t)b * a.cap;
-  const mhfd_blob me = C[k];
+  struct { int x, y, scale; } me = {me4.x, me4.y, me4.z};
+  const int64_t k = me4.w;
   const double r = a.rad[me.scale];
   const int Dm = a.dmax[me.scale];
   const float2* th = a.thr + me.scale * a.n;
-  const int ylo = max(0, me.y - Dm), yhi = min(a.H - 1, me.y + Dm);
-  const int kb0 = max(0, me.x - Dm) >> 5, kb1 = min(a.nbx, ((me.x + Dm) >> 5) + 1);
-  const int32_t* ri = a.rbi + (int64_t)b * a.H * (a.nbx + 1);
-  for (int yy = ylo + r0; yy <= yhi; yy += rstep) {
-    const int32_t* rrow = ri + (int64_t)yy * (a.nbx + 1);
-    const int lo = __ldcg(rrow + kb0), hi = __ldcg(rrow + kb1);
-    for (int q = lo; q < hi; ++q) {
-      const mhfd_blob o = C[q];
-      if (o.x > me.x + Dm) break;
-      if (o.x < me.x - Dm) continue;
-      if (q == k) continue;
-      const bool higher = o.scale > me.scale ||
-                          (o.scale == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
+  const int yb = me.y >> a.cs_shift, cx = me.x >> a.cs_shift;
+  const int b0 = max(0, yb - 1), b1 = min(a.nbands - 1, yb + 1);
+  const int c0 = max(0, cx - 1), c1 = min(a.ncx, cx + 2);
+  const int32_t* cst = a.cellstart + (int64_t)b * a.nbands * (a.ncx + 1);
+  int lo[3], hi[3];
+  // cst and R were written in phase 1b of this launch and are read-only since: plain
+  // (L1-cached) loads are coherent here (no SM cached these lines before the barrier,
+  // and L1 starts empty at launch), and neighbouring blobs share most of their windows
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {   // six independent loads
+    const int bb = min(b0 + j, b1);
+    lo[j] = cst[(int64_t)bb * (a.ncx + 1) + c0];
+    hi[j] = b0 + j <= b1 ? cst[(int64_t)bb * (a.ncx + 1) + c1] : lo[j];
+  }
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    const int4* R = j == 0 ? R0p : j == 1 ? R1p : R2p;   // records of band b0 + j
+    if (PRUNE_STAMPS && hi[j] > lo[j] + i0) atomicAdd(&a.counters[8], (hi[j] - lo[j] - i0 + istep - 1) / istep);
+#pragma unroll 4
+    for (int i = lo[j] + i0; i < hi[j]; i += istep) {
+      const int4 o = R[i];   // {x, y, scale, k}
+      const int dx = o.x - me.x, dy = o.y - me.y;
+      if (dx > Dm || dx < -Dm || dy > Dm || dy < -Dm) continue;
+      if (o.w == k) continue;
+      const bool higher = o.z > me.scale || (o.z == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
       if (!higher) continue;
       // frac(d) > overlap, frac decreasing in d: d^2 < lo -> yes, d^2 >= hi -> no, else
       // evaluate the lens formula (the band is 1e-6 relative around the bisected root)
-      const int dx = o.x - me.x, dy = o.y - me.y;
       const float d2 = (float)(dx * dx + dy * dy);
-      const float2 t2 = __ldg(th + o.scale);
+      const float2 t2 = __ldg(th + o.z);
       const bool over = d2 < t2.x ? true
                         : d2 >= t2.y ? false
-                                     : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.scale]) > a.overlap;
+                                     : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.z]) > a.overlap;
       if (over) {
-        const uint8_t s = __ldcg(st + q);
+        const uint8_t s = __ldcg(st + o.w);
         if (s == kKept) return true;
         if (s == kUndecided) *blocked = true;
-        rec(q);
+        rec(o.w);
       }
     }
   }
   return false;
+}
+
+template <class Rec>
+__device__ __forceinline__ bool scan_rows(const PruneArgs& a, int b, int64_t k, int i0, int istep, bool* blocked,
+                                          Rec rec) {
+  const mhfd_blob m = a.cand[(int64_t)b * a.cap + k];
+  const int4* R = a.crec + (int64_t)b * a.cap;
+  return scan_cells(a, b, make_int4(m.x, m.y, m.scale, (int)k), R, R, R, i0, istep, blocked, rec);
 }
 
 __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
@@ -169,6 +203,16 @@ __device__ uint8_t decide_list(const PruneArgs& a, int b, const int4& r0, const 
 
 __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   cg::grid_group grid = cg::this_grid();
+  int pst_ = 0;
+  auto PSTAMP = [&]() {
+    if (PRUNE_STAMPS && blockIdx.x == 0 && threadIdx.x == 0 && pst_ < 24) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      reinterpret_cast<unsigned long long*>(a.counters + 16)[pst_] = t_;
+    }
+    ++pst_;
+  };
+  PSTAMP();
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
   __shared__ int32_t red[8];
@@ -189,15 +233,16 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     a.counters[0] = a.counters[1] = a.counters[2] = 0;
     a.counters[3] = 0;
     a.counters[4] = 0;
+    if (PRUNE_STAMPS) a.counters[8] = 0;
   }
   grid.sync();
+  PSTAMP();
   const int64_t total = a.img_off[a.B];
   const int64_t nchunks = a.chunk_off[a.B];
 
-  // phase 1: row index rowstart[b][y] (first candidate of row >= y) and row-block index
-  // rbi[b][y][k] (first candidate of row y with x >= 32 k; k = nbx -> row end), both by
-  // scatter from the raster-sorted list: candidate k (and a sentinel k = n at row H)
-  // owns the entries between its predecessor and itself, so each entry is written once.
+  // phase 1: row index rowstart[b][y] (first candidate of row >= y), by scatter from the
+  // raster-sorted list: candidate k (and a sentinel k = n at row H) owns the entries
+  // between its predecessor's row and its own, so each entry is written once.
   for (int64_t g = gtid; g < total + a.B; g += gsize) {
     // g enumerates, per image, candidates 0..n (n = sentinel): image b holds entries
     // [img_off[b] + b, img_off[b+1] + b + 1)
@@ -210,25 +255,60 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     const int64_t k = g - a.img_off[b] - b;
     const int64_t n = a.img_off[b + 1] - a.img_off[b];
     const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
-    int y, x, yp, xp;
-    if (k < n) { const mhfd_blob m = C[k]; y = m.y; x = m.x; } else { y = a.H; x = 0; }
-    if (k > 0) { const mhfd_blob m = C[k - 1]; yp = m.y; xp = m.x; } else { yp = -1; xp = 0; }
+    const int y = k < n ? C[k].y : a.H, yp = k > 0 ? C[k - 1].y : -1;
     int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
     for (int yy = yp + 1; yy <= y; ++yy) rs[yy] = (int32_t)k;
     if (k < n) a.st[(int64_t)b * a.cap + k] = a.prune ? kUndecided : kKept;
-    if (!a.prune) continue;
-    int32_t* ri = a.rbi + (int64_t)b * a.H * (a.nbx + 1);
-    if (yp >= 0 && yp < y) {   // predecessor ends its row: its trailing blocks point past it
-      for (int kb = (xp >> 5) + 1; kb <= a.nbx; ++kb) ri[(int64_t)yp * (a.nbx + 1) + kb] = (int32_t)k;
-    }
-    for (int yy = yp + 1; yy < y && yy < a.H; ++yy)   // empty rows in between
-      for (int kb = 0; kb <= a.nbx; ++kb) ri[(int64_t)yy * (a.nbx + 1) + kb] = (int32_t)k;
-    if (k < n) {   // blocks of row y whose first candidate is k
-      const int kb0 = (yp == y) ? (xp >> 5) + 1 : 0;
-      for (int kb = kb0; kb <= (x >> 5); ++kb) ri[(int64_t)y * (a.nbx + 1) + kb] = (int32_t)k;
-    }
   }
   grid.sync();
+  PSTAMP();
+
+  // phase 1b: cell index.  Band (b, j) = rows [j cs, (j+1) cs) = the contiguous range
+  // [rowstart[j cs], rowstart[(j+1) cs]) of the raster list; one CTA counting-sorts it by
+  // column cell in shared memory (order inside a cell is irrelevant: decisions do not
+  // depend on it) and writes the cell starts and the cell-ordered records.
+  if (a.prune) {
+    __shared__ int32_t cell[kMaxCells];
+    const int cs = 1 << a.cs_shift;
+    for (int64_t item = blockIdx.x; item < (int64_t)a.B * a.nbands; item += gridDim.x) {
+      const int b = (int)(item / a.nbands), j = (int)(item % a.nbands);
+      const int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
+      const int k0 = rs[j * cs], k1 = rs[min(a.H, (j + 1) * cs)];
+      const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cell[c] = 0;
+      __syncthreads();
+      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&cell[C[k].x >> a.cs_shift], 1);
+      __syncthreads();
+      if (threadIdx.x < 32) {   // exclusive scan of ncx + 1 counts by one warp
+        int carry = 0;
+        for (int c0 = 0; c0 <= a.ncx; c0 += 32) {
+          const int c = c0 + threadIdx.x;
+          const int v = c <= a.ncx ? cell[c] : 0;
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)threadIdx.x >= o) x += t;
+          }
+          if (c <= a.ncx) cell[c] = k0 + carry + x - v;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      __syncthreads();
+      int32_t* cst = a.cellstart + ((int64_t)b * a.nbands + j) * (a.ncx + 1);
+      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cst[c] = cell[c];
+      __syncthreads();
+      int4* R = a.crec + (int64_t)b * a.cap;
+      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const mhfd_blob m = C[k];
+        const int pos = atomicAdd(&cell[m.x >> a.cs_shift], 1);
+        R[pos] = make_int4(m.x, m.y, m.scale, k);
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    PSTAMP();
+  }
 
   // phase 2: decision rounds.  Round 0 visits every blob; a blob it leaves UNDECIDED is
   // appended to the worklist with its overlapping higher-priority neighbours, and later
@@ -237,61 +317,102 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   // tile) run round 0 one warp per blob, the rows of its search window split over the
   // lanes: the serial chain of dependent row-index loads, not throughput, bounds them.
   if (a.prune) {
-    const int64_t gw = gtid >> 5, nwarps = gsize >> 5;
     const int lane0 = threadIdx.x & 31;
     int undecided = 0;
     if (gtid == 0) a.counters[1] = 0;
-    auto append = [&](int64_t g, int nq, const int (&qs)[kNbMax]) -> bool {
-      const int pos = atomicAdd(&a.counters[4], 1);
-      if (pos >= a.wl_cap) return false;
-      a.wl[2 * pos] = make_int4((int)g, nq > kNbMax ? kNbMax + 1 : nq, qs[0], qs[1]);
-      a.wl[2 * pos + 1] = make_int4(qs[2], qs[3], qs[4], qs[5]);
-      return true;
-    };
-    if (total * 32 <= gsize * 4) {   // warp per blob
-      __shared__ int wq[8][kNbMax + 1];
-      const int wib = threadIdx.x >> 5;
-      for (int64_t g = gw; g < total; g += nwarps) {
-        const int b = image_of(a.img_off, a.B, g);
-        const int64_t k = g - a.img_off[b];
-        if (lane0 == 0) wq[wib][kNbMax] = 0;
+    // Round 0.  Lanes per blob: enough groups of G lanes to give every thread about one
+    // blob-share (1 for batches: many blobs per thread average the per-blob cost out; a
+    // single tile has ~1 blob per thread, and the round lasts as long as the slowest
+    // thread's window scan).  Measured alternative that lost: each CTA copying a band
+    // piece's window into shared memory and scanning it there.
+    int G = 1;
+    while (G < 32 && total * G < gsize * 4) G <<= 1;
+    if (G > 1) {   // a group of G lanes per blob, striding over its window's records
+      __shared__ int wq[8][32][kNbMax + 1];
+      const int wib = threadIdx.x >> 5, grp = lane0 / G, gl = lane0 & (G - 1);
+      const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
+      for (int64_t gb = (gtid - lane0) / G; gb < total; gb += gsize / G) {
+        const int64_t g = gb + grp;
+        const bool in = g < total;
+        int b = 0;
+        int64_t k = 0;
+        if (gl == 0) wq[wib][grp][kNbMax] = 0;
         __syncwarp();
-        bool blocked = false;
-        const bool rem = scan_rows(a, b, k, lane0, 32, &blocked, [&](int q) {
-          const int pos = atomicAdd(&wq[wib][kNbMax], 1);
-          if (pos < kNbMax) wq[wib][pos] = q;
-        });
-        const bool any_rem = __any_sync(0xffffffffu, rem);
-        const bool any_blk = __any_sync(0xffffffffu, blocked);
+        bool blocked = false, rem = false;
+        if (in) {
+          b = image_of(a.img_off, a.B, g);
+          k = g - a.img_off[b];
+          rem = scan_rows(a, b, k, gl, G, &blocked, [&](int q) {
+            const int pos = atomicAdd(&wq[wib][grp][kNbMax], 1);
+            if (pos < kNbMax) wq[wib][grp][pos] = q;
+          });
+        }
+        const bool any_rem = (__ballot_sync(0xffffffffu, rem) & gmask) != 0;
+        const bool any_blk = (__ballot_sync(0xffffffffu, blocked) & gmask) != 0;
         __syncwarp();
-        if (lane0 == 0) {
-          uint8_t d = any_rem ? kRemoved : any_blk ? kUndecided : kKept;
-          if (d == kUndecided) {
-            int qs[kNbMax];
-            for (int i = 0; i < kNbMax; ++i) qs[i] = wq[wib][i];
+        const bool lead = in && gl == 0;
+        const uint8_t d = any_rem ? kRemoved : any_blk ? kUndecided : kKept;
+        if (lead && d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
+        const uint32_t m = __ballot_sync(0xffffffffu, lead && d == kUndecided);
+        if (m) {   // one worklist atomic per warp
+          int base = 0;
+          if (lane0 == __ffs(m) - 1) base = atomicAdd(&a.counters[4], __popc(m));
+          base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+          if (lead && d == kUndecided) {
             ++undecided;
-            append(g, wq[wib][kNbMax], qs);
+            const int pos = base + __popc(m & ((1u << lane0) - 1u));
+            const int* w = wq[wib][grp];
+            if (pos < a.wl_cap) {
+              a.wl[2 * pos] = make_int4((int)g, w[kNbMax] > kNbMax ? kNbMax + 1 : w[kNbMax], w[0], w[1]);
+              a.wl[2 * pos + 1] = make_int4(w[2], w[3], w[4], w[5]);
+            }
           }
-          if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
         }
         __syncwarp();
       }
     } else {
-      for (int64_t g = gtid; g < total; g += gsize) {
-        const int b = image_of(a.img_off, a.B, g);
-        const int64_t k = g - a.img_off[b];
+      // every lane of a warp runs the same number of iterations (gsize is a multiple of
+      // 32), so the worklist slots are claimed with one atomic per warp and iteration: a
+      // per-blob atomic on the one counter serialised ~10^5 appends
+      for (int64_t g0 = gtid - lane0; g0 < total; g0 += gsize) {
+        const int64_t g = g0 + lane0;
+        const bool in = g < total;
+        int b = 0;
+        int64_t k = 0;
         int nq = 0, qs[kNbMax] = {0, 0, 0, 0, 0, 0};
-        const uint8_t d = decide_collect(a, b, k, &nq, qs);
-        if (d != kUndecided) {
-          __stcg(a.st + (int64_t)b * a.cap + k, d);
-        } else {
-          ++undecided;
-          append(g, nq, qs);
+        uint8_t d = kKept;
+        if (in) {
+          b = image_of(a.img_off, a.B, g);
+          k = g - a.img_off[b];
+          d = decide_collect(a, b, k, &nq, qs);
+          if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
+        }
+        const bool und = in && d == kUndecided;
+        const uint32_t m = __ballot_sync(0xffffffffu, und);
+        if (m) {
+          int base = 0;
+          if (lane0 == __ffs(m) - 1) base = atomicAdd(&a.counters[4], __popc(m));
+          base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+          if (und) {
+            ++undecided;
+            const int pos = base + __popc(m & ((1u << lane0) - 1u));
+            if (pos < a.wl_cap) {
+              a.wl[2 * pos] = make_int4((int)g, nq > kNbMax ? kNbMax + 1 : nq, qs[0], qs[1]);
+              a.wl[2 * pos + 1] = make_int4(qs[2], qs[3], qs[4], qs[5]);
+            }
+          }
         }
       }
     }
     if (undecided) atomicAdd(&a.counters[0], undecided);
+    if (PRUNE_STAMPS) {   // per-CTA end of round-0 work (globaltimer, low 32 bits) -> the worklist's tail
+      __syncthreads();
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      if (threadIdx.x == 0) reinterpret_cast<int32_t*>(a.wl + 2 * (a.wl_cap - 1024))[blockIdx.x] = (int32_t)(uint32_t)t_;
+    }
     grid.sync();
+    PSTAMP();
     int left = *((volatile int32_t*)&a.counters[0]);
     const int64_t nwl = *((volatile int32_t*)&a.counters[4]);
     const bool full = nwl > a.wl_cap;   // some undecided blob is not on the list
@@ -322,11 +443,13 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
       }
       if (undecided) atomicAdd(&a.counters[round % 3], undecided);
       grid.sync();
+      PSTAMP();
       left = *((volatile int32_t*)&a.counters[round % 3]);
       if (gtid == 0) a.counters[3] = round + 1;
     }
   }
   grid.sync();
+  PSTAMP();
 
   // phase 3: kept count per chunk of 256 candidates
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -346,6 +469,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     __syncthreads();
   }
   grid.sync();
+  PSTAMP();
 
   // phase 4: per-image exclusive scan over chunks (one warp per image)
   {
@@ -377,6 +501,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   }
   if (!a.blobs) return;
   grid.sync();
+  PSTAMP();
 
   // phase 5: write kept blobs in (y, x, scale) order
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {

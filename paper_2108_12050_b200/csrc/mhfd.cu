@@ -56,6 +56,7 @@ struct mhfd_ctx {
   uint8_t* d_tc2tab; // its device pair tables (context-owned, immutable)
   float2* d_thr;     // pruning: n x n squared-distance bands (context-owned, immutable)
   int32_t dmax[kMaxLevels];
+  int cs_shift, ncx, nbands;   // pruning cell index: cell edge 1 << cs_shift >= every dmax
   // bench instrumentation (mhfd_timing_*): 5 events per recorded call
   cudaEvent_t* tev;
   int tmax, tcount;
@@ -89,7 +90,7 @@ mhfd_status cuda_fail(cudaError_t e, const char* where) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, rbi, imgoff, chunkoff,
+  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, cellstart, crec, imgoff, chunkoff,
       chunkcnt, chunkpos, counters, scores, counts, rx, xtc, slab, wl, total;
 };
 
@@ -148,12 +149,13 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.cand = take(sizeof(mhfd_blob) * c->cap * B);
   L.st = take(c->cap * B);
   L.rowstart = take(sizeof(int32_t) * (c->p.height + 1) * (size_t)B);
-  L.rbi = take(sizeof(int32_t) * (size_t)c->p.height * ((c->p.width + 31) / 32 + 1) * (size_t)B);
+  L.cellstart = take(sizeof(int32_t) * (size_t)c->nbands * (c->ncx + 1) * (size_t)B);   // pruning cell index
+  L.crec = take(sizeof(int4) * c->cap * (size_t)B);
   L.imgoff = take(sizeof(int64_t) * (B + 1));
   L.chunkoff = take(sizeof(int64_t) * (B + 1));
   L.chunkcnt = take(sizeof(int32_t) * nchunk * B);
   L.chunkpos = take(sizeof(int32_t) * nchunk * B);
-  L.counters = take(sizeof(int32_t) * 8);
+  L.counters = take(sizeof(int32_t) * 64);   // 8 counters; [16, 64): k_prune phase stamps (PRUNE_STAMPS builds)
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
   // two-pass schedules: Rx of every level (LoG: of each of the 2n sub-levels) for up to
@@ -644,8 +646,11 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   pa.n = c->n;
   pa.st = reinterpret_cast<uint8_t*>(ws + L.st);
   pa.rowstart = reinterpret_cast<int32_t*>(ws + L.rowstart);
-  pa.rbi = reinterpret_cast<int32_t*>(ws + L.rbi);
-  pa.nbx = (c->p.width + 31) / 32;
+  pa.cs_shift = c->cs_shift;
+  pa.ncx = c->ncx;
+  pa.nbands = c->nbands;
+  pa.cellstart = reinterpret_cast<int32_t*>(ws + L.cellstart);
+  pa.crec = reinterpret_cast<int4*>(ws + L.crec);
   pa.img_off = reinterpret_cast<int64_t*>(ws + L.imgoff);
   pa.chunk_off = reinterpret_cast<int64_t*>(ws + L.chunkoff);
   pa.chunk_cnt = reinterpret_cast<int32_t*>(ws + L.chunkcnt);
@@ -669,6 +674,25 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
     cudaMemcpyAsync(&tot, pa.img_off + B, sizeof(tot), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "mhfd prune: %lld candidates, %d rounds\n", (long long)tot, r);
+    unsigned long long ts[24] = {0};
+    cudaMemcpyAsync(ts, pa.counters + 16, sizeof(ts), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (ts[0]) {
+      int32_t nrec = 0;
+      cudaMemcpy(&nrec, pa.counters + 8, sizeof(nrec), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "mhfd prune: %d records scanned in all rounds\n", nrec);
+      std::vector<uint32_t> ce(c->prune_grid);
+      cudaMemcpy(ce.data(), pa.wl + 2 * (pa.wl_cap - 1024), 4 * ce.size(), cudaMemcpyDeviceToHost);
+      std::vector<double> us;
+      for (uint32_t v : ce) us.push_back((double)(uint32_t)(v - (uint32_t)ts[0]) / 1000.0);
+      std::sort(us.begin(), us.end());
+      fprintf(stderr, "mhfd prune: round-0 work end per CTA (us): min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f\n", us[0],
+              us[us.size() / 10], us[us.size() / 2], us[us.size() * 9 / 10], us.back());
+      fprintf(stderr, "mhfd prune phase stamps (us from start):");
+      for (int i = 1; i < 12 && ts[i] >= ts[0] && ts[i] - ts[0] < 100000000ull; ++i)
+        fprintf(stderr, " %.1f", (ts[i] - ts[0]) / 1000.0);
+      fprintf(stderr, "\n");
+    }
   }
   MARK(4);
   return MHFD_OK;
@@ -997,6 +1021,15 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
       return fail(MHFD_ERR_CUDA, "pruning threshold table upload failed");
     }
     cudaSetDevice(prev);
+  }
+  {   // cell edge: a power of two >= every search radius, and few enough cells per band
+    int dm = 8;
+    for (int s = 0; s < n; ++s) dm = std::max(dm, (int)c->dmax[s]);
+    int sh = 3;
+    while ((1 << sh) < dm || (p->width + (1 << sh) - 1) / (1 << sh) + 1 > kMaxCells) ++sh;
+    c->cs_shift = sh;
+    c->ncx = (p->width + (1 << sh) - 1) >> sh;
+    c->nbands = (p->height + (1 << sh) - 1) >> sh;
   }
   const int64_t half = (int64_t)((p->width + 1) / 2) * ((p->height + 1) / 2);
   c->cap = p->max_candidates > 0 ? p->max_candidates : (p->nms == MHFD_NMS_PAPER ? half : half * n);
