@@ -134,43 +134,46 @@ __global__ void __launch_bounds__(256) k_nms_count(NmsArgs a, int nseg, int32_t*
   if (lane == 0) segcnt[(int64_t)b * nseg + seg] = cnt;
 }
 
-// One CTA (1024 threads) per image: exclusive scan of the segment counts.
+// One CTA (1024 threads) per image: exclusive scan of the segment counts.  Each thread
+// owns a contiguous run of ceil(nseg / 1024) counts: one read pass, a thread-local scan,
+// one block-wide scan of the 1024 run totals, one write pass (a 1024-wide loop with four
+// barriers per 1024 segments took 17 us for the 16384 segments of one 4096^2 tile).
 __global__ void __launch_bounds__(1024) k_seg_scan(const int32_t* __restrict__ segcnt, int nseg,
                                                    int32_t* __restrict__ segoff, int32_t* __restrict__ ncand) {
   __shared__ int32_t wsum[32];
-  __shared__ int32_t carry;
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
+  const int per = (nseg + 1023) / 1024;
+  const int i0 = min(nseg, (int)threadIdx.x * per), i1 = min(nseg, i0 + per);
+  const int32_t* sc = segcnt + (int64_t)b * nseg;
+  int32_t* so = segoff + (int64_t)b * nseg;
+  int run = 0;
+  for (int i = i0; i < i1; ++i) run += sc[i];
+  int x = run;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
   __syncthreads();
-  for (int base = 0; base < nseg; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int v = (i < nseg) ? segcnt[(int64_t)b * nseg + i] : 0;
-    int x = v;
+  if (warp == 0) {
+    int s = wsum[lane];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
+      const int y = __shfl_up_sync(0xffffffffu, s, off);
+      if (lane >= off) s += y;
     }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int s = wsum[lane];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, s, off);
-        if (lane >= off) s += y;
-      }
-      wsum[lane] = s;
-    }
-    __syncthreads();
-    const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
-    if (i < nseg) segoff[(int64_t)b * nseg + i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
+    wsum[lane] = s;
   }
-  if (threadIdx.x == 0) ncand[b] = carry;
+  __syncthreads();
+  int excl = (warp ? wsum[warp - 1] : 0) + x - run;
+  for (int i = i0; i < i1; ++i) {
+    const int v = sc[i];
+    so[i] = excl;
+    excl += v;
+  }
+  if (threadIdx.x == 1023) ncand[b] = wsum[31];
 }
 
 template <int MODE>
@@ -230,7 +233,8 @@ namespace mhfd {
 // segment bookkeeping as k_nms_count / k_nms_write.
 constexpr int kNmsRows = 2;   // output rows per warp in k_nms_rows (4: 2.98 ms, 2: 2.77 ms per 64 images)
 
-constexpr int kSlab = 32;    // records a segment parks in its slab during the count pass
+constexpr int kSlab = 64;    // records a segment parks in its slab during the count pass (32 -> 64: a sharp
+                             // 4096^2 tile had enough overflowing segments to make the gather's re-evaluation 60 us)
 
 template <bool WRITE>
 __global__ void __launch_bounds__(256, 4) k_nms_rows(NmsArgs a, int nseg, int32_t* __restrict__ segcnt,
@@ -501,7 +505,8 @@ __global__ void __launch_bounds__(256) k_nms_gather(NmsArgs a, int nseg, const i
   int64_t off = segoff[(int64_t)b * nseg + seg];
   mhfd_blob* out = cand + (int64_t)b * cap;
   if (cnt <= kSlab) {
-    if (lane < cnt && off + lane < cap) out[off + lane] = slab[((int64_t)b * nseg + seg) * kSlab + lane];
+    for (int r = lane; r < cnt; r += 32)
+      if (off + r < cap) out[off + r] = slab[((int64_t)b * nseg + seg) * kSlab + r];
     return;
   }
   const int64_t plane = (int64_t)a.H * a.W;

@@ -254,11 +254,17 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   // k_nms_roll<8> is the default count pass (NMS stage 1.695 -> 1.551 ms per 64 tiles
   // against k_nms_rows; <4> 1.603); MHFD_NMS_ROLL=0/4/8 selects for A/B runs
   static const int roll = [] { const char* e = getenv("MHFD_NMS_ROLL"); return e ? atoi(e) : 8; }();
-  if (rows_fast && (roll == 8 || roll == 4)) {
-    const int nr = roll;
+  if (rows_fast && (roll == 8 || roll == 4 || roll == 2 || roll == 1)) {
+    // rows per warp: 8 when there is work for two waves of warp slots (3 CTAs x 8 warps per SM),
+    // fewer for small calls, where the warps' serial row walks set the latency (one
+    // 4096^2 tile: 256 CTAs of 8-row warps; one 1024^2 tile: 16)
+    int nr = roll;
+    while (nr > 1 && (int64_t)((row1 - row0 + nr - 1) / nr) * (W / kSeg) * B < (int64_t)c->sms * 48) nr >>= 1;
     const dim3 g8((((row1 - row0 + nr - 1) / nr) * (W / kSeg) + 7) / 8, B);
     if (nr == 8) k_nms_roll<8><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
-    else k_nms_roll<4><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
+    else if (nr == 4) k_nms_roll<4><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
+    else if (nr == 2) k_nms_roll<2><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
+    else k_nms_roll<1><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
   } else if (rows_fast) {
     k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1, slab);
   } else if (paper) {
