@@ -281,6 +281,32 @@ mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t
                                   size_t workspace_bytes, mhfd_blob* d_blobs, int32_t blob_capacity,
                                   int32_t* d_count, double* d_score, int32_t* d_flags, void* stream);
 
+/* Sharded pruning of one image ("border-blob exchange for pruning";
+ * the paper's gather bottleneck): instead of every rank pruning the
+ * gathered full list, rank r prunes only its band [y0, y1) from the candidates of an
+ * extended band [e0, e1) (mhfd_detect_band on the extended rows) and the ranks sum their
+ * counts (one all-reduce of 8 bytes).
+ *
+ * mhfd_prune_band: the pruning rule of mhfd_prune_candidates applied to the ncand
+ * raster-ordered candidates of rows [e0, e1) (0 <= e0 <= y0 < y1 <= e1 <= height), in
+ * synchronous rounds (a round's decisions read only the previous rounds' states, so a
+ * blob decided in round t depends only on the candidates within (t + 1) D of it, D =
+ * mhfd_interaction_radius).  d_count (1 int32) = kept blobs with y0 <= y < y1.  d_cert
+ * (1 int32) = 1 when every such blob was decided in a round t with (t + 1) D <= its
+ * distance to a truncated edge of [e0, e1) (e0 > 0 or e1 < height), i.e. when d_count is
+ * provably the whole image's count of kept blobs in [y0, y1); else 0, and the caller
+ * falls back to mhfd_prune_candidates on the gathered full list.  Errors: as
+ * mhfd_prune_candidates; SHAPE for the row ranges.  d_nband (nullable, 1 int32) = the
+ * candidates with y0 <= y < y1 (their sum over the bands is the image's candidate count,
+ * which the caller compares with max_candidates: mhfd_detect_batch truncates the list).
+ *
+ * mhfd_interaction_radius: D in pixels, the largest pruning search radius (a blob's
+ * decision can only involve candidates closer than D in one round); -1 if c is NULL. */
+mhfd_status mhfd_prune_band(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t ncand, int32_t e0, int32_t e1, int32_t y0,
+                            int32_t y1, void* d_workspace, size_t workspace_bytes, int32_t* d_count, int32_t* d_cert,
+                            int32_t* d_nband, void* stream);
+int32_t mhfd_interaction_radius(const mhfd_ctx* c);
+
 /* mhfd_downsample: the bilinear downsampling pre-step (PAPER.md:401
  * "preprocessing by downsampling, by bilinear interpolation, in order to satisfy GPU RAM
  * constraints"; SPEC.md:48-56 fixes the output shape ceil(W/f) x ceil(H/f) and factor 1 =

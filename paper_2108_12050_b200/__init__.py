@@ -230,6 +230,25 @@ class Detector:
                                                    self._stream()))
         return blobs, cnt, score, flags
 
+    def interaction_radius(self) -> int:
+        """Largest pruning search radius D in pixels (mhfd_interaction_radius)."""
+        return int(self._lib.mhfd_interaction_radius(self._h))
+
+    def prune_band(self, cands: torch.Tensor, ncand: int, e0: int, e1: int, y0: int, y1: int):
+        """Sharded pruning of one band (mhfd_prune_band): the candidates of rows [e0, e1)
+        (raster order) pruned in synchronous rounds -> 1-element int32 device tensors:
+        kept blobs with y in [y0, y1); certificate (1 = provably the whole image's count for
+        the band); candidates with y in [y0, y1)."""
+        ws = self._workspace(1)
+        cands = cands.contiguous()
+        cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+        cert = torch.empty(1, dtype=torch.int32, device=self.device)
+        nband = torch.empty(1, dtype=torch.int32, device=self.device)
+        _abi.check(self._lib.mhfd_prune_band(self._h, cands.data_ptr() if ncand > 0 else None, int(ncand), int(e0),
+                                             int(e1), int(y0), int(y1), self._ws_ptr(ws), ws.numel() - 256,
+                                             cnt.data_ptr(), cert.data_ptr(), nband.data_ptr(), self._stream()))
+        return cnt, cert, nband
+
     def timing_enable(self, max_calls: int) -> None:
         _abi.check(self._lib.mhfd_timing_enable(self._h, int(max_calls)))
 

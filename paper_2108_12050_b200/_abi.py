@@ -27,7 +27,7 @@ EXPORTS = ["mhfd_params_default", "mhfd_create", "mhfd_workspace_bytes", "mhfd_d
            "mhfd_destroy", "mhfd_status_string", "mhfd_last_error", "mhfd_abi_version",
            "mhfd_focus_score_host", "mhfd_timing_enable", "mhfd_timing_read", "mhfd_schedule_name",
            "mhfd_schedule_flops_per_pixel", "mhfd_detect_band", "mhfd_prune_candidates",
-           "mhfd_downsample"]
+           "mhfd_prune_band", "mhfd_interaction_radius", "mhfd_downsample"]
 
 
 class mhfd_params(ctypes.Structure):
@@ -78,6 +78,8 @@ def load() -> ctypes.CDLL:
             "mhfd_schedule_flops_per_pixel": (ctypes.c_double, [P, i32]),
             "mhfd_detect_band": (i32, [P, P, i32, i64, i32, i32, P, sz, P, i32, P, P]),
             "mhfd_prune_candidates": (i32, [P, P, i32, P, sz, P, i32, P, P, P, P]),
+            "mhfd_prune_band": (i32, [P, P, i32, i32, i32, i32, i32, P, sz, P, P, P, P]),
+            "mhfd_interaction_radius": (i32, [P]),
             "mhfd_downsample": (i32, [P, i32, i32, i32, i64, i32, P, i64, i32, P]),
         }
         for name, (res, args) in sig.items():

@@ -35,6 +35,19 @@ namespace cg = cooperative_groups;
 #endif                   // records scanned -> counters[8]
 
 constexpr uint8_t kUndecided = 0, kKept = 1, kRemoved = 2;
+
+// State byte: decision in bits 0-1, and in synchronous mode (PruneArgs::sync) the round
+// that decided it in bits 2-7 (saturating at 63).  Synchronous rounds (Jacobi instead of
+// the default Gauss-Seidel, where a blob may use a decision made earlier in the same
+// round) make a round-t decision a function of the candidates within (t + 1) dmax of the
+// blob only: the certificate of the sharded pruning (mhfd_prune_band) rests on that.
+__device__ __forceinline__ uint8_t st_vis(uint8_t s, int round, int sync) {
+  const uint8_t d = s & 3u;
+  return (sync && d != kUndecided && (int)(s >> 2) >= round) ? kUndecided : d;
+}
+__device__ __forceinline__ uint8_t st_enc(uint8_t d, int round, int sync) {
+  return sync ? (uint8_t)(d | (min(round, 63) << 2)) : d;
+}
 constexpr int kChunk = 256;
 
 struct PruneArgs {
@@ -44,6 +57,7 @@ struct PruneArgs {
   const int32_t* ncand;     // exact candidate counts
   double overlap;
   int prune;                // overlap < 1
+  int sync;                 // synchronous rounds (f2 sharded pruning): see st_vis
   double radmax;
   double rad[kMaxLevels];   // sqrt(2) * t_s
   int32_t dmax[kMaxLevels]; // search radius of a plane-s blob: ceil(sqrt(max_{s'>=s} thr_hi(s, s')))
@@ -106,7 +120,7 @@ constexpr int kMaxCells = 2048;   // ncx + 1 per band (shared-memory counting so
 // that R[i] is record i (k_prune round 0)
 template <class Rec>
 __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4 me4, const int4* R0p, const int4* R1p,
-                                           const int4* R2p, int i0, int istep, bool* blocked, Rec rec) {
+                                           const int4* R2p, int i0, int istep, bool* blocked, Rec rec, int round) {
   const uint8_t* st = a.st + (int64_t)b * a.cap;
   struct { int x, y, scale; } me = {me4.x, me4.y, me4.z};
   const int64_t k = me4.w;
@@ -147,7 +161,7 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
                         : d2 >= t2.y ? false
                                      : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.z]) > a.overlap;
       if (over) {
-        const uint8_t s = __ldcg(st + o.w);
+        const uint8_t s = st_vis(__ldcg(st + o.w), round, a.sync);
         if (s == kKept) return true;
         if (s == kUndecided) *blocked = true;
         rec(o.w);
@@ -159,15 +173,15 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
 
 template <class Rec>
 __device__ __forceinline__ bool scan_rows(const PruneArgs& a, int b, int64_t k, int i0, int istep, bool* blocked,
-                                          Rec rec) {
+                                          Rec rec, int round) {
   const mhfd_blob m = a.cand[(int64_t)b * a.cap + k];
   const int4* R = a.crec + (int64_t)b * a.cap;
-  return scan_cells(a, b, make_int4(m.x, m.y, m.scale, (int)k), R, R, R, i0, istep, blocked, rec);
+  return scan_cells(a, b, make_int4(m.x, m.y, m.scale, (int)k), R, R, R, i0, istep, blocked, rec, round);
 }
 
-__device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
+__device__ uint8_t decide(const PruneArgs& a, int b, int64_t k, int round) {
   bool blocked = false;
-  if (scan_rows(a, b, k, 0, 1, &blocked, [](int) {})) return kRemoved;
+  if (scan_rows(a, b, k, 0, 1, &blocked, [](int) {}, round)) return kRemoved;
   return blocked ? kUndecided : kKept;
 }
 
@@ -176,24 +190,27 @@ __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k) {
 __device__ uint8_t decide_collect(const PruneArgs& a, int b, int64_t k, int* nq, int (&qs)[kNbMax]) {
   bool blocked = false;
   int n = 0;
-  if (scan_rows(a, b, k, 0, 1, &blocked, [&](int q) {
-        if (n < kNbMax) qs[n] = q;
-        ++n;
-      }))
+  if (scan_rows(
+          a, b, k, 0, 1, &blocked,
+          [&](int q) {
+            if (n < kNbMax) qs[n] = q;
+            ++n;
+          },
+          0))
     return kRemoved;
   *nq = n;
   return blocked ? kUndecided : kKept;
 }
 
 // later rounds: the recorded neighbours decide (no geometric search)
-__device__ uint8_t decide_list(const PruneArgs& a, int b, const int4& r0, const int4& r1) {
+__device__ uint8_t decide_list(const PruneArgs& a, int b, const int4& r0, const int4& r1, int round) {
   const uint8_t* st = a.st + (int64_t)b * a.cap;
   const int q[kNbMax] = {r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
   bool blocked = false;
 #pragma unroll
   for (int i = 0; i < kNbMax; ++i) {
     if (i < r0.y) {
-      const uint8_t s = __ldcg(st + q[i]);
+      const uint8_t s = st_vis(__ldcg(st + q[i]), round, a.sync);
       if (s == kKept) return kRemoved;
       if (s == kUndecided) blocked = true;
     }
@@ -342,17 +359,20 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         if (in) {
           b = image_of(a.img_off, a.B, g);
           k = g - a.img_off[b];
-          rem = scan_rows(a, b, k, gl, G, &blocked, [&](int q) {
-            const int pos = atomicAdd(&wq[wib][grp][kNbMax], 1);
-            if (pos < kNbMax) wq[wib][grp][pos] = q;
-          });
+          rem = scan_rows(
+              a, b, k, gl, G, &blocked,
+              [&](int q) {
+                const int pos = atomicAdd(&wq[wib][grp][kNbMax], 1);
+                if (pos < kNbMax) wq[wib][grp][pos] = q;
+              },
+              0);
         }
         const bool any_rem = (__ballot_sync(0xffffffffu, rem) & gmask) != 0;
         const bool any_blk = (__ballot_sync(0xffffffffu, blocked) & gmask) != 0;
         __syncwarp();
         const bool lead = in && gl == 0;
         const uint8_t d = any_rem ? kRemoved : any_blk ? kUndecided : kKept;
-        if (lead && d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
+        if (lead && d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, st_enc(d, 0, a.sync));
         const uint32_t m = __ballot_sync(0xffffffffu, lead && d == kUndecided);
         if (m) {   // one worklist atomic per warp
           int base = 0;
@@ -385,7 +405,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
           b = image_of(a.img_off, a.B, g);
           k = g - a.img_off[b];
           d = decide_collect(a, b, k, &nq, qs);
-          if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, d);
+          if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, st_enc(d, 0, a.sync));
         }
         const bool und = in && d == kUndecided;
         const uint32_t m = __ballot_sync(0xffffffffu, und);
@@ -427,18 +447,18 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
           const int b = image_of(a.img_off, a.B, g);
           const int64_t k = g - a.img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
-          if (__ldcg(sp) != kUndecided) continue;
-          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1]) : decide(a, b, k);
-          if (d != kUndecided) __stcg(sp, d); else ++undecided;
+          if ((__ldcg(sp) & 3u) != kUndecided) continue;
+          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], round) : decide(a, b, k, round);
+          if (d != kUndecided) __stcg(sp, st_enc(d, round, a.sync)); else ++undecided;
         }
       } else {
         for (int64_t g = gtid; g < total; g += gsize) {
           const int b = image_of(a.img_off, a.B, g);
           const int64_t k = g - a.img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
-          if (__ldcg(sp) != kUndecided) continue;
-          const uint8_t d = decide(a, b, k);
-          if (d != kUndecided) __stcg(sp, d); else ++undecided;
+          if ((__ldcg(sp) & 3u) != kUndecided) continue;
+          const uint8_t d = decide(a, b, k, round);
+          if (d != kUndecided) __stcg(sp, st_enc(d, round, a.sync)); else ++undecided;
         }
       }
       if (undecided) atomicAdd(&a.counters[round % 3], undecided);
@@ -457,7 +477,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     const int b = image_of(a.chunk_off, a.B, c);
     const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
     const int64_t n = a.img_off[b + 1] - a.img_off[b];
-    const bool kept = k < n && __ldcg(a.st + (int64_t)b * a.cap + k) == kKept;
+    const bool kept = k < n && (__ldcg(a.st + (int64_t)b * a.cap + k) & 3u) == kKept;
     const int cnt = __popc(__ballot_sync(0xffffffffu, kept));
     if (lane == 0) red[warp] = cnt;
     __syncthreads();
@@ -508,7 +528,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     const int b = image_of(a.chunk_off, a.B, c);
     const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
     const int64_t n = a.img_off[b + 1] - a.img_off[b];
-    const bool kept = k < n && __ldcg(a.st + (int64_t)b * a.cap + k) == kKept;
+    const bool kept = k < n && (__ldcg(a.st + (int64_t)b * a.cap + k) & 3u) == kKept;
     const uint32_t m = __ballot_sync(0xffffffffu, kept);
     if (lane == 0) red[warp] = __popc(m);
     __syncthreads();

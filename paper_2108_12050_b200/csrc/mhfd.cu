@@ -155,7 +155,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.chunkoff = take(sizeof(int64_t) * (B + 1));
   L.chunkcnt = take(sizeof(int32_t) * nchunk * B);
   L.chunkpos = take(sizeof(int32_t) * nchunk * B);
-  L.counters = take(sizeof(int32_t) * 64);   // 8 counters; [16, 64): k_prune phase stamps (PRUNE_STAMPS builds)
+  L.counters = take(sizeof(int32_t) * 64);   // k_prune: [0, 9); mhfd_prune_band's tally: 12, 13; [16, 64): PRUNE_STAMPS
   L.scores = take(sizeof(double) * B);
   L.counts = take(sizeof(int32_t) * B);
   // two-pass schedules: Rx of every level (LoG: of each of the 2n sub-levels) for up to
@@ -634,7 +634,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
 
 mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_blob* blobs, int32_t blob_cap,
                       int32_t* counts, double* scores, int32_t* flags, cudaStream_t st, int& launches,
-                      cudaEvent_t* ev, const mhfd_blob* ext_cand = nullptr) {
+                      cudaEvent_t* ev, const mhfd_blob* ext_cand = nullptr, int sync = 0) {
   PruneArgs pa;
   memset(&pa, 0, sizeof(pa));
   pa.B = B;
@@ -645,6 +645,7 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   pa.ncand = reinterpret_cast<const int32_t*>(ws + L.ncand);
   pa.overlap = c->p.overlap;
   pa.prune = c->p.overlap < 1.0f ? 1 : 0;
+  pa.sync = sync;
   pa.radmax = c->radmax;
   for (int s = 0; s < c->n; ++s) pa.rad[s] = c->rad[s];
   for (int s = 0; s < c->n; ++s) pa.dmax[s] = c->dmax[s];
@@ -712,6 +713,36 @@ __global__ void k_copy_cands(const mhfd_blob* __restrict__ src, const int32_t* _
     dst[i] = src[i];
 }
 __global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
+
+// mhfd_prune_band's tally: kept blobs of rows [y0, y1) and the certificate (out[1] starts
+// at 1 and is cleared if some band blob's decision round t has (t + 1) D above its
+// distance to a truncated edge of the extended band [e0, e1))
+__global__ void k_band_tally(const mhfd_blob* __restrict__ cand, const uint8_t* __restrict__ st, int32_t n, int y0,
+                             int y1, int e0, int e1, int H, int D, int32_t* __restrict__ out) {
+  int kept = 0, nb = 0;
+  bool bad = false;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int y = cand[k].y;
+    if (y < y0 || y >= y1) continue;
+    ++nb;
+    const uint8_t s = st[k];
+    kept += (s & 3u) == kKept;
+    const int t = s >> 2;
+    const int margin = min(e0 > 0 ? y - e0 : INT_MAX, e1 < H ? e1 - 1 - y : INT_MAX);
+    if ((s & 3u) == kUndecided || t >= 63 || (int64_t)(t + 1) * D > margin) bad = true;
+  }
+  for (int o = 16; o; o >>= 1) {
+    kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (kept) atomicAdd(&out[0], kept);
+    if (nb) atomicAdd(&out[2], nb);
+    if (bad) atomicExch(&out[1], 0);
+  }
+}
+__global__ void k_tally_init(int32_t* out) { out[0] = 0; out[1] = 1; out[2] = 0; }
 
 __global__ void k_copy_lohi(const ImgPar* par, int32_t* lohi, int B) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1289,6 +1320,54 @@ mhfd_status mhfd_prune_candidates(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t
   mhfd_status s = run_prune(c, 1, ws, L, blob_capacity > 0 ? d_blobs : nullptr, blob_capacity, d_count, d_score,
                             d_flags, st, launches, nullptr, ncand > 0 ? d_cands : reinterpret_cast<const mhfd_blob*>(ws + L.cand));
   if (s != MHFD_OK) return s;
+  g_launches = launches;
+  return MHFD_OK;
+}
+
+int32_t mhfd_interaction_radius(const mhfd_ctx* c) {
+  if (!c) return -1;
+  int d = 0;
+  for (int s = 0; s < c->n; ++s) d = std::max(d, (int)c->dmax[s]);
+  return d;
+}
+
+mhfd_status mhfd_prune_band(mhfd_ctx* c, const mhfd_blob* d_cands, int32_t ncand, int32_t e0, int32_t e1, int32_t y0,
+                            int32_t y1, void* d_workspace, size_t workspace_bytes, int32_t* d_count, int32_t* d_cert,
+                            int32_t* d_nband, void* stream) {
+  g_err.clear();
+  if (!c) return fail(MHFD_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  const int H = c->p.height;
+  if (!(0 <= e0 && e0 <= y0 && y0 < y1 && y1 <= e1 && e1 <= H))
+    return fail(MHFD_ERR_SHAPE, "need 0 <= e0 <= y0 < y1 <= e1 <= height (%d %d %d %d, %d)", e0, y0, y1, e1, H);
+  if (ncand < 0 || ncand > c->cap) return fail(MHFD_ERR_CAPACITY, "ncand %d not in [0, %lld]", ncand, (long long)c->cap);
+  if (ncand > 0 && !d_cands) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_cands is NULL");
+  if (!d_count || !d_cert) return fail(MHFD_ERR_INVALID_ARGUMENT, "d_count / d_cert is NULL");
+  if (!d_workspace || ((uintptr_t)d_workspace) % 256 != 0) return fail(MHFD_ERR_WORKSPACE, "workspace");
+  const Layout L = layout(c, 1);
+  if (workspace_bytes < L.total) return fail(MHFD_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, L.total);
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != c->p.device)
+    return fail(MHFD_ERR_DEVICE, "current device %d != context device %d", dev, c->p.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(d_workspace);
+  k_set_i32<<<1, 1, 0, st>>>(reinterpret_cast<int32_t*>(ws + L.ncand), ncand);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_set_i32");
+  int launches = 1;
+  const mhfd_blob* cand = ncand > 0 ? d_cands : reinterpret_cast<const mhfd_blob*>(ws + L.cand);
+  int32_t* scratch = reinterpret_cast<int32_t*>(ws + L.counts);   // 1 int (the full-list count, unused)
+  mhfd_status s = run_prune(c, 1, ws, L, nullptr, 0, scratch, nullptr, nullptr, st, launches, nullptr, cand, 1);
+  if (s != MHFD_OK) return s;
+  int32_t* tally = reinterpret_cast<int32_t*>(ws + L.counters) + 12;   // {count, cert, nband}; k_prune: 0-8, 16-63
+  k_tally_init<<<1, 1, 0, st>>>(tally);
+  k_band_tally<<<std::max(1, std::min(c->sms * 4, (ncand + 255) / 256)), 256, 0, st>>>(
+      cand, reinterpret_cast<const uint8_t*>(ws + L.st), ncand, y0, y1, e0, e1, H, mhfd_interaction_radius(c), tally);
+  launches += 2;
+  e = cudaMemcpyAsync(d_count, tally, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_cert, tally + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && d_nband) e = cudaMemcpyAsync(d_nband, tally + 2, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "band tally");
   g_launches = launches;
   return MHFD_OK;
 }

@@ -93,3 +93,43 @@ def focus_score_single_image(det, image: torch.Tensor, src: int = 0):
     if over:
         flags |= 1
     return blobs, cnt, score, flags
+
+
+def halo_rows(det, rounds: int = 5) -> int:
+    """Rows a band is extended by for the sharded pruning: a blob decided in synchronous
+    round t depends on the candidates within (t + 1) D (mhfd_prune_band), so a halo of
+    (rounds + 1) D certifies every band blob decided by round `rounds`.  5 rounds certified
+    all 8 bands of sharp and defocused C3 and C5 tiles (3 suffice for C3;
+    tools/halo_sweep.py)."""
+    return (rounds + 1) * det.interaction_radius()
+
+
+def focus_score_single_image_sharded(det, image: torch.Tensor, src: int = 0, halo: int | None = None):
+    """Score ONE image on all ranks with the pruning sharded too (each
+    rank prunes its own band from the candidates of the band plus `halo` rows on each
+    side, mhfd_prune_band; one all-reduce of (kept, certificate failures, band
+    candidates) replaces the all-gather of the candidate list and the replicated
+    pruning).  Falls back to focus_score_single_image's gather + replicated pruning when
+    some band's certificate fails or the image has more candidates than max_candidates
+    (whose truncation rule needs the whole list).  Returns (count, score, sharded) with
+    count and score identical on every rank and equal to det.focus_score on the whole
+    image; `sharded` says which path produced them."""
+    dist.broadcast(image, src)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    H, cap = det.height, det.max_candidates
+    y0, y1 = band_rows(H, world, rank)
+    h = halo_rows(det) if halo is None else int(halo)
+    e0, e1 = max(0, y0 - h), min(H, y1 + h)
+    cands, n = det.detect_band(image, e0, e1)
+    n_ext = int(n.item())
+    if n_ext <= cap:
+        kept, cert, nband = det.prune_band(cands, n_ext, e0, e1, y0, y1)
+        red = torch.stack([kept[0].to(torch.int64), 1 - cert[0].to(torch.int64), nband[0].to(torch.int64)])
+    else:   # the extended band alone overflows the pruning capacity: not certifiable
+        red = torch.tensor([0, 1, cap + 1], dtype=torch.int64, device=cands.device)
+    dist.all_reduce(red)   # SUM: kept blobs, failed certificates, candidates
+    kept_all, fails, total = (int(v) for v in red.cpu().tolist())
+    if fails == 0 and total <= cap:
+        return kept_all, float(kept_all), True
+    _, cnt, score, _ = focus_score_single_image(det, image, src)
+    return int(cnt.item()), float(score.item()), False

@@ -162,3 +162,81 @@ def test_gather_candidates_overflow_world2():
         assert got.shape == (8, 4)
         assert got[:5, 0].tolist() == [0, 1, 2, 3, 4] and (got[:5, 1] == 0).all()
         assert got[5:, 0].tolist() == [0, 1, 2] and (got[5:, 1] == 10).all()
+
+
+# ---------------------------------------------------------------- sharded pruning (f2)
+class _FakeDet:
+    """Stands in for the Detector (the kernels need a B200): a fixed candidate set; a
+    candidate is 'kept' iff its x is even, so band counts and the full-list count agree
+    exactly as mhfd_prune_band's certified counts and mhfd_prune_candidates' do."""
+
+    def __init__(self, H, cap, fail_rank=-1):
+        rng = np.random.default_rng(5)
+        ys = np.sort(rng.integers(0, H, 60))
+        xs = rng.integers(0, 50, 60)
+        self.rec = torch.tensor(np.stack([xs, ys, np.zeros(60), np.zeros(60)], 1), dtype=torch.int32)
+        self.height, self.max_candidates, self.fail_rank = H, cap, fail_rank
+        self.calls = []
+
+    def interaction_radius(self):
+        return 3
+
+    def detect_band(self, image, y0, y1):
+        m = self.rec[(self.rec[:, 1] >= y0) & (self.rec[:, 1] < y1)]
+        cap = max(self.max_candidates, 1)
+        out = torch.zeros((cap, 4), dtype=torch.int32)
+        out[:min(len(m), cap)] = m[:cap]
+        self.calls.append(("detect_band", y0, y1))
+        return out, torch.tensor([len(m)], dtype=torch.int32)
+
+    def prune_band(self, cands, n, e0, e1, y0, y1):
+        c = cands[:n]
+        inb = (c[:, 1] >= y0) & (c[:, 1] < y1)
+        kept = int((inb & (c[:, 0] % 2 == 0)).sum())
+        cert = 0 if dist.get_rank() == self.fail_rank else 1
+        self.calls.append(("prune_band", e0, e1, y0, y1))
+        return (torch.tensor([kept], dtype=torch.int32), torch.tensor([cert], dtype=torch.int32),
+                torch.tensor([int(inb.sum())], dtype=torch.int32))
+
+    def prune_candidates(self, allc, total):
+        k = int((allc[:total, 0] % 2 == 0).sum())
+        self.calls.append(("prune_candidates", total))
+        return None, torch.tensor([k], dtype=torch.int32), torch.tensor([float(k)], dtype=torch.float64), \
+            torch.tensor([0], dtype=torch.int32)
+
+
+def _sharded_worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2108_12050_b200.dist import focus_score_single_image_sharded
+    det = _FakeDet(40, cap=100 if case != "overflow" else 30, fail_rank=1 if case == "fail" else -1)
+    img = torch.zeros((40, 50), dtype=torch.uint8)
+    cnt, score, sharded = focus_score_single_image_sharded(det, img)
+    truth = int((det.rec[:, 0] % 2 == 0).sum()) if case != "overflow" else int((det.rec[:30, 0] % 2 == 0).sum())
+    q.put((rank, cnt, score, sharded, truth, [c[0] for c in det.calls]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["ok", "fail", "overflow"])
+def test_sharded_pruning_world2(case):
+    """dist.focus_score_single_image_sharded over gloo, world 2: certified bands -> the
+    summed band counts (no candidate gather, no prune_candidates call); one failed
+    certificate or more candidates than max_candidates (whose truncation needs the whole
+    raster list) -> every rank falls back to the gather + replicated pruning, and all
+    ranks return the same count."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, cnt, score, sharded, truth, calls in res:
+        assert cnt == truth and score == float(truth)
+        assert sharded == (case == "ok")
+        assert ("prune_candidates" in calls) == (case != "ok")

@@ -765,3 +765,46 @@ def test_tc2_batch_ragged_rows_and_degenerate():
     eps = P.REL_EPS * float(ref["D"].max())
     assert float(np.abs(d["dog"][7].cpu().numpy() - ref["D"]).max()) <= eps
     P.assert_score(int(cnt[7]), ref["count"])
+
+
+@pytest.mark.parametrize("size,G", [(1024, 2), (1024, 3), (4096, 8)])
+def test_sharded_pruning_certificate(size, G):
+    """f2 sharded pruning (mhfd_prune_band; SURVEY §8(f) f2 "border-blob exchange"), the
+    G ranks run one after another on this GPU.  (1) Synchronous rounds decide exactly
+    like the default rounds: the whole image as one band (no truncated edge, certificate
+    trivially 1) gives detect()'s count.  (2) Every certified band's count equals the
+    number of the whole image's kept blobs in its rows, with the default halo and with a
+    halo of one interaction radius D (which certifies fewer bands: the certificate must
+    never claim a wrong count).  (3) With the default halo every band certifies on these
+    EM tiles and the band counts sum to the image's count; the band candidate counts sum
+    to the image's candidate count."""
+    from paper_2108_12050_b200.dist import band_rows, halo_rows
+    img = synth.em_tile(size, size, 1004, defocus=0.5, dose=300.0, device="cuda")
+    det = mhfd.Detector(size, size, threshold=0.09, **C3)
+    blobs, cnt, _ = det.detect(img)
+    torch.cuda.synchronize()
+    k_full = int(cnt[0])
+    ys = blobs[0, :k_full, 1].cpu()
+    c, n = det.detect_band(img, 0, size)
+    kept, cert, nb = det.prune_band(c, int(n), 0, size, 0, size)
+    assert int(kept[0]) == k_full and int(cert[0]) == 1 and int(nb[0]) == int(n)
+    D = det.interaction_radius()
+    assert D > 0
+    for halo, expect_all in ((halo_rows(det), True), (D, False)):
+        tot_kept, tot_n, ncert = 0, 0, 0
+        for r in range(G):
+            y0, y1 = band_rows(size, G, r)
+            e0, e1 = max(0, y0 - halo), min(size, y1 + halo)
+            c, n = det.detect_band(img, e0, e1)
+            kept, cert, nb = det.prune_band(c, int(n), e0, e1, y0, y1)
+            torch.cuda.synchronize()
+            truth = int(((ys >= y0) & (ys < y1)).sum())
+            if int(cert[0]):
+                assert int(kept[0]) == truth, (halo, r, int(kept[0]), truth)
+                ncert += 1
+            tot_kept += int(kept[0])
+            tot_n += int(nb[0])
+        if expect_all:
+            assert ncert == G and tot_kept == k_full
+        full = det.debug_dump(img, dog=False, cands=True)
+        assert tot_n == int(full["ncand"][0])
