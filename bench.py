@@ -469,7 +469,7 @@ def sharded_single_image(dev, dist, steps: int) -> dict:
     broadcast + bands + all-gathers + pruning; device time, max over ranks."""
     import synth
     import paper_2108_12050_b200 as mhfd
-    from paper_2108_12050_b200.dist import focus_score_single_image
+    from paper_2108_12050_b200.dist import focus_score_single_image, focus_score_single_image_sharded
     img = synth.em_tile(SIZE, SIZE, 1000, defocus=0.0, dose=300.0, device=dev)
     det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP, device=dev.index)
     ref = float(det.focus_score(img)[0])
@@ -486,8 +486,22 @@ def sharded_single_image(dev, dist, steps: int) -> dict:
     ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     assert float(score[0]) == ref, "sharded score differs from the single-GPU score"
+    # the same with the pruning sharded too (band + halo, certificate, one all-reduce)
+    for _ in range(3):
+        focus_score_single_image_sharded(det, img)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(steps):
+        _, score2, sharded = focus_score_single_image_sharded(det, img)
+    e1.record()
+    torch.cuda.synchronize()
+    ms2 = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+    assert score2 == ref, "sharded-pruning score differs from the single-GPU score"
     return {"workload": "one 4096^2 u8 tile per step, row bands across ranks (SURVEY §8(f) f2)",
-            "ms_per_image": float(ms.item()), "score": ref}
+            "ms_per_image": float(ms.item()), "score": ref,
+            "sharded_pruning": {"ms_per_image": float(ms2.item()), "certified": bool(sharded)}}
 
 
 # ------------------------------------------------------------------ GPU arm
