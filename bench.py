@@ -589,14 +589,14 @@ def main() -> None:
     if not args.no_e2e:
         host = imgs.cpu().pin_memory()
         for _ in range(2):
-            det.focus_score_host(host, chunk=16)
+            det.focus_score_host(host, chunk=8)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         e0 = time.perf_counter()
         ev0.record(stream)
         for _ in range(args.steps):
-            hs = det.focus_score_host(host, chunk=16)
+            hs = det.focus_score_host(host, chunk=8)
             if dist is not None:
                 gather_results(hs.to(dev), hs.to(dev), gathered)
         ev1.record(stream)
@@ -609,7 +609,7 @@ def main() -> None:
         assert torch.equal(hs, scores.cpu()), "host-path scores differ from the device path"
         e2e = {"value": px_step / (e_ms * 1e-3) / 1e6, "unit": "MPix/s", "ms_per_step": e_ms,
                "wall_ms_per_step": wall, "h2d_bytes_per_step": B * SIZE * SIZE, "d2h_bytes_per_step": B * 12,
-               "api": "mhfd_focus_score_host (pinned host batch, chunks ramping 2,3,4,6,8,12,16 images, copy/compute overlap)"}
+               "api": "mhfd_focus_score_host (pinned host batch, chunks of 1, 2, ..., 8, 8, ... images, copy/compute overlap)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -749,6 +749,24 @@ __global__ void k_copy_lohi(const ImgPar* par, int32_t* lohi, int B) {
   if (b < B) { lohi[2 * b] = par[b].lo; lohi[2 * b + 1] = par[b].hi; }
 }
 
+// e2e chunk sizes.  Round 1 ramped them up geometrically (2, 3, 4, 6, 8, 12, 16, ...:
+// the compute, ~0.43 ms per image, outran the ~0.31 ms copy, so growing chunks kept the
+// copies hidden).  Now a chunk of n images computes in ~0.31 n + 0.24 ms (the per-call
+// latency of the percentiles, NMS and pruning), about as fast as its copy: a chunk
+// larger than its predecessor by more than about one image makes the compute wait for
+// the copy.  So the sizes grow by one image per chunk from 1 up to the caller's size
+// (1, 2, ..., chunk, chunk, ...): only the first image's copy is exposed, and the chunk
+// count (each costing its ~0.24 ms) stays small.  64 x 4096^2 u8: 24.9 ms (geometric, 16)
+// -> 23.7 (uniform 8) -> see DESIGN.md §8 for this ramp.
+std::vector<int> e2e_chunks(int batch, int chunk) {
+  std::vector<int> out;
+  for (int left = batch, n = 1; left > 0; n = std::min(chunk, n + 1)) {
+    out.push_back(std::min(n, left));
+    left -= out.back();
+  }
+  return out;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1187,15 +1205,9 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
   if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[1], st);
   if (e != cudaSuccess) return cuda_fail(e, "event record");
   int launches = 0;
-  // chunk sizes ramp up geometrically by ~1.4x from <= 2 images (chunk 16: 2, 3, 4, 6, 8,
-  // 12, 16, ...): the first copy, which nothing can hide, is short; each next copy (~0.31
-  // ms per 4096^2 u8 image over PCIe) still fits under the previous chunk's compute (~0.43
-  // ms per image), which a doubling ramp (2, 4, 8) does not (0.7 ms stall before the first
-  // full chunk); later chunks are large enough that per-call fixed costs stay small.
-  // 64 x 4096^2 u8 end to end: 29.5 ms (doubling ramp, chunk 8) -> 28.4 ms (chunk 16)
-  for (int b0 = 0, k = 0, nb = 0, want = std::max(1, std::min(2, chunk / 4)); b0 < batch; b0 += nb, ++k) {
-    if (k > 0) want = std::min(chunk, std::max(want + 1, (want * 7 + 4) / 5));
-    nb = std::min(want, batch - b0);
+  const std::vector<int> sizes = e2e_chunks(batch, chunk);
+  for (int b0 = 0, k = 0, nb = 0; k < (int)sizes.size(); b0 += nb, ++k) {
+    nb = sizes[k];
     const int h = k & 1;
     char* dst = static_cast<char*>(d_staging) + (size_t)h * chunk * img_bytes;
     e = cudaStreamWaitEvent(c->copy_stream, c->ev_free[h], 0);
