@@ -134,46 +134,52 @@ __global__ void __launch_bounds__(256) k_nms_count(NmsArgs a, int nseg, int32_t*
   if (lane == 0) segcnt[(int64_t)b * nseg + seg] = cnt;
 }
 
-// One CTA (1024 threads) per image: exclusive scan of the segment counts.  Each thread
-// owns a contiguous run of ceil(nseg / 1024) counts: one read pass, a thread-local scan,
-// one block-wide scan of the 1024 run totals, one write pass (a 1024-wide loop with four
-// barriers per 1024 segments took 17 us for the 16384 segments of one 4096^2 tile).
+// One CTA (1024 threads) per image: exclusive scan of the segment counts.  Warp w owns a
+// contiguous block of ceil(nseg / 1024) x 32 counts and walks it 32 at a time (coalesced
+// loads, a warp scan per step, a running carry), the 32 warp totals are scanned once,
+// and the block's offsets are written in a second coalesced walk.  (Round 1's 1024-wide
+// loop with four barriers per step took 17 us for the 16384 segments of a 4096^2 tile;
+// per-thread contiguous runs were uncoalesced and no faster.)
 __global__ void __launch_bounds__(1024) k_seg_scan(const int32_t* __restrict__ segcnt, int nseg,
                                                    int32_t* __restrict__ segoff, int32_t* __restrict__ ncand) {
   __shared__ int32_t wsum[32];
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (nseg + 1023) / 1024;
-  const int i0 = min(nseg, (int)threadIdx.x * per), i1 = min(nseg, i0 + per);
+  const int per = ((nseg + 1023) / 1024) * 32;   // counts per warp (multiple of 32)
+  const int i0 = min(nseg, warp * per), i1 = min(nseg, i0 + per);
   const int32_t* sc = segcnt + (int64_t)b * nseg;
   int32_t* so = segoff + (int64_t)b * nseg;
-  int run = 0;
-  for (int i = i0; i < i1; ++i) run += sc[i];
-  int x = run;
+  int tot = 0;
+#pragma unroll 4
+  for (int i = i0 + lane; i - lane < i1; i += 32) tot += i < i1 ? __ldg(sc + i) : 0;
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, off);
-    if (lane >= off) x += y;
-  }
-  if (lane == 31) wsum[warp] = x;
+  for (int off = 16; off; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+  if (lane == 0) wsum[warp] = tot;
   __syncthreads();
   if (warp == 0) {
-    int s = wsum[lane];
+    const int v = wsum[lane];
+    int x = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, off);
-      if (lane >= off) s += y;
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
     }
-    wsum[lane] = s;
+    wsum[lane] = x - v;   // exclusive
+    if (lane == 31) ncand[b] = x;
   }
   __syncthreads();
-  int excl = (warp ? wsum[warp - 1] : 0) + x - run;
-  for (int i = i0; i < i1; ++i) {
-    const int v = sc[i];
-    so[i] = excl;
-    excl += v;
+  int carry = wsum[warp];
+  for (int i = i0 + lane; i - lane < i1; i += 32) {
+    const int v = i < i1 ? __ldg(sc + i) : 0;
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (i < i1) so[i] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
-  if (threadIdx.x == 1023) ncand[b] = wsum[31];
 }
 
 template <int MODE>
