@@ -204,13 +204,16 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" :::
 // Hazards: row(g) writes D1 after col(g-1) read A2 (in-order tcgen05.mma); col(g) writes
 // D2[g&1] (= L_{g-2}) after every warp's DoG of g-1 (it precedes their split arrivals);
 // B1 is restaged after rowDone of the tile's last level (waited before its split).
-template <bool DOG>   // DOG: also write every DoG plane to dog_out (26-neighbour NMS, dumps)
+// DOG: also write every DoG plane to dog_out (26-neighbour NMS, dumps).  NP: level parts
+// per tile (1, or 2 for calls with few tiles; a template so the batch path pays nothing)
+template <bool DOG, int NP = 1>
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
      float* __restrict__ v_out, uint8_t* __restrict__ idx_out, float* __restrict__ dog_out, int batch,
-     int row_lo, int row_hi,
+     int row_lo, int row_hi, int lsplit, float* __restrict__ v_out2, uint8_t* __restrict__ idx_out2,
      unsigned long long* __restrict__ trace) {
+  constexpr int nparts = NP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int S = P.S, LW = tc_lw(P), OFF = tc_off(P);
   uint8_t* B1 = smem_raw;                                          // S x S fp16, canonical K-major
@@ -228,11 +231,21 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   // rows [row_lo, row_hi) of every image (the whole image, or one band: mhfd_detect_band)
   const int tx = (s.W + kTcTile - 1) / kTcTile, ty = (row_hi - row_lo + kTcTile - 1) / kTcTile;
-  const int ntiles = tx * ty * batch;
+  // Work units: a tile (nparts = 1), or for calls with fewer tiles than SMs a tile's levels
+  // in two parts (nparts = 2): part 0 levels [0, lsplit], part 1 [lsplit, nlev) (level
+  // lsplit twice: part 1's first DoG plane needs it), DoG planes [0, lsplit) and
+  // [lsplit, n), v / argmax of part 1 to v_out2 / idx_out2 (merged by k_merge_parts).
+  // The grid is even, so a CTA's units all have the part t0 & 1.
+  const int ntiles = tx * ty * batch * nparts;   // units
   const int t0 = blockIdx.x;
   if (t0 >= ntiles) return;
+  const int part = nparts > 1 ? (t0 & 1) : 0;
+  const int lev_lo = part ? lsplit : 0;
+  const int nl2 = part ? P.nlev - lsplit : lsplit + 1;
+#define nl (NP > 1 ? nl2 : P.nlev)   // levels per unit (NP = 1: read from the parameter bank, no register)
   const int my_tiles = (ntiles - 1 - t0) / gridDim.x + 1;
-  const int G = my_tiles * P.nlev;   // levels this CTA processes
+  const int G = my_tiles * nl;   // levels this CTA processes
+
   const int SBO1 = (S / 8) * 128;
 
   if (tid == kTcThreads) {
@@ -253,7 +266,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     if (lane != 0) tr = nullptr;
     auto issue_table = [&](int gg) {
       if (lane == 0) {
-        const int lev = gg % P.nlev;
+        const int lev = lev_lo + gg % nl;
         const int bytes = 2 * P.lev[lev].npairs * 256;
         uint64_t* tb = &bars[8 + (gg & 1)];
         mbar_arrive_expect_tx(tb, (uint32_t)bytes);
@@ -266,9 +279,9 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     int tile_i = 0;
     uint32_t sph = 0;   // phase bits of the split barriers (group 3 is not used on every level)
     for (int g = 0; g < G; ++g) {
-      const int lev = g % P.nlev;
+      const int lev = lev_lo + g % nl;
       TC_STAMP(g, 0);
-      if (lev == 0) mbar_wait(&bars[7], (uint32_t)(tile_i++ & 1));
+      if (lev == lev_lo) mbar_wait(&bars[7], (uint32_t)(tile_i++ & 1));
       mbar_wait(&bars[8 + (g & 1)], (uint32_t)((g >> 1) & 1));
       umma::fence_after();
       TC_STAMP(g, 1);
@@ -315,20 +328,22 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     const int q = warp & 3, wg = warp >> 2;
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
     const int64_t plane = (int64_t)s.H * s.W;
-    int t = t0;
-    TcTile tt = tc_tile(t, tx, ty, row_lo);
-    int mode = tc_fetch_epi(tt, land, &bars[0], images, s, &tmap, use_tmap, P);
+    // tiles are kept as unit indices (t: staged next, ou: current, wu: output pending) and
+    // expanded with tc_tile where needed: three ints instead of three TcTiles of state
+    auto tile_of = [&](int u) { return tc_tile(u / nparts, tx, ty, row_lo); };
+    int t = t0, ou = t0;
+    int mode = tc_fetch_epi(tile_of(t), land, &bars[0], images, s, &tmap, use_tmap, P);
     uint32_t land_phase = 0;
-    TcTile ot = tt;
     float oinv = 0.f;
     int odeg = 0;
     float vbest[32];
     uint32_t ibest[8];
 
     auto consume = [&](int gg) {   // DoG plane lev-1 from L_lev (D2[gg&1]) and L_{lev-1} (D2[(gg-1)&1])
-      const int lev = gg % P.nlev;
-      if (lev == 0) return;
+      const int lev = lev_lo + gg % nl;
+      if (lev == lev_lo) return;   // a unit's first level has no DoG of its own
       const float tf = P.lev[lev - 1].tdog * oinv;
+      const TcTile ot = tile_of(ou);   // (the DOG variant's plane writes only)
       const uint32_t cur = tq + 256 + 128 * (gg & 1) + 32 * wg, prv = tq + 256 + 128 * ((gg - 1) & 1) + 32 * wg;
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {   // 8 rows at a time: fewer live registers (96 with 17 warps)
@@ -363,12 +378,13 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         }
       }
     };
-    auto write_out = [&](const TcTile& wt, int wdeg) {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
+    auto write_out = [&](int wu, int wdeg) {   // v and argmax of column 32 q + lane, rows 32 wg .. +32
       if ((DOG && !v_out) || TC_EXP == 5) return;
+      const TcTile wt = tile_of(wu);
       const int x = wt.x0 + 32 * q + lane, y0 = wt.y0 + 32 * wg;
       const int64_t p0 = (int64_t)wt.b * plane + (int64_t)y0 * s.W + x;
-      float* vo = v_out + p0;
-      uint8_t* io = idx_out + p0;
+      float* vo = ((NP > 1 && part) ? v_out2 : v_out) + p0;      // level part 1 -> its own planes
+      uint8_t* io = ((NP > 1 && part) ? idx_out2 : idx_out) + p0;
       if (x < s.W && y0 + 32 <= row_hi) {   // whole column piece inside: pointer walk, no checks
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
@@ -387,7 +403,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         }
       }
     };
-    TcTile wt = tt;   // tile whose output is pending (written after the split of the next tile's level 0)
+    int wu = t0;   // unit whose output is pending (written after the split of the next unit's first level)
     int wdeg = 0;
     bool pending = false;
 
@@ -396,26 +412,27 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     // call site each for consume and the output, which keeps the kernel's code small)
     for (int g = 0; g <= G; ++g) {
       const bool last = g == G;
-      const int lev = last ? 0 : g % P.nlev;
+      const int lev = last ? lev_lo : lev_lo + g % nl;
+      const bool first = lev == lev_lo;   // a unit's first level (tile boundary) or the tail step
       const uint32_t par_g = (uint32_t)(g & 1);
       TC_STAMP(g, 8);
       ImgPar ip{};
       int tn = 0;
-      if (lev == 0 && !last) {
+      if (first && !last) {
         // ---- stage tile tt (rowDone of the previous tile's last level was waited below)
         if (mode) {
           mbar_wait(&bars[0], land_phase);
           land_phase ^= 1u;
         }
         epi_sync();
-        ip = par[tt.b];
+        ip = par[tile_of(t).b];
         tc_stage_b1(land, B1, S, LW, OFF, ip.lo, ip.hi, ip.lo + (ip.hi - ip.lo + 1) / 2);
         umma::fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive1(&bars[7]);
         epi_sync();   // landing zone free
         tn = t + gridDim.x;
-        if (tn < ntiles) mode = tc_fetch_epi(tc_tile(tn, tx, ty, row_lo), land, &bars[0], images, s, &tmap, use_tmap, P);
+        if (tn < ntiles) mode = tc_fetch_epi(tile_of(tn), land, &bars[0], images, s, &tmap, use_tmap, P);
       }
       // ---- DoG of level g-1.  At level 0 that is the previous tile's last level; it runs
       // before this level's column pass overwrites D2[g & 1] (= its L_{n-1}), and the
@@ -427,17 +444,17 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         TC_STAMP(g, 9);
         consume(g - 1);
       }
-      if (lev == 0) {
+      if (first) {
         if (g > 0) {
-          wt = ot;
+          wu = ou;
           wdeg = odeg;
           pending = true;
         }
         if (!last) {
-          ot = tt;
+          ou = t;
           oinv = ip.inv * (1.f / kTcWScale);
           odeg = ip.degen;
-          if (tn < ntiles) { t = tn; tt = tc_tile(tn, tx, ty, row_lo); }
+          if (tn < ntiles) t = tn;
         }
       }
       TC_STAMP(g, 10);
@@ -457,8 +474,8 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
           TC_STAMP(g, 12 + grp);
         }
       }
-      if (lev == 0) {
-        if (pending) write_out(wt, wdeg);
+      if (first) {
+        if (pending) write_out(wu, wdeg);
         pending = false;
 #pragma unroll
         for (int u = 0; u < 32; ++u) vbest[u] = -INFINITY;
@@ -471,6 +488,27 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 512);
 #undef TC_STAMP
+#undef nl
+}
+
+// v / argmax of the two level parts (k_tc with nparts = 2): part 0 holds DoG planes
+// [0, lsplit), part 1 [lsplit, n); the first argmax over all planes is part 1's only where
+// its maximum is strictly larger.  4 pixels per thread (16-byte and 4-byte accesses).
+__global__ void __launch_bounds__(256) k_merge_parts(float* __restrict__ v, uint8_t* __restrict__ idx,
+                                                     const float* __restrict__ v2, const uint8_t* __restrict__ idx2,
+                                                     int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = reinterpret_cast<const float4*>(v)[i];
+    const float4 b = __ldg(reinterpret_cast<const float4*>(v2) + i);
+    uchar4 ia = reinterpret_cast<const uchar4*>(idx)[i];
+    const uchar4 ib = __ldg(reinterpret_cast<const uchar4*>(idx2) + i);
+    if (b.x > a.x) { a.x = b.x; ia.x = ib.x; }
+    if (b.y > a.y) { a.y = b.y; ia.y = ib.y; }
+    if (b.z > a.z) { a.z = b.z; ia.z = ib.z; }
+    if (b.w > a.w) { a.w = b.w; ia.w = ib.w; }
+    reinterpret_cast<float4*>(v)[i] = a;
+    reinterpret_cast<uchar4*>(idx)[i] = ia;
+  }
 }
 
 }  // namespace mhfd

@@ -90,7 +90,7 @@ mhfd_status cuda_fail(cudaError_t e, const char* where) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t par, sel, hist1, hist2, fimg, v, idx, dog, segcnt, segoff, ncand, cand, st, rowstart, cellstart, crec, imgoff, chunkoff,
+  size_t par, sel, hist1, hist2, fimg, v, idx, v2, idx2, dog, segcnt, segoff, ncand, cand, st, rowstart, cellstart, crec, imgoff, chunkoff,
       chunkcnt, chunkpos, counters, scores, counts, rx, xtc, slab, wl, total;
 };
 
@@ -103,6 +103,29 @@ bool tc2_fit(const mhfd_ctx* c) {
          c->p.width >= c->tc2->S;
 }
 int tc2_nrt(const mhfd_ctx* c) { return (c->p.height + c->tc2->NR - 1) / c->tc2->NR; }
+
+// k_tc splits each tile's levels over two CTAs when the call has at most half as many
+// tiles as SMs (one 1024^2 tile: 64 tiles on 148 SMs), whole images only
+bool tc_parts(const mhfd_ctx* c, int B) {
+  if (!c->tc) return false;
+  const int64_t tiles = (int64_t)((c->p.width + kTcTile - 1) / kTcTile) * ((c->p.height + kTcTile - 1) / kTcTile) * B;
+  return c->tc->nlev >= 3 && tiles * 2 <= c->sms;
+}
+// the level both parts compute: balances sum_i (K_i^2/16 + 12 K_i) (row + column pass
+// MMA cycles) between [0, m] and [m, nlev)
+int tc_lsplit(const TcPlan& P) {
+  std::vector<double> cost(P.nlev);
+  for (int i = 0; i < P.nlev; ++i) cost[i] = P.lev[i].K * (double)P.lev[i].K / 16.0 + 12.0 * P.lev[i].K;
+  int best = 1;
+  double bmax = 1e300;
+  for (int m = 1; m + 1 < P.nlev; ++m) {
+    double a = 0, b = 0;
+    for (int i = 0; i <= m; ++i) a += cost[i];
+    for (int i = m; i < P.nlev; ++i) b += cost[i];
+    if (std::max(a, b) < bmax) { bmax = std::max(a, b); best = m; }
+  }
+  return best;
+}
 
 int nseg_of(const mhfd_ctx* c) {
   const int64_t plane = (int64_t)c->p.width * c->p.height;
@@ -142,6 +165,10 @@ Layout layout(const mhfd_ctx* c, int B) {
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   L.v = take(paper ? sizeof(float) * plane * B : 0);
   L.idx = take(paper ? plane * B : 0);
+  // k_tc's level parts (calls with fewer than half as many tiles as SMs): part 1's v / argmax
+  const bool parts = paper && tc_parts(c, B);
+  L.v2 = take(parts ? sizeof(float) * plane * B : 0);
+  L.idx2 = take(parts ? plane * B : 0);
   L.dog = take(paper ? 0 : sizeof(float) * plane * c->n * B);
   L.segcnt = take(sizeof(int32_t) * nseg * B);
   L.segoff = take(sizeof(int32_t) * nseg * B);
@@ -359,23 +386,35 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
-    auto kern = tc_dog ? k_tc<true> : k_tc<false>;
+    const int nparts = (!band && paper && tc_parts(c, B)) ? 2 : 1;
+    auto kern = tc_dog ? (nparts > 1 ? k_tc<true, 2> : k_tc<true, 1>) : (nparts > 1 ? k_tc<false, 2> : k_tc<false, 1>);
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc attribute");
     // band mode: rows [band_lo - 1, band_hi + 1) on the whole image's 128-row tile grid, so
     // every pixel sees the same K-step grouping (and rounding) as in the whole-image run
     const int r_lo = band ? std::max(0, band_lo - 1) / kTcTile * kTcTile : 0;
     const int r_hi = band ? std::min(H, (std::min(H, band_hi + 1) + kTcTile - 1) / kTcTile * kTcTile) : H;
-    const int64_t ntiles = (int64_t)((W + kTcTile - 1) / kTcTile) * ((r_hi - r_lo + kTcTile - 1) / kTcTile) * B;
-    dim3 gb((unsigned)std::min<int64_t>(ntiles, c->sms));   // persistent: one CTA per SM
+    const int lsplit = nparts > 1 ? tc_lsplit(P) : 0;
+    const int64_t ntiles = (int64_t)((W + kTcTile - 1) / kTcTile) * ((r_hi - r_lo + kTcTile - 1) / kTcTile) * B * nparts;
+    int64_t grid = std::min<int64_t>(ntiles, c->sms);   // persistent: one CTA per SM
+    if (nparts > 1) grid &= ~(int64_t)1;                 // even: a CTA's units share a part
+    dim3 gb((unsigned)grid);
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     const int use_tm = (pitch % 16 == 0) && encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, img, (uint64_t)W,
                                                       (uint64_t)H * B, (uint64_t)pitch, (uint32_t)tc_lw(P),
                                                       (uint32_t)P.S);
+    float* v2 = reinterpret_cast<float*>(ws + L.v2);
+    uint8_t* idx2 = reinterpret_cast<uint8_t*>(ws + L.idx2);
     kern<<<gb, kTcThreads + 32, smem, st>>>(img, s, par, P, c->d_tctab, tm, use_tm, paper ? v : nullptr,
-                                            paper ? idx : nullptr, tc_dog, B, r_lo, r_hi, nullptr);
+                                            paper ? idx : nullptr, tc_dog, B, r_lo, r_hi, lsplit, v2, idx2,
+                                            nullptr);
     LAUNCH_CHECK("k_tc");
+    if (nparts > 1) {
+      const int64_t n4 = (int64_t)W * H * B / 4;
+      k_merge_parts<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, c->sms * 8), 256, 0, st>>>(v, idx, v2, idx2, n4);
+      LAUNCH_CHECK("k_merge_parts");
+    }
     MARK(2);
     return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
   }

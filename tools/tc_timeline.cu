@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    k_tc<false><<<148, kTcThreads + 32, smem>>>(dimg, s, dpar, P, dtab, tm, 1, dv, didx, nullptr, B, 0, H, rep == 2 ? dtr : nullptr);
+    k_tc<false><<<148, kTcThreads + 32, smem>>>(dimg, s, dpar, P, dtab, tm, 1, dv, didx, nullptr, B, 0, H, 0, nullptr, nullptr, rep == 2 ? dtr : nullptr);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
