@@ -18,11 +18,61 @@ struct SelState {      // per image, between the two passes
   int64_t rem_lo, rem_hi;   // ranks inside those bins
 };
 
+__device__ __forceinline__ void finish(ImgPar* p, int lo, int hi) {
+  p->lo = lo;
+  p->hi = hi;
+  p->degen = (hi == lo) ? 1 : 0;
+  p->inv = (hi == lo) ? 0.0f : 1.0f / (float)(hi - lo);
+}
+
+// Smallest bin whose cumulative count exceeds `rank` (returns the rank left inside it),
+// warp-cooperative: lane l holds bins 8l .. 8l + 7 (two 16-byte loads), a warp
+// scan of the lane sums finds the lane whose range holds `rank`, that lane walks its 8
+// bins (a serial 256-bin walk is 256 dependent loads: ~14 us for one image).
+__device__ __forceinline__ int select_bin_warp(const uint32_t* h, int64_t rank, int64_t* rem) {
+  const int lane = threadIdx.x & 31;
+  const uint4 a = reinterpret_cast<const uint4*>(h)[2 * lane], c = reinterpret_cast<const uint4*>(h)[2 * lane + 1];
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  int64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sum += v[i];
+  int64_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int64_t excl = incl - sum;
+  const uint32_t m = __ballot_sync(0xffffffffu, incl > rank);   // lanes past the rank
+  int bin = 255;
+  int64_t r = 0;
+  if (m) {
+    const int src = __ffs(m) - 1;
+    if (lane == src) {
+      int64_t cum = excl;
+      bin = 8 * lane + 7;
+      for (int i = 0; i < 8; ++i) {
+        if (cum + v[i] > rank) { bin = 8 * lane + i; break; }
+        cum += v[i];
+      }
+      r = rank - cum;
+    }
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    r = __shfl_sync(0xffffffffu, r, src);
+  }
+  *rem = r;
+  return bin;
+}
+
 // Pass 1: 256-bin histogram of (u8 value) or (u16 value >> 8).
 // Pass 2 (u16 only, second=true): low-byte histograms of the two selected bins.
-template <int BPP, bool SECOND>
+// SELECT (u8): the image's last CTA to flush (a ticket after hist[b]'s 256 bins, zeroed
+// with the histogram) selects the two ranks itself, so percentiles take one launch.
+template <int BPP, bool SECOND, bool SELECT = false>
 __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images, Shape s, int rows_per_cta,
-                                              uint32_t* __restrict__ hist, const SelState* __restrict__ sel) {
+                                              uint32_t* __restrict__ hist, const SelState* __restrict__ sel,
+                                              RankPar rk = RankPar{}, ImgPar* __restrict__ par = nullptr,
+                                              uint32_t* __restrict__ ticket = nullptr) {
   constexpr int NH = SECOND ? 2 : 1;
   __shared__ uint32_t sh[8][NH * 256];
   const int b = blockIdx.y;
@@ -88,52 +138,21 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
     for (int w = 0; w < 8; ++w) c += sh[w][i];
     if (c) atomicAdd(&hist[(int64_t)b * (NH * 256) + i], c);
   }
-}
-
-__device__ __forceinline__ void finish(ImgPar* p, int lo, int hi) {
-  p->lo = lo;
-  p->hi = hi;
-  p->degen = (hi == lo) ? 1 : 0;
-  p->inv = (hi == lo) ? 0.0f : 1.0f / (float)(hi - lo);
-}
-
-// Smallest bin whose cumulative count exceeds `rank` (returns the rank left inside it),
-// warp-cooperative: lane l holds bins 8l .. 8l + 7 (two 16-byte loads), a warp
-// scan of the lane sums finds the lane whose range holds `rank`, that lane walks its 8
-// bins (a serial 256-bin walk is 256 dependent loads: ~14 us for one image).
-__device__ __forceinline__ int select_bin_warp(const uint32_t* h, int64_t rank, int64_t* rem) {
-  const int lane = threadIdx.x & 31;
-  const uint4 a = reinterpret_cast<const uint4*>(h)[2 * lane], c = reinterpret_cast<const uint4*>(h)[2 * lane + 1];
-  const uint32_t v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-  int64_t sum = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) sum += v[i];
-  int64_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int64_t excl = incl - sum;
-  const uint32_t m = __ballot_sync(0xffffffffu, incl > rank);   // lanes past the rank
-  int bin = 255;
-  int64_t r = 0;
-  if (m) {
-    const int src = __ffs(m) - 1;
-    if (lane == src) {
-      int64_t cum = excl;
-      bin = 8 * lane + 7;
-      for (int i = 0; i < 8; ++i) {
-        if (cum + v[i] > rank) { bin = 8 * lane + i; break; }
-        cum += v[i];
-      }
-      r = rank - cum;
+  if (SELECT) {
+    __shared__ int last;
+    __threadfence();   // this CTA's bins are in L2 before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&ticket[b], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+      __threadfence();
+      const uint32_t* h = hist + (int64_t)b * 256;   // every CTA's atomics have landed (L2; not in this L1)
+      int64_t rl, rh;
+      const int bl = select_bin_warp(h, rk.rank_lo, &rl);
+      const int bh = select_bin_warp(h, rk.rank_hi, &rh);
+      if (threadIdx.x == 0) finish(&par[b], bl, bh);
     }
-    bin = __shfl_sync(0xffffffffu, bin, src);
-    r = __shfl_sync(0xffffffffu, r, src);
   }
-  *rem = r;
-  return bin;
 }
 
 // One warp per image: select the two ranks in the 256-bin histogram(s).

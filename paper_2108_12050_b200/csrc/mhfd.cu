@@ -159,7 +159,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
   L.par = take(sizeof(ImgPar) * B);
   L.sel = take(sizeof(SelState) * B);
-  L.hist1 = take(sizeof(uint32_t) * 256 * B);
+  L.hist1 = take(sizeof(uint32_t) * 257 * B);   // 256 bins per image, then per-image tickets (u8 select)
   L.hist2 = take(sizeof(uint32_t) * 512 * B);
   L.fimg = take(sizeof(float) * plane * B);
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
@@ -337,7 +337,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   rp.npx = N;
   rp.rank_lo = std::min<int64_t>((int64_t)std::floor((double)c->p.sat_low * (double)N), N - 1);
   rp.rank_hi = N - 1 - std::min<int64_t>((int64_t)std::floor((double)c->p.sat_high * (double)N), N - 1);
-  cudaError_t e = bpp == 4 ? cudaSuccess : cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 256 * B, st);
+  cudaError_t e = bpp == 4 ? cudaSuccess : cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 257 * B, st);
   if (e == cudaSuccess && bpp >= 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset hist");
   // ~2 CTAs per SM of rows (fewer, fuller CTAs: each flushes 256 global atomics)
@@ -355,11 +355,9 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     k_select_f32<3><<<(B + 3) / 4, 128, 0, st>>>(h2, rp, sel, par, B);
     LAUNCH_CHECK("k_hist_f32 / k_select_f32");
     launches += 7;
-  } else if (bpp == 1) {
-    k_hist<1, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
+  } else if (bpp == 1) {   // histogram + select in one launch (the image's last CTA selects)
+    k_hist<1, false, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel, rp, par, h1 + 256 * B);
     LAUNCH_CHECK("k_hist");
-    k_select1<1><<<(B + 3) / 4, 128, 0, st>>>(h1, rp, sel, par, B);
-    LAUNCH_CHECK("k_select1");
   } else {
     k_hist<2, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
     LAUNCH_CHECK("k_hist");
