@@ -357,6 +357,8 @@ def other_configs(dev) -> dict:
         out[name] = {"size": size, "dtype": f"u{bits}", "sigma": list(sig), "scales": n, "schedule": det.schedule(
             f"u{bits}"), "device_ms": dms, "host_visible_ms": hms, "MPix_per_s_device": size * size / dms / 1e3,
             "score": score}
+        if name in ("C2", "C3"):   # the same call replayed from a CUDA graph (launch gaps gone)
+            out[name]["graph"] = graph_times(det, img.unsqueeze(0).contiguous(), score)
     out["C3_bands_1gpu"] = band_times(dev)
     out["C5_bands_1gpu"] = band_times(dev, c5=True)
     out["downsample_f2"] = downsample_times(dev)
@@ -371,6 +373,37 @@ def other_configs(dev) -> dict:
                      "MPix_per_s_device": SIZE * SIZE / dms / 1e3, "score": score,
                      "fp32_tflops_direct": fpp * SIZE * SIZE / (dms * 1e-3) / 1e12}
     return out
+
+
+def graph_times(det, img, ref: float) -> dict:
+    """One focus_score call captured in a CUDA graph (the call is stream-ordered with no
+    host synchronisation, so it captures whole) and replayed: device time (CUDA events)
+    and host-visible time (replay + synchronize), medians of 50."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        det.focus_score(img)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        out = det.focus_score(img)
+    g.replay()
+    torch.cuda.synchronize()
+    assert float(out[0]) == ref, "graph replay score differs"
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(5):
+        g.replay()
+    d, w = [], []
+    for _ in range(50):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        w.append((time.perf_counter() - t0) * 1e3)
+        d.append(e0.elapsed_time(e1))
+    return {"device_ms": statistics.median(d), "host_visible_ms": statistics.median(w),
+            "note": "device-resident image; torch.cuda.CUDAGraph replay of one mhfd_focus_score call"}
 
 
 def downsample_times(dev) -> dict:
