@@ -808,3 +808,25 @@ def test_sharded_pruning_certificate(size, G):
             assert ncert == G and tot_kept == k_full
         full = det.debug_dump(img, dog=False, cands=True)
         assert tot_n == int(full["ncand"][0])
+
+
+def test_focus_score_cuda_graph_capture():
+    """The whole mhfd_focus_score call is stream-ordered with no host synchronisation, so
+    it captures in a CUDA graph; replays give the eager result, also after the input is
+    overwritten in place (the graph reads the buffer, not a snapshot)."""
+    imgs = [synth.em_tile(1024, 1024, 1000 + g, defocus=1.0 * g, dose=300.0, device="cuda") for g in range(2)]
+    det = mhfd.Detector(1024, 1024, threshold=0.09, overlap=0.5, **C3)
+    ref = [float(det.focus_score(im[None])[0]) for im in imgs]
+    buf = imgs[0][None].clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        det.focus_score(buf)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        out = det.focus_score(buf)
+    for k in (0, 1, 0):
+        buf.copy_(imgs[k][None])
+        g.replay()
+        torch.cuda.synchronize()
+        assert float(out[0]) == ref[k], (k, float(out[0]), ref[k])
