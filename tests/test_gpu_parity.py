@@ -767,8 +767,8 @@ def test_tc2_batch_ragged_rows_and_degenerate():
     P.assert_score(int(cnt[7]), ref["count"])
 
 
-@pytest.mark.parametrize("size,G", [(1024, 2), (1024, 3), (4096, 8)])
-def test_sharded_pruning_certificate(size, G):
+@pytest.mark.parametrize("size,G,bits", [(1024, 2, 8), (1024, 3, 8), (4096, 8, 8), (1024, 3, 16)])
+def test_sharded_pruning_certificate(size, G, bits):
     """f2 sharded pruning (mhfd_prune_band; SURVEY §8(f) f2 "border-blob exchange"), the
     G ranks run one after another on this GPU.  (1) Synchronous rounds decide exactly
     like the default rounds: the whole image as one band (no truncated edge, certificate
@@ -779,8 +779,14 @@ def test_sharded_pruning_certificate(size, G):
     EM tiles and the band counts sum to the image's count; the band candidate counts sum
     to the image's candidate count."""
     from paper_2108_12050_b200.dist import band_rows, halo_rows
-    img = synth.em_tile(size, size, 1004, defocus=0.5, dose=300.0, device="cuda")
-    det = mhfd.Detector(size, size, threshold=0.09, **C3)
+    if bits == 8:
+        img = synth.em_tile(size, size, 1004, defocus=0.5, dose=300.0, device="cuda")
+        det = mhfd.Detector(size, size, threshold=0.09, **C3)
+    else:   # u16 on k_tc2 at sigma 1-20 (R_max 100): the large-radius band path
+        a = synth.em_tile_np(size, size, 1009, defocus=0.5, dose=300.0, bits=16)
+        img = torch.from_numpy(a.astype(np.int32)).cuda().to(torch.uint16)
+        det = mhfd.Detector(size, size, 1.0, 20.0, 12, threshold=0.1 * 19.0 / 12)
+        assert det.schedule("u16") == "k_tc2"
     blobs, cnt, _ = det.detect(img)
     torch.cuda.synchronize()
     k_full = int(cnt[0])
