@@ -49,6 +49,7 @@ __device__ __forceinline__ uint8_t st_enc(uint8_t d, int round, int sync) {
   return sync ? (uint8_t)(d | (min(round, 63) << 2)) : d;
 }
 constexpr int kChunk = 256;
+constexpr int kPruneSmemB = 128;   // batches whose prefixes every k_prune CTA computes itself
 
 struct PruneArgs {
   int B, W, H;
@@ -235,27 +236,48 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   __shared__ int32_t red[8];
   __shared__ int32_t wpre[8];
 
-  // phase 0: per-image prefixes (one thread; B is small)
-  if (gtid == 0) {
+  // phase 0: per-image prefixes of the candidate and chunk counts.  For batches up to
+  // kPruneSmemB every CTA computes them itself into shared memory (no grid barrier: one
+  // of the ~8 that bound a single tile's latency); larger batches use one thread and
+  // the global copy.  The counters are reset here; their first use is two barriers on.
+  __shared__ int64_t s_off[2][kPruneSmemB + 1];
+  const bool local_off = a.B <= kPruneSmemB;
+  if (gtid == 0 || (local_off && threadIdx.x == 0)) {
     int64_t o = 0, c = 0;
     for (int b = 0; b < a.B; ++b) {
-      a.img_off[b] = o;
-      a.chunk_off[b] = c;
+      if (gtid == 0) {
+        a.img_off[b] = o;
+        a.chunk_off[b] = c;
+      }
+      if (local_off) {
+        s_off[0][b] = o;
+        s_off[1][b] = c;
+      }
       const int64_t n = min((int64_t)a.ncand[b], a.cap);
       o += n;
       c += (n + kChunk - 1) / kChunk;
     }
-    a.img_off[a.B] = o;
-    a.chunk_off[a.B] = c;
-    a.counters[0] = a.counters[1] = a.counters[2] = 0;
-    a.counters[3] = 0;
-    a.counters[4] = 0;
-    if (PRUNE_STAMPS) a.counters[8] = 0;
+    if (gtid == 0) {
+      a.img_off[a.B] = o;
+      a.chunk_off[a.B] = c;
+      a.counters[0] = a.counters[1] = a.counters[2] = 0;
+      a.counters[3] = 0;
+      a.counters[4] = 0;
+      a.counters[5] = 0;
+      if (PRUNE_STAMPS) a.counters[8] = 0;
+    }
+    if (local_off) {
+      s_off[0][a.B] = o;
+      s_off[1][a.B] = c;
+    }
   }
-  grid.sync();
+  if (local_off) __syncthreads();
+  else grid.sync();
   PSTAMP();
-  const int64_t total = a.img_off[a.B];
-  const int64_t nchunks = a.chunk_off[a.B];
+  const int64_t* img_off = local_off ? s_off[0] : a.img_off;
+  const int64_t* chunk_off = local_off ? s_off[1] : a.chunk_off;
+  const int64_t total = img_off[a.B];
+  const int64_t nchunks = chunk_off[a.B];
 
   // phase 1: row index rowstart[b][y] (first candidate of row >= y), by scatter from the
   // raster-sorted list: candidate k (and a sentinel k = n at row H) owns the entries
@@ -266,11 +288,11 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     int lo = 0, hi = a.B;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (a.img_off[mid] + mid <= g) lo = mid; else hi = mid;
+      if (img_off[mid] + mid <= g) lo = mid; else hi = mid;
     }
     const int b = lo;
-    const int64_t k = g - a.img_off[b] - b;
-    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const int64_t k = g - img_off[b] - b;
+    const int64_t n = img_off[b + 1] - img_off[b];
     const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
     const int y = k < n ? C[k].y : a.H, yp = k > 0 ? C[k - 1].y : -1;
     int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
@@ -357,8 +379,8 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         __syncwarp();
         bool blocked = false, rem = false;
         if (in) {
-          b = image_of(a.img_off, a.B, g);
-          k = g - a.img_off[b];
+          b = image_of(img_off, a.B, g);
+          k = g - img_off[b];
           rem = scan_rows(
               a, b, k, gl, G, &blocked,
               [&](int q) {
@@ -402,8 +424,8 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         int nq = 0, qs[kNbMax] = {0, 0, 0, 0, 0, 0};
         uint8_t d = kKept;
         if (in) {
-          b = image_of(a.img_off, a.B, g);
-          k = g - a.img_off[b];
+          b = image_of(img_off, a.B, g);
+          k = g - img_off[b];
           d = decide_collect(a, b, k, &nq, qs);
           if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, st_enc(d, 0, a.sync));
         }
@@ -444,8 +466,8 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         for (int64_t i = gtid; i < nwl; i += gsize) {
           const int4 r0 = a.wl[2 * i];
           const int64_t g = r0.x;
-          const int b = image_of(a.img_off, a.B, g);
-          const int64_t k = g - a.img_off[b];
+          const int b = image_of(img_off, a.B, g);
+          const int64_t k = g - img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
           if ((__ldcg(sp) & 3u) != kUndecided) continue;
           const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], round) : decide(a, b, k, round);
@@ -453,8 +475,8 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         }
       } else {
         for (int64_t g = gtid; g < total; g += gsize) {
-          const int b = image_of(a.img_off, a.B, g);
-          const int64_t k = g - a.img_off[b];
+          const int b = image_of(img_off, a.B, g);
+          const int64_t k = g - img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
           if ((__ldcg(sp) & 3u) != kUndecided) continue;
           const uint8_t d = decide(a, b, k, round);
@@ -474,9 +496,9 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   // phase 3: kept count per chunk of 256 candidates
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const int b = image_of(a.chunk_off, a.B, c);
-    const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
-    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const int b = image_of(chunk_off, a.B, c);
+    const int64_t k = (c - chunk_off[b]) * kChunk + threadIdx.x;
+    const int64_t n = img_off[b + 1] - img_off[b];
     const bool kept = k < n && (__ldcg(a.st + (int64_t)b * a.cap + k) & 3u) == kKept;
     const int cnt = __popc(__ballot_sync(0xffffffffu, kept));
     if (lane == 0) red[warp] = cnt;
@@ -488,24 +510,38 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     }
     __syncthreads();
   }
-  grid.sync();
+  // Without an output list (focus scores) phase 4 runs in the CTA that finishes phase 3
+  // last (a ticket instead of a grid barrier); with one, every warp of the grid scans.
+  int64_t gw = gtid >> 5, nw = gsize >> 5;
+  if (a.blobs) {
+    grid.sync();
+  } else {
+    __shared__ int last_cta;
+    __threadfence();   // this CTA's chunk counts are visible before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last_cta = atomicAdd(&a.counters[5], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last_cta) return;
+    __threadfence();
+    gw = warp;
+    nw = blockDim.x >> 5;
+  }
   PSTAMP();
 
   // phase 4: per-image exclusive scan over chunks (one warp per image)
   {
-    const int64_t gw = gtid >> 5, nw = gsize >> 5;
     for (int64_t b = gw; b < a.B; b += nw) {
       int64_t run = 0;
-      for (int64_t c0 = a.chunk_off[b]; c0 < a.chunk_off[b + 1]; c0 += 32) {
+      for (int64_t c0 = chunk_off[b]; c0 < chunk_off[b + 1]; c0 += 32) {
         const int64_t c = c0 + lane;
-        const int v = c < a.chunk_off[b + 1] ? __ldcg(a.chunk_cnt + c) : 0;
+        const int v = c < chunk_off[b + 1] ? __ldcg(a.chunk_cnt + c) : 0;
         int x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, x, o);
           if (lane >= o) x += y;
         }
-        if (c < a.chunk_off[b + 1]) a.chunk_pos[c] = (int32_t)(run + x - v);
+        if (c < chunk_off[b + 1]) a.chunk_pos[c] = (int32_t)(run + x - v);
         run += __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) {
@@ -525,9 +561,9 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
 
   // phase 5: write kept blobs in (y, x, scale) order
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const int b = image_of(a.chunk_off, a.B, c);
-    const int64_t k = (c - a.chunk_off[b]) * kChunk + threadIdx.x;
-    const int64_t n = a.img_off[b + 1] - a.img_off[b];
+    const int b = image_of(chunk_off, a.B, c);
+    const int64_t k = (c - chunk_off[b]) * kChunk + threadIdx.x;
+    const int64_t n = img_off[b + 1] - img_off[b];
     const bool kept = k < n && (__ldcg(a.st + (int64_t)b * a.cap + k) & 3u) == kKept;
     const uint32_t m = __ballot_sync(0xffffffffu, kept);
     if (lane == 0) red[warp] = __popc(m);
