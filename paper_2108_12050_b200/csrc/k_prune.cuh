@@ -66,6 +66,8 @@ struct PruneArgs {
   int n;                    // DoG planes
   uint8_t* st;              // B x cap
   int32_t* rowstart;        // B x (H + 1): first candidate of each row
+  const int32_t* segoff;    // nullable: NMS segment offsets (whole-row 1024-pixel segments) = row starts
+  int nseg, spr;            // segments per image, per row
   int cs_shift;             // cell edge cs = 1 << cs_shift (>= every dmax)
   int ncx, nbands;          // ceil(W / cs) cells per band, ceil(H / cs) bands
   int32_t* cellstart;       // B x nbands x (ncx + 1): first crec index of cell (band, cx)
@@ -282,7 +284,11 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   // phase 1: row index rowstart[b][y] (first candidate of row >= y), by scatter from the
   // raster-sorted list: candidate k (and a sentinel k = n at row H) owns the entries
   // between its predecessor's row and its own, so each entry is written once.
-  for (int64_t g = gtid; g < total + a.B; g += gsize) {
+  // With the NMS's segment offsets (whole-row segments: row y starts at segoff[y spr])
+  // the row index is already there: phase 1 and its barrier are skipped and phase 1b
+  // initialises the states.
+  const bool seg_rows = a.segoff != nullptr && a.prune;
+  for (int64_t g = seg_rows ? total + a.B : gtid; g < total + a.B; g += gsize) {
     // g enumerates, per image, candidates 0..n (n = sentinel): image b holds entries
     // [img_off[b] + b, img_off[b+1] + b + 1)
     int lo = 0, hi = a.B;
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     for (int yy = yp + 1; yy <= y; ++yy) rs[yy] = (int32_t)k;
     if (k < n) a.st[(int64_t)b * a.cap + k] = a.prune ? kUndecided : kKept;
   }
-  grid.sync();
+  if (!seg_rows) grid.sync();
   PSTAMP();
 
   // phase 1b: cell index.  Band (b, j) = rows [j cs, (j+1) cs) = the contiguous range
@@ -311,9 +317,15 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     const int cs = 1 << a.cs_shift;
     for (int64_t item = blockIdx.x; item < (int64_t)a.B * a.nbands; item += gridDim.x) {
       const int b = (int)(item / a.nbands), j = (int)(item % a.nbands);
-      const int32_t* rs = a.rowstart + (int64_t)b * (a.H + 1);
-      const int k0 = rs[j * cs], k1 = rs[min(a.H, (j + 1) * cs)];
+      const int64_t nb_ = img_off[b + 1] - img_off[b];
+      auto row_start = [&](int y) -> int {
+        if (!seg_rows) return a.rowstart[(int64_t)b * (a.H + 1) + y];
+        return y >= a.H ? (int)nb_ : (int)min((int64_t)a.segoff[(int64_t)b * a.nseg + (int64_t)y * a.spr], nb_);
+      };
+      const int k0 = row_start(j * cs), k1 = row_start(min(a.H, (j + 1) * cs));
       const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
+      if (seg_rows)
+        for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) a.st[(int64_t)b * a.cap + k] = kUndecided;
       for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cell[c] = 0;
       __syncthreads();
       for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&cell[C[k].x >> a.cs_shift], 1);

@@ -671,7 +671,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
 
 mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_blob* blobs, int32_t blob_cap,
                       int32_t* counts, double* scores, int32_t* flags, cudaStream_t st, int& launches,
-                      cudaEvent_t* ev, const mhfd_blob* ext_cand = nullptr, int sync = 0) {
+                      cudaEvent_t* ev, const mhfd_blob* ext_cand = nullptr, int sync = 0, bool seg_rows = false) {
   PruneArgs pa;
   memset(&pa, 0, sizeof(pa));
   pa.B = B;
@@ -690,6 +690,11 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   pa.n = c->n;
   pa.st = reinterpret_cast<uint8_t*>(ws + L.st);
   pa.rowstart = reinterpret_cast<int32_t*>(ws + L.rowstart);
+  // the NMS fast path's segment offsets are row starts when segments are whole-row pieces
+  pa.segoff = (seg_rows && !ext_cand && c->p.nms == MHFD_NMS_PAPER && c->p.width % kSeg == 0)
+                  ? reinterpret_cast<const int32_t*>(ws + L.segoff) : nullptr;
+  pa.nseg = nseg_of(c);
+  pa.spr = c->p.width / kSeg;
   pa.cs_shift = c->cs_shift;
   pa.ncx = c->ncx;
   pa.nbands = c->nbands;
@@ -1257,7 +1262,7 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
     cudaEvent_t* ev = next_timing(c);
     s = run_front(c, dst, dtype, nb, pitch_bytes, ws, L, nullptr, st, launches, ev);
     if (s != MHFD_OK) return s;
-    s = run_prune(c, nb, ws, L, nullptr, 0, d_ct, d_sc, nullptr, st, launches, ev);
+    s = run_prune(c, nb, ws, L, nullptr, 0, d_ct, d_sc, nullptr, st, launches, ev, nullptr, 0, true);
     if (s != MHFD_OK) return s;
     e = cudaEventRecord(c->ev_free[h], st);
     if (e == cudaSuccess)
@@ -1493,7 +1498,7 @@ mhfd_status mhfd_detect_batch(mhfd_ctx* c, const void* d_images, int32_t dtype, 
   s = run_front(c, d_images, dtype, batch, pitch_bytes, ws, L, nullptr, st, launches, ev);
   if (s != MHFD_OK) return s;
   s = run_prune(c, batch, ws, L, d_blobs ? d_blobs : nullptr, blob_capacity, d_counts, nullptr, d_flags, st,
-                launches, ev);
+                launches, ev, nullptr, 0, true);
   if (s != MHFD_OK) return s;
   g_launches = launches;
   return MHFD_OK;
@@ -1513,7 +1518,7 @@ mhfd_status mhfd_focus_score(mhfd_ctx* c, const void* d_images, int32_t dtype, i
   cudaEvent_t* ev = next_timing(c);
   s = run_front(c, d_images, dtype, batch, pitch_bytes, ws, L, nullptr, st, launches, ev);
   if (s != MHFD_OK) return s;
-  s = run_prune(c, batch, ws, L, nullptr, 0, d_counts, d_scores, nullptr, st, launches, ev);
+  s = run_prune(c, batch, ws, L, nullptr, 0, d_counts, d_scores, nullptr, st, launches, ev, nullptr, 0, true);
   if (s != MHFD_OK) return s;
   g_launches = launches;
   return MHFD_OK;
