@@ -33,6 +33,11 @@
  *    enqueued on `stream`; outputs are valid once the caller synchronises it.
  *    Launch failures return MHFD_ERR_CUDA; asynchronous faults surface at the
  *    caller's synchronisation.
+ *  - CUDA graphs: mhfd_detect_batch, mhfd_focus_score and mhfd_debug_dump enqueue only
+ *    kernels, memsets and device-to-device copies and never synchronise the host, so a
+ *    call can be captured into a CUDA graph and replayed (on new contents of the same
+ *    buffers); make one call outside the capture first (it sets kernel attributes).
+ *    (tests/test_gpu_parity.py::test_focus_score_cuda_graph_capture)
  *  - Thread safety: a context is immutable after mhfd_create; concurrent calls
  *    with distinct workspaces (and outputs) on distinct streams are safe.
  *  - Determinism: results are bitwise reproducible run to run and independent
