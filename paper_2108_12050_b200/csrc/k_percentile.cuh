@@ -86,6 +86,35 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
   const int y1 = min(s.H, y0 + rows_per_cta);
   const int row_bytes = s.W * BPP;
   const int nvec = (row_bytes + 15) >> 4;
+  if (!SECOND && (row_bytes & 15) == 0 && nvec <= (int)blockDim.x) {
+    // whole-vector rows of at most one vector per thread (u8 up to 4096 wide, u16 up to
+    // 2048): four rows' loads in flight per thread before their atomics, so a CTA's
+    // rows_per_cta rows are not a chain of dependent load latencies (8 x 4096^2: 0.10 ms)
+    const int v = threadIdx.x;
+    uint32_t* hw = sh[warp];
+    for (int y = y0; y < y1; y += 4) {
+      uint4 q[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        q[r] = (v < nvec && y + r < y1) ? __ldg(reinterpret_cast<const uint4*>(img + (int64_t)(y + r) * s.pitch) + v)
+                                        : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (v >= nvec || y + r >= y1) continue;
+        const uint32_t wds[4] = {q[r].x, q[r].y, q[r].z, q[r].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (BPP == 1) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicAdd(hw + ((wds[k] >> (8 * j)) & 255u), 1u);
+          } else {
+            atomicAdd(hw + ((wds[k] >> 8) & 255u), 1u);
+            atomicAdd(hw + (wds[k] >> 24), 1u);
+          }
+        }
+      }
+    }
+  } else
   for (int y = y0; y < y1; ++y) {
     const uint4* row = reinterpret_cast<const uint4*>(img + (int64_t)y * s.pitch);
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
