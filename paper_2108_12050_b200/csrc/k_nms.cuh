@@ -419,6 +419,97 @@ __device__ __forceinline__ void nms_halo(NmsRow& r, int lane) {
   if (lane != 31) r.v[9] = dn;
 }
 
+// Interior warps of k_nms_roll (all NR + 2 rows inside the image, NR output rows): no
+// per-row validity tests, a pointer walk down the rows, and a fully unrolled row loop
+// without early exits, so the three live rows rotate by renaming instead of ~60
+// register moves per row (ncu: the generic loop issued ~250 instructions per 8-pixel
+// row step, a quarter of them IMAD.MOV).
+#ifndef NMS_FAST
+#define NMS_FAST 1
+#endif
+template <int NR>
+__device__ __forceinline__ void nms_roll_fast(const NmsArgs& a, const float* __restrict__ vb,
+                                              const uint8_t* __restrict__ ib, int y0, int xseg, int lane,
+                                              mhfd_blob* __restrict__ sl0, int spr, int& parked) {
+  const int W = a.W;
+  const float tau = a.tau;
+  const bool strict = a.strict != 0;
+  auto load = [&](const float* q, bool lft, bool rgt, float (&r)[10]) {
+    const float4 p0 = __ldg(reinterpret_cast<const float4*>(q));
+    const float4 p1 = __ldg(reinterpret_cast<const float4*>(q + 4));
+    r[1] = p0.x; r[2] = p0.y; r[3] = p0.z; r[4] = p0.w;
+    r[5] = p1.x; r[6] = p1.y; r[7] = p1.z; r[8] = p1.w;
+    r[0] = lft ? __ldg(q - 1) : -INFINITY;   // lane 0 only (others take the shuffle)
+    r[9] = rgt ? __ldg(q + 8) : -INFINITY;   // lane 31 only
+  };
+  auto halo = [&](float (&r)[10]) {
+    const float up = __shfl_up_sync(0xffffffffu, r[8], 1);
+    const float dn = __shfl_down_sync(0xffffffffu, r[1], 1);
+    if (lane != 0) r[0] = up;
+    if (lane != 31) r[9] = dn;
+  };
+#pragma unroll 1
+  for (int step = 0; step < kSeg / 256; ++step) {
+    const int x = xseg + step * 256 + 8 * lane;
+    const bool lft = lane == 0 && x > 0, rgt = lane == 31 && x + 8 < W;
+    const float* q = vb + (int64_t)(y0 - 1) * W + x;
+    float u[10], c[10], d[10];
+    load(q, lft, rgt, u);
+    load(q + W, lft, rgt, c);
+    load(q + 2 * W, lft, rgt, d);
+    halo(u);
+    halo(c);
+#pragma unroll
+    for (int o = 0; o < NR; ++o) {
+      float nx[10];
+      if (o + 1 < NR) load(q + (int64_t)(o + 3) * W, lft, rgt, nx);
+      halo(d);
+      float V[10];
+#pragma unroll
+      for (int j = 0; j < 10; ++j) V[j] = fmaxf(u[j], d[j]);
+      uint32_t bb = 0;
+#pragma unroll
+      for (int k = 1; k < 9; ++k) {
+        const float m = fmaxf(fmaxf(V[k - 1], V[k]), fmaxf(V[k + 1], fmaxf(c[k - 1], c[k + 1])));
+        const bool ok = (c[k] > tau) && (strict ? (c[k] > m) : (c[k] >= m));
+        bb |= (uint32_t)ok << (k - 1);
+      }
+      const int n = __popc(bb);
+      int incl = n;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, sh);
+        if (lane >= sh) incl += t;
+      }
+      int pos = __shfl_sync(0xffffffffu, parked, o) + incl - n;
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == o) parked += tot;
+      if (bb) {
+        const int y = y0 + o;
+        const uint8_t* irow = ib + (int64_t)y * W;
+        mhfd_blob* sl = sl0 + (int64_t)o * spr * kSlab;
+        uint32_t m = bb;
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          if (pos < kSlab) {
+            mhfd_blob r;
+            r.x = x + k; r.y = y; r.scale = irow[x + k]; r.response = c[1 + k];
+            sl[pos] = r;
+          }
+          ++pos;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 10; ++j) {
+        u[j] = c[j];
+        c[j] = d[j];
+        if (o + 1 < NR) d[j] = nx[j];
+      }
+    }
+  }
+}
+
 template <int NR>
 __global__ void __launch_bounds__(256, 3) k_nms_roll(NmsArgs a, int nseg, int32_t* __restrict__ segcnt, int row0,
                                                     int row1, mhfd_blob* __restrict__ slab) {
@@ -437,6 +528,11 @@ __global__ void __launch_bounds__(256, 3) k_nms_roll(NmsArgs a, int nseg, int32_
   const int nrow = min(NR, row1 - y0);   // output rows of this warp (ragged last group)
   auto rowp = [&](int y) -> const float* { return (y >= 0 && y < H) ? vb + (int64_t)y * W : nullptr; };
   int parked = 0;   // lane o holds the running count of segment o (NR <= 32)
+  if (NMS_FAST && nrow == NR && y0 >= 1 && y0 + NR < H) {   // warp-uniform
+    nms_roll_fast<NR>(a, vb, ib, y0, xseg, lane, slab + ((int64_t)b * nseg + seg0) * kSlab, spr, parked);
+    if (lane < nrow) segcnt[(int64_t)b * nseg + seg0 + lane * spr] = parked;
+    return;
+  }
   for (int step = 0; step < kSeg / 256; ++step) {
     const int x = xseg + step * 256 + 8 * lane;
     NmsRow u = nms_load_row(rowp(y0 - 1), x, W, lane);
