@@ -109,7 +109,9 @@ typedef enum { MHFD_DARK = 0, MHFD_BRIGHT = 1 } mhfd_polarity;
  * d_xx by zero-sum sampled second-derivative taps w2(d) = w(d)(d^2 - m2)/t^4,
  * m2 = sum_d w(d) d^2, over the same support ceil(5 t) as the blur; same sign and
  * polarity conventions as Eq. 2, responses on the LoG scale (about 1/dt times Eq. 2's).
- * LOG runs the two-pass CUDA-core schedule: width % 256 == 0 and 2n <= 62 required. */
+ * width % 256 == 0 and 2n <= 62 required.  LOG runs on "k_tc2" where it fits (periodic,
+ * height % 16 == 0, width >= its staged window), else on the two-pass CUDA-core
+ * schedule "k_rows_pair+k_cols_pair<log>". */
 typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
 
 /* Image boundary of the blur (ABI 3).  MHFD_BOUNDARY_PERIODIC: what the paper's FFT
@@ -340,8 +342,9 @@ mhfd_status mhfd_get_params(const mhfd_ctx* c, mhfd_params* out);
  * fits), "k_band" (u8, CUDA-core band schedule), "k_scale_space"
  * (generic: widths that are not multiples of 256, MHFD_SCHEDULE=generic, and DoG-plane
  * calls below R_max 96), or the two-pass schedule through an HBM row-blur intermediate:
- * "k_rows_pair+k_cols_pair" (Eq. 3 NMS, width % 256 == 0, any radius; also every
- * MHFD_RESPONSE_LOG context, named "k_rows_pair+k_cols_pair<log>"), "k_rows2+k_cols_all"
+ * "k_rows_pair+k_cols_pair" (Eq. 3 NMS, width % 256 == 0, any radius; also the
+ * MHFD_RESPONSE_LOG contexts k_tc2 does not fit, named "k_rows_pair+k_cols_pair<log>"),
+ * "k_rows2+k_cols_all"
  * (DoG planes at R_max >= 96: 3x3x3 mode, dumps, MHFD_NO_COLS_PAIR=1).  params.schedule
  * (or, with MHFD_SCHEDULE_AUTO, the environment variable MHFD_SCHEDULE=tc|band|generic
  * read at mhfd_create) selects among the applicable ones.  Static string; "none" for a

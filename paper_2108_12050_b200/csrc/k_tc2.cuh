@@ -266,7 +266,14 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
 // (tx), 6/7 table free (commit), 8.. stage full (tx), 8+kT2Stages.. stage empty (commit).
 // 18 warps: at most 5 per SM sub-partition, so 96 registers; each epilogue thread keeps
 // 56 running maxima and 56 packed argmax bytes (N = 224 rows; 256 would spill)
-template <bool DOG>
+//
+// LOG (reading R23, response = t_j^2 (d_xx + d_yy) L(., t_j)): the plan's levels are 2n
+// sub-levels, 2j with row taps w_j and column taps t_j^2 w2_j, 2j+1 with row taps
+// t_j^2 w2_j and column taps w_j, so  t_j^2 (w2 (x) w + w (x) w2) x  is the sum of the two
+// sub-levels' column products: both accumulate into one TMEM accumulator (j), and the
+// epilogue takes the response from it directly (scaled and signed by lev[2j].tdog).
+// The row pass and the slab / table producer are the DoG ones, level for sub-level.
+template <bool DOG, bool LOG = false>
 __global__ void __launch_bounds__(kT2Threads, 1)
 k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const __grid_constant__ Tc2Plan P,
            const uint8_t* __restrict__ tabs, float* __restrict__ v_out, uint8_t* __restrict__ idx_out,
@@ -313,26 +320,28 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
       for (int g = 0; g < G; ++g) {
         const int lev = g % nlev;
         const int K2 = P.lev[lev].K2, np2 = P.lev[lev].npairs2;
+        const int ga = LOG ? (g >> 1) : g;            // accumulator index (LOG: two sub-levels each)
+        const bool first = !LOG || (lev & 1) == 0;    // first product into this accumulator
         mbar_wait(&bars[4 + (g & 1)], (uint32_t)((g >> 1) & 1));
-        if (g >= 2) mbar_wait(&bars[2 + (g & 1)], (uint32_t)(((g >> 1) - 1) & 1));
+        if (first && ga >= 2) mbar_wait(&bars[2 + (ga & 1)], (uint32_t)(((ga >> 1) - 1) & 1));
         umma::fence_after();
         const int E1 = K2 / 8 - 2;
         const uint32_t thi = umma::smem_addr(tbuf + (size_t)(g & 1) * P.max_lev_bytes2);
         const uint64_t dH = umma::desc_kmajor(thi + E1 * 256, 128, 256);
         const uint64_t dL = umma::desc_kmajor(thi + np2 * 256 + E1 * 256, 128, 256);
-        const uint32_t d2 = tmem + (uint32_t)(kT2ColRows * (g & 1));
+        const uint32_t d2 = tmem + (uint32_t)(kT2ColRows * (ga & 1));
         for (int j = 0; j < K2 / 16; ++j, ++cnt) {
           const uint32_t st = cnt % kT2Stages;
           mbar_wait(&bars[8 + st], (cnt / kT2Stages) & 1u);
           umma::fence_after();
           const uint64_t aH = umma::desc_kmajor(ring0 + st * 2 * kT2SlabBytes, kT2SlabBytes / 2, 128);
           const uint64_t aL = umma::desc_kmajor(ring0 + st * 2 * kT2SlabBytes + kT2SlabBytes, kT2SlabBytes / 2, 128);
-          umma::mma_ss_w(d2, aH, dH - 32u * j, idesc, j > 0);
+          umma::mma_ss_w(d2, aH, dH - 32u * j, idesc, j > 0 || !first);
           umma::mma_ss_w(d2, aH, dL - 32u * j, idesc, 1);
           umma::mma_ss_w(d2, aL, dH - 32u * j, idesc, 1);
           umma::commit_w(&bars[8 + kT2Stages + st]);
         }
-        umma::commit_w(&bars[g & 1]);
+        if (!first || !LOG) umma::commit_w(&bars[ga & 1]);
         umma::commit_w(&bars[6 + (g & 1)]);
       }
     }
@@ -377,7 +386,60 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
     float vbest[RPW];
     uint32_t ibest[RPW / 4];
     int odeg = 0;
-    for (int g = 0; g < G; ++g) {
+    if (LOG) {   // one accumulator per plane j: the response itself
+      const int n = nlev / 2;
+      for (int ga = 0; ga < G / 2; ++ga) {
+        const int jp = ga % n;
+        int b, x0, y0;
+        tile_of(ga / n, b, x0, y0);
+        mbar_wait(&bars[ga & 1], (uint32_t)((ga >> 1) & 1));
+        umma::fence_after();
+        if (jp == 0) {
+          odeg = par[b].degen;
+#pragma unroll
+          for (int u = 0; u < RPW; ++u) vbest[u] = -INFINITY;
+#pragma unroll
+          for (int u = 0; u < RPW / 4; ++u) ibest[u] = 0u;
+        }
+        const float tf = P.lev[2 * jp].tdog * (1.f / (kTcWScale * kT2XScale));
+        const uint32_t cur = tq + kT2ColRows * (ga & 1) + RPW * wg;
+#pragma unroll
+        for (int qq = 0; qq < RPW / 8; ++qq) {
+          uint32_t a8[8];
+          umma::ld8(cur + 8 * qq, a8);
+          umma::wait_ld();
+#pragma unroll
+          for (int uu = 0; uu < 8; ++uu) {
+            const int u = 8 * qq + uu;
+            const float D = tf * __uint_as_float(a8[uu]);
+            if (DOG) {
+              const int y = y0 + RPW * wg + u;
+              if (y < H) dog_out[((int64_t)b * n + jp) * plane + (int64_t)y * W + x0 + c] = odeg ? 0.f : D;
+            }
+            if (D > vbest[u]) {
+              vbest[u] = D;
+              const int sh = (u & 3) * 8;
+              ibest[u >> 2] = (ibest[u >> 2] & ~(0xffu << sh)) | ((uint32_t)jp << sh);
+            }
+          }
+        }
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) t2_arrive(&bars[2 + (ga & 1)]);
+        if (jp == n - 1 && v_out) {
+#pragma unroll
+          for (int u = 0; u < RPW; ++u) {
+            const int y = y0 + RPW * wg + u;
+            if (y < H) {
+              const int64_t pidx = (int64_t)b * plane + (int64_t)y * W + x0 + c;
+              v_out[pidx] = odeg ? 0.f : vbest[u];
+              idx_out[pidx] = odeg ? (uint8_t)0 : (uint8_t)((ibest[u >> 2] >> ((u & 3) * 8)) & 0xffu);
+            }
+          }
+        }
+      }
+    }
+    for (int g = 0; g < (LOG ? 0 : G); ++g) {
       const int lev = g % nlev;
       int b, x0, y0;
       tile_of(g / nlev, b, x0, y0);

@@ -94,11 +94,11 @@ struct Layout {
       chunkcnt, chunkpos, counters, scores, counts, rx, xtc, slab, wl, total;
 };
 
-// k_tc2 (two-pass tensor-core schedule) applies: Eq. 2 DoG, periodic, plan built, widths
+// k_tc2 (two-pass tensor-core schedule) applies: Eq. 2 DoG or LoG, periodic, plan built, widths
 // in whole 128-column tiles, heights in whole 16-row slabs, one periodic wrap of the
 // staged row window
-bool tc2_fit(const mhfd_ctx* c) {
-  return c->tc2 && c->d_tc2tab && c->band_enabled && c->p.response == MHFD_RESPONSE_DOG &&
+bool tc2_fit(const mhfd_ctx* c) {   // (a LoG context's plan holds its 2n sub-levels)
+  return c->tc2 && c->d_tc2tab && c->band_enabled &&
          c->p.boundary == MHFD_BOUNDARY_PERIODIC && c->p.width % kT2Cols == 0 && c->p.height % kT2SlabRows == 0 &&
          c->p.width >= c->tc2->S;
 }
@@ -440,7 +440,8 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       }
     }
     const size_t sm1 = tc2_rows_smem(P), sm2 = tc2_cols_smem(P);
-    auto kc = tc_dog ? k_tc2_cols<true> : k_tc2_cols<false>;
+    auto kc = dogr ? (tc_dog ? k_tc2_cols<true> : k_tc2_cols<false>)
+                   : (tc_dog ? k_tc2_cols<true, true> : k_tc2_cols<false, true>);
     cudaError_t ea = cudaFuncSetAttribute(k_tc2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     if (ea == cudaSuccess) ea = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc2 attributes");
@@ -1040,18 +1041,43 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
     }
   }
   // two-pass tensor-core plan (k_tc2) and its tables
-  c->tc2 = new (std::nothrow) Tc2Plan;
-  if (c->tc2 && tc2_plan_build(*c->tc2, n + 1, R, t)) {
-    if (p->polarity == MHFD_BRIGHT)
-      for (int i = 0; i <= n; ++i) c->tc2->lev[i].tdog = -c->tc2->lev[i].tdog;
-    std::vector<std::vector<double>> wv(n + 1);
-    for (int i = 0; i <= n; ++i) {
-      double sum = 0.0;
-      for (int d = -R[i]; d <= R[i]; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
-      for (int d = -R[i]; d <= R[i]; ++d) wv[i].push_back(std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum);
+  // Eq. 2: the n + 1 Gaussian levels.  LoG (reading R23): 2n sub-levels, 2j = (rows w_j,
+  // columns t_j^2 w2_j) and 2j+1 = (rows t_j^2 w2_j, columns w_j), whose column products
+  // k_tc2_cols<., true> sums into t_j^2 (d_xx + d_yy) L(., t_j); w2 as the pair path's
+  // (zero-sum sampled second derivative), with t_j^2 folded in (tdog = the sign only)
+  const bool log_resp = p->response == MHFD_RESPONSE_LOG;
+  std::vector<int> R2;
+  std::vector<double> t2;
+  for (int i = 0; i < (log_resp ? n : n + 1); ++i)
+    for (int k = 0; k < (log_resp ? 2 : 1); ++k) {
+      R2.push_back(R[i]);
+      t2.push_back(t[i]);
     }
+  c->tc2 = new (std::nothrow) Tc2Plan;
+  if (c->tc2 && tc2_plan_build(*c->tc2, (int)R2.size(), R2.data(), t2.data())) {
+    const int nl2 = (int)R2.size();
+    std::vector<std::vector<double>> wr(nl2), wc(nl2);
+    for (int i = 0; i < (log_resp ? n : n + 1); ++i) {
+      std::vector<double> w, w2s;
+      double sum = 0.0, m2 = 0.0;
+      for (int d = -R[i]; d <= R[i]; ++d) sum += std::exp(-(double)d * d / (2.0 * t[i] * t[i]));
+      for (int d = -R[i]; d <= R[i]; ++d) {
+        w.push_back(std::exp(-(double)d * d / (2.0 * t[i] * t[i])) / sum);
+        m2 += w.back() * (double)d * d;
+      }
+      if (!log_resp) {
+        wr[i] = wc[i] = w;
+        continue;
+      }
+      for (int d = -R[i]; d <= R[i]; ++d) w2s.push_back(w[d + R[i]] * ((double)d * d - m2) / (t[i] * t[i]));
+      wr[2 * i] = wc[2 * i + 1] = w;
+      wc[2 * i] = wr[2 * i + 1] = w2s;
+      c->tc2->lev[2 * i].tdog = c->tc2->lev[2 * i + 1].tdog = 1.f;
+    }
+    if (p->polarity == MHFD_BRIGHT)
+      for (int i = 0; i < nl2; ++i) c->tc2->lev[i].tdog = -c->tc2->lev[i].tdog;
     std::vector<uint8_t> tabh((size_t)c->tc2->tab_bytes);
-    tc2_fill_tables(*c->tc2, wv, tabh.data());
+    tc2_fill_tables(*c->tc2, wr, wc, tabh.data());
     int prev = 0;
     cudaGetDevice(&prev);
     const bool ok = cudaSetDevice(p->device) == cudaSuccess &&
@@ -1279,7 +1305,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (!c) return "none";
   const int W = c->p.width, H = c->p.height;
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
-  if (c->p.response == MHFD_RESPONSE_LOG) return "k_rows_pair+k_cols_pair<log>";
+  if (c->p.response == MHFD_RESPONSE_LOG)
+    return c->band_kind == 3 && tc2_fit(c) ? "k_tc2" : "k_rows_pair+k_cols_pair<log>";
   if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
   if (c->band_kind == 3 && tc2_fit(c)) return "k_tc2";

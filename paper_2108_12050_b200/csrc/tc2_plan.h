@@ -142,15 +142,21 @@ inline void tc2_fill_pairs(uint16_t* hi, uint16_t* lo, int npairs, int K, int s,
     }
 }
 
-inline void tc2_fill_tables(const Tc2Plan& P, const std::vector<std::vector<double>>& w, uint8_t* out) {
+// Row-pass taps wr[i] and column-pass taps wc[i] of every level (the Gaussian levels of
+// Eq. 2 use the same taps in both passes; the LoG sub-levels do not, see k_tc2.cuh)
+inline void tc2_fill_tables(const Tc2Plan& P, const std::vector<std::vector<double>>& wr,
+                            const std::vector<std::vector<double>>& wc, uint8_t* out) {
   std::memset(out, 0, (size_t)P.tab_bytes);
   for (int i = 0; i < P.nlev; ++i) {
     const Tc2Level& L = P.lev[i];
     uint16_t* h1 = reinterpret_cast<uint16_t*>(out + L.tab_off);
-    tc2_fill_pairs(h1, h1 + L.npairs * 128, L.npairs, L.K, L.s, L.R, w[i]);
+    tc2_fill_pairs(h1, h1 + L.npairs * 128, L.npairs, L.K, L.s, L.R, wr[i]);
     uint16_t* h2 = reinterpret_cast<uint16_t*>(out + L.tab_off2);
-    tc2_fill_pairs(h2, h2 + L.npairs2 * 128, L.npairs2, L.K2, L.s2, L.R, w[i]);
+    tc2_fill_pairs(h2, h2 + L.npairs2 * 128, L.npairs2, L.K2, L.s2, L.R, wc[i]);
   }
+}
+inline void tc2_fill_tables(const Tc2Plan& P, const std::vector<std::vector<double>>& w, uint8_t* out) {
+  tc2_fill_tables(P, w, w, out);
 }
 
 }  // namespace mhfd

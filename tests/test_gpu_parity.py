@@ -554,16 +554,40 @@ def test_downsample_bit_exact(dtype):
 
 
 # ---------------------------------------------------------------- LoG response (f3)
-@pytest.mark.parametrize("nms", ["paper", "26"])
-def test_log_response_full_parity(c1_img, nms):
-    """response="log" (reading R23): t_i^2 lap L(t_i) through k_rows_pair / k_cols_pair<log>
-    against the oracle's LoG stack: responses within 1e-4 of the peak, argmax, candidates,
-    pruned blobs, counts and score under the same parity rules as Eq. 2."""
+@pytest.mark.parametrize("nms,schedule", [("paper", None), ("26", None), ("paper", "band"), ("26", "band")])
+def test_log_response_full_parity(c1_img, nms, schedule):
+    """response="log" (reading R23): t_i^2 lap L(t_i) on the tensor cores (k_tc2: 2n
+    sub-levels whose column products share one accumulator) and on the CUDA-core pair
+    kernels (schedule="band") against the oracle's LoG stack: responses within 1e-4 of the
+    peak, argmax, candidates, pruned blobs, counts and score under Eq. 2's parity rules."""
     tau = 0.1   # C1's tau / dt: LoG responses are ~1/dt times Eq. 2's
-    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response="log")
+    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response="log", schedule=schedule)
     assert s["n_oracle"] > 100
-    det = mhfd.Detector(256, 256, threshold=tau, response="log", **C1)
-    assert det.schedule("u8") == "k_rows_pair+k_cols_pair<log>"
+    det = mhfd.Detector(256, 256, threshold=tau, response="log", schedule=schedule, **C1)
+    assert det.schedule("u8") == ("k_tc2" if schedule is None else "k_rows_pair+k_cols_pair<log>")
+
+
+@pytest.mark.parametrize("bright", [False, True])
+def test_log_response_k_tc2_multi_tile(bright):
+    """LoG on k_tc2 over several 128-column x 224-row output tiles and NR-row row tiles
+    (1024 x 512 u16, sigma 1-10, 10 scales, both polarities): LoG planes, v / argmax and
+    the score against the oracle."""
+    cfg = dict(min_sigma=1.0, max_sigma=10.0, num_scales=10)
+    a = synth.em_tile_np(512, 1024, 1310, defocus=0.5, dose=300.0, bits=16)
+    pol = "bright" if bright else "dark"
+    det = mhfd.Detector(1024, 512, threshold=0.1, response="log", polarity=pol, **cfg)
+    assert det.schedule("u16") == "k_tc2"
+    t = torch.from_numpy(a.astype(np.int32)).cuda().to(torch.uint16)
+    d = det.debug_dump(t, dog=True, cands=False)
+    s = float(det.focus_score(t)[0])
+    torch.cuda.synchronize()
+    ref = oracle.detect(a, 1.0, 10.0, 10, 0.1, 0.5, dump=True, response="log", polarity=pol)
+    eps = P.REL_EPS * float(ref["D"].max())
+    assert float(np.abs(d["dog"][0].cpu().numpy() - ref["D"]).max()) <= eps
+    assert float(np.abs(d["v"][0].cpu().numpy() - ref["v"]).max()) <= eps
+    tie = P.scale_tie(ref["D"], eps)
+    assert np.array_equal(d["idx"][0].cpu().numpy()[~tie], ref["idx"][~tie])
+    P.assert_score(s, ref["count"])
 
 
 def test_log_response_u16_ragged_and_degenerate():
@@ -599,7 +623,7 @@ def test_two_pass_batch_chunks(response):
     batch = torch.from_numpy(np.stack(imgs).astype(np.int32)).cuda().to(torch.uint16)
     det = mhfd.Detector(512, 256, 1.0, 6.0, 5, threshold=0.1 if response == "log" else 0.1,
                         response=response)
-    assert det.schedule("u16") == ("k_tc2" if response == "dog" else "k_rows_pair+k_cols_pair<log>")
+    assert det.schedule("u16") == "k_tc2"
     blobs, cnt, _ = det.detect(batch)
     torch.cuda.synchronize()
     assert int(cnt[10]) == 0
