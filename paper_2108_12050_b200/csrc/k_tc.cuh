@@ -34,7 +34,8 @@ namespace mhfd {
 
 #ifndef TC_EXP
 #define TC_EXP 0   // performance experiments only (tools/tc_exp.py): 1 no DoG reads, 2 one DoG read, 3 no split, 4 = 1 + 3,
-                   // 5 no output writes, 6 no staging conversion
+                   // 5 no output writes, 6 no staging conversion, 7 / 8 column pass without the
+                   // A2_hi T_lo / A2_lo T_hi product (numerics: tools/precision_probe.py)
 #endif
 
 constexpr int kTcThreads = 512;
@@ -315,8 +316,8 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         TC_STAMP(g, 3 + grp);
         for (int j = 4 * grp; j < nj && j < 4 * grp + 4; ++j) {
           umma::mma_ts_w(d2, tmem + 16 * j, dH - 32u * j, idc, j > 0);
-          umma::mma_ts_w(d2, tmem + 16 * j, dL - 32u * j, idc, 1);
-          umma::mma_ts_w(d2, tmem + 16 * j + 8, dH - 32u * j, idc, 1);
+          if (TC_EXP != 7) umma::mma_ts_w(d2, tmem + 16 * j, dL - 32u * j, idc, 1);
+          if (TC_EXP != 8) umma::mma_ts_w(d2, tmem + 16 * j + 8, dH - 32u * j, idc, 1);
         }
       }
       umma::commit_w(&bars[2]);
