@@ -219,15 +219,22 @@ mhfd_status mhfd_focus_score(mhfd_ctx* c, const void* d_images, int32_t dtype, i
 
 /* End-to-end call with HOST buffers (the e2e path): h_images is batch x height
  * rows of pitch_bytes in host memory (pinned for overlap; pageable works but
- * serialises).  The batch is processed in chunks of
- *   chunk = staging_bytes / (2 * height * pitch_bytes)   images (>= 1 required):
- * chunk k+1 is copied host->device into one half of d_staging on a context-owned
- * copy stream while chunk k is processed on `stream`; each chunk's scores are
- * copied device->host into h_scores (batch doubles) and, if non-NULL, h_counts.
+ * serialises).  The batch is processed in chunks of at most
+ *   chunk = staging_bytes / (3 * height * pitch_bytes)   images (>= 1 required):
+ * d_staging holds three slots of `chunk` images, used round-robin; the next chunks
+ * are copied host->device into free slots on a context-owned copy stream while
+ * earlier ones are processed on `stream`, and each chunk's scores are copied
+ * device->host into h_scores (batch doubles) and, if non-NULL, h_counts.
+ * Back-to-back calls with the same staging buffer pipeline: a call's copies wait only
+ * for the compute that last used their slot, so they overlap the previous call's last
+ * chunks, and such a call uses whole chunks throughout; a call that finds the device
+ * idle ramps its chunks up (1, 2, 3, ... images) so compute starts after one image's
+ * copy.  The staging buffer therefore stays in use until `stream` is synchronised.
  * d_workspace must hold mhfd_workspace_bytes(c, chunk).  Outputs are valid after
- * the caller synchronises `stream`.  Uses context-owned streams/events: do not call
- * concurrently on the same context.
- * Errors: as mhfd_focus_score; WORKSPACE if the staging holds < 1 image per half. */
+ * the caller synchronises `stream` (h_scores / h_counts of a call are written by its
+ * own chunks only).  Uses context-owned streams/events: do not call concurrently on
+ * the same context.
+ * Errors: as mhfd_focus_score; WORKSPACE if the staging holds < 1 image per slot. */
 mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dtype, int32_t batch,
                                   int64_t pitch_bytes, void* d_staging, size_t staging_bytes,
                                   void* d_workspace, size_t workspace_bytes, double* h_scores,

@@ -169,11 +169,13 @@ class Detector:
                                              ptr(out["idx"]), ptr(out["cands"]), ptr(out["ncand"]), self._stream()))
         return out
 
-    def focus_score_host(self, host_images: torch.Tensor, chunk: int = 8, counts: bool = False):
+    def focus_score_host(self, host_images: torch.Tensor, chunk: int = 8, counts: bool = False, out=None):
         """End-to-end call with HOST buffers (mhfd_focus_score_host): chunked H2D copies
         from (pinned) host memory overlapped with compute; returns host float64 scores.
-        The results are views of this detector's pinned buffers, valid after the current
-        stream is synchronised and until the next call (copy them to keep them)."""
+        Back-to-back calls pipeline (the next call's copies overlap this call's last
+        chunks).  The results are views of this detector's pinned buffers, valid after the
+        current stream is synchronised and until the next call (copy them to keep them),
+        or the caller's pinned (scores float64, counts int32) tensors given as ``out``."""
         if host_images.dim() == 2:
             host_images = host_images.unsqueeze(0)
         if host_images.device.type != "cpu":
@@ -185,18 +187,25 @@ class Detector:
             raise ValueError("host images must be contiguous (B, H, W) with W*bytes % 16 == 0")
         pitch = W * bpp
         chunk = max(1, min(int(chunk), B))
-        need_stage = 2 * chunk * H * pitch
+        need_stage = 3 * chunk * H * pitch   # three staging slots (kStageSlots)
         if getattr(self, "_stage", None) is None or self._stage.numel() < need_stage + 256:
             self._stage = torch.empty(need_stage + 256, dtype=torch.uint8, device=self.device)
         ws = self._workspace(chunk)
-        if getattr(self, "_hs", None) is None or self._hs.numel() < B:
-            self._hs = torch.empty(B, dtype=torch.float64).pin_memory()
-            self._hc = torch.empty(B, dtype=torch.int32).pin_memory()
+        if out is not None:
+            hs, hc = out
+            if (hs.dtype != torch.float64 or hc.dtype != torch.int32 or hs.numel() < B or hc.numel() < B
+                    or hs.device.type != "cpu" or hc.device.type != "cpu"):
+                raise ValueError("out must be host (float64, int32) tensors of >= batch elements")
+        else:
+            if getattr(self, "_hs", None) is None or self._hs.numel() < B:
+                self._hs = torch.empty(B, dtype=torch.float64).pin_memory()
+                self._hc = torch.empty(B, dtype=torch.int32).pin_memory()
+            hs, hc = self._hs, self._hc
         _abi.check(self._lib.mhfd_focus_score_host(self._h, host_images.data_ptr(), dt, B, pitch,
                                                    self._ws_ptr(self._stage), need_stage, self._ws_ptr(ws),
-                                                   ws.numel() - 256, self._hs.data_ptr(), self._hc.data_ptr(),
+                                                   ws.numel() - 256, hs.data_ptr(), hc.data_ptr(),
                                                    self._stream()))
-        return (self._hs[:B], self._hc[:B]) if counts else self._hs[:B]
+        return (hs[:B], hc[:B]) if counts else hs[:B]
 
     # -------------------------------------------------- single-image sharding (f2)
     def detect_band(self, image: torch.Tensor, y0: int, y1: int, capacity: int | None = None):

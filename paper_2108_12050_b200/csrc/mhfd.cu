@@ -35,6 +35,8 @@
 
 using namespace mhfd;
 
+constexpr int kStageSlots = 3;   // host path: staging slots of `chunk` images each
+
 struct mhfd_ctx {
   mhfd_params p;
   LevelTable* tab;   // host copy, passed by value to k_scale_space
@@ -62,7 +64,10 @@ struct mhfd_ctx {
   int tmax, tcount;
   // e2e host path (mhfd_focus_score_host): copy stream + double-buffer events
   cudaStream_t copy_stream;
-  cudaEvent_t ev_ready[2], ev_free[2];
+  cudaEvent_t ev_ready[kStageSlots], ev_free[kStageSlots], ev_done;   // host path (e2e)
+  uint32_t stage_next;         // next staging slot (continues across calls)
+  const void* stage_ptr;       // staging buffer / chunk of the previous host-path call
+  int stage_chunk;
 };
 
 namespace {
@@ -801,9 +806,9 @@ __global__ void k_copy_lohi(const ImgPar* par, int32_t* lohi, int B) {
 // (1, 2, ..., chunk, chunk, ...): only the first image's copy is exposed, and the chunk
 // count (each costing its ~0.24 ms) stays small.  64 x 4096^2 u8: 24.9 ms (geometric, 16)
 // -> 23.7 (uniform 8) -> see DESIGN.md §8 for this ramp.
-std::vector<int> e2e_chunks(int batch, int chunk) {
+std::vector<int> e2e_chunks(int batch, int chunk, bool ramp) {
   std::vector<int> out;
-  for (int left = batch, n = 1; left > 0; n = std::min(chunk, n + 1)) {
+  for (int left = batch, n = ramp ? 1 : chunk; left > 0; n = std::min(chunk, n + 1)) {
     out.push_back(std::min(n, left));
     left -= out.back();
   }
@@ -1229,7 +1234,8 @@ void mhfd_destroy(mhfd_ctx* c) {
   }
   if (c->copy_stream) {
     cudaStreamDestroy(c->copy_stream);
-    for (int i = 0; i < 2; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
+    for (int i = 0; i < kStageSlots; ++i) { cudaEventDestroy(c->ev_ready[i]); cudaEventDestroy(c->ev_free[i]); }
+    cudaEventDestroy(c->ev_done);
   }
   if (c->d_tctab) cudaFree(c->d_tctab);
   if (c->d_tc2tab) cudaFree(c->d_tc2tab);
@@ -1249,34 +1255,49 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
   if (!h_images || !h_scores || !d_staging) return fail(MHFD_ERR_INVALID_ARGUMENT, "NULL argument");
   if (batch < 1) return fail(MHFD_ERR_SHAPE, "batch %d < 1", batch);
   const size_t img_bytes = (size_t)c->p.height * (size_t)pitch_bytes;
-  const int chunk = (int)std::min<size_t>(staging_bytes / (2 * img_bytes), (size_t)batch);
-  if (chunk < 1) return fail(MHFD_ERR_WORKSPACE, "staging holds < 1 image per half");
+  const int chunk = (int)std::min<size_t>(staging_bytes / (kStageSlots * img_bytes), (size_t)batch);
+  if (chunk < 1) return fail(MHFD_ERR_WORKSPACE, "staging holds < 1 image per slot (%d slots)", kStageSlots);
   if (((uintptr_t)d_staging) % 256 != 0) return fail(MHFD_ERR_WORKSPACE, "staging not 256-byte aligned");
   mhfd_status s = check_call(c, d_staging, dtype, chunk, pitch_bytes, d_workspace, workspace_bytes);
   if (s != MHFD_OK) return s;
   cudaError_t e = cudaSuccess;
+  bool fresh = false;
   if (!c->copy_stream) {
     e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (int i = 0; i < kStageSlots && e == cudaSuccess; ++i) {
       e = cudaEventCreateWithFlags(&c->ev_ready[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
     }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "host-path stream/events");
+    fresh = true;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(d_workspace);
   const Layout L = layout(c, chunk);
   double* d_sc = reinterpret_cast<double*>(ws + L.scores);
   int32_t* d_ct = reinterpret_cast<int32_t*>(ws + L.counts);
-  // the copy stream must not overwrite staging the caller's stream may still read
-  e = cudaEventRecord(c->ev_free[0], st);
-  if (e == cudaSuccess) e = cudaEventRecord(c->ev_free[1], st);
-  if (e != cudaSuccess) return cuda_fail(e, "event record");
+  // Consecutive calls pipeline: chunk k's copy waits only for the compute that last used
+  // its staging slot (ev_free), so the next call's first copies overlap this call's last
+  // chunks.  A first call, or a different staging buffer / slot size, instead orders the
+  // copies after everything already on the caller's stream (which may still read staging).
+  if (fresh || c->stage_ptr != d_staging || c->stage_chunk != chunk) {
+    for (int i = 0; i < kStageSlots && e == cudaSuccess; ++i) e = cudaEventRecord(c->ev_free[i], st);
+    if (e != cudaSuccess) return cuda_fail(e, "event record");
+    c->stage_ptr = d_staging;
+    c->stage_chunk = chunk;
+    c->stage_next = 0;
+  }
+  // Chunk plan: with the previous call still in flight its tail hides this call's first
+  // copy, so every chunk is `chunk` images (fewest per-call overheads); on an idle device
+  // the chunks ramp up 1, 2, 3, ... so that compute starts after one image's copy
+  const bool in_flight = !fresh && cudaEventQuery(c->ev_done) == cudaErrorNotReady;
+  cudaGetLastError();   // (cudaEventQuery's not-ready status is not an error)
   int launches = 0;
-  const std::vector<int> sizes = e2e_chunks(batch, chunk);
+  const std::vector<int> sizes = e2e_chunks(batch, chunk, !in_flight);
   for (int b0 = 0, k = 0, nb = 0; k < (int)sizes.size(); b0 += nb, ++k) {
     nb = sizes[k];
-    const int h = k & 1;
+    const int h = (int)(c->stage_next++ % kStageSlots);
     char* dst = static_cast<char*>(d_staging) + (size_t)h * chunk * img_bytes;
     e = cudaStreamWaitEvent(c->copy_stream, c->ev_free[h], 0);
     if (e == cudaSuccess)
@@ -1297,6 +1318,8 @@ mhfd_status mhfd_focus_score_host(mhfd_ctx* c, const void* h_images, int32_t dty
       e = cudaMemcpyAsync(h_counts + b0, d_ct, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "host-path readback");
   }
+  e = cudaEventRecord(c->ev_done, st);
+  if (e != cudaSuccess) return cuda_fail(e, "event record");
   g_launches = launches;
   return MHFD_OK;
 }

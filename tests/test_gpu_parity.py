@@ -720,6 +720,29 @@ def test_focus_score_host_equals_device(kind):
     assert float(hs.min()) > 0
 
 
+def test_focus_score_host_pipelined_calls():
+    """Back-to-back mhfd_focus_score_host calls without a synchronisation in between (the
+    second call's copies overlap the first call's last chunks through the three staging
+    slots, and it uses whole chunks): every call's scores equal the device path's, for
+    two different batches and a ragged batch size."""
+    n = 512
+    mk = lambda seed, B: np.stack([synth.em_tile_np(n, n, seed + k, defocus=0.4 * (k % 5), dose=300.0, bits=8)
+                                   for k in range(B)])
+    batches = [torch.from_numpy(mk(1600, 13)).pin_memory(), torch.from_numpy(mk(1700, 9)).pin_memory()]
+    det = mhfd.Detector(n, n, threshold=_tau(C3), **C3)
+    ref = [det.focus_score(b.cuda()).cpu() for b in batches]
+    torch.cuda.synchronize()
+    order = [0, 1, 0, 1, 1, 0]
+    outs = [(torch.empty(13, dtype=torch.float64).pin_memory(), torch.empty(13, dtype=torch.int32).pin_memory())
+            for _ in order]
+    for i, o in zip(order, outs):   # no synchronisation between the calls
+        det.focus_score_host(batches[i], chunk=3, out=o)
+    torch.cuda.synchronize()
+    for i, (hs, hc) in zip(order, outs):
+        B = batches[i].shape[0]
+        assert torch.equal(hs[:B], ref[i]) and torch.equal(hc[:B].to(torch.float64), ref[i])
+
+
 def test_downsample_pitched_buffers():
     """mhfd_downsample through the C ABI with row pitches wider than the rows (input and
     output), u8 factor 2 (vector path off: odd width) and u16 factor 3: bit-exact, and the

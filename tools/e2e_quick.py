@@ -35,6 +35,15 @@ def t(fn, n=5):
 ch = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 dev = t(lambda: det.focus_score(imgs))
 e2e = t(lambda: det.focus_score_host(host, chunk=ch))
+
+
+def five():   # five back-to-back calls, no synchronisation between them (bench.py's e2e loop)
+    for _ in range(5):
+        det.focus_score_host(host, chunk=ch)
+
+
+e2e5 = t(five, 3) / 5
 cp = t(lambda: imgs.copy_(host, non_blocking=True))
-print(f"device {dev:.2f} ms ({B * 16.777216 / dev:.0f} GPix/s... MPix/ms), e2e chunk {ch}: {e2e:.2f} ms "
-      f"({B * 16.777216 / e2e * 1e3:.0f} MPix/s), plain H2D copy {cp:.2f} ms ({B * 16.777216 / cp:.1f} GB/s)")
+print(f"device {dev:.2f} ms, e2e chunk {ch}: one call {e2e:.2f} ms ({B * 16.777216 / e2e * 1e3:.0f} MPix/s), "
+      f"5 back-to-back calls {e2e5:.2f} ms per call ({B * 16.777216 / e2e5 * 1e3:.0f} MPix/s), "
+      f"plain H2D copy {cp:.2f} ms ({B * 16.777216 / cp:.1f} GB/s)")
