@@ -72,7 +72,8 @@ __device__ __forceinline__ bool cand26(const float* __restrict__ dog, int W, int
         if (di == 0 && dy == 0 && dx == 0) continue;
         const int xx = x + dx;
         if (xx < 0 || xx >= W) continue;
-        if (!dominates(c, __ldg(P + (int64_t)yy * W + xx), strict)) return false;
+        const float q = __ldg(P + (int64_t)yy * W + xx);   // NaN skipped, as in paper_cand
+        if (q == q && !dominates(c, q, strict)) return false;
       }
     }
   }
@@ -592,6 +593,129 @@ __global__ void __launch_bounds__(256, 3) k_nms_roll(NmsArgs a, int nseg, int32_
   if (lane < nrow) segcnt[(int64_t)b * nseg + seg0 + lane * spr] = parked;
 }
 
+// 26-neighbour mode (readings R8, R16), count + park pass for widths that
+// are whole 1024-pixel segments: one warp per (row y, segment), 8 pixels per lane per
+// 256-pixel step.  The scale loop keeps, per pixel, D_i, the max of its 8 spatial
+// neighbours in plane i (M8_i) and the 3 x 3 max of plane i-1 (M9_{i-1}); plane i+1's
+// three rows are loaded while plane i is decided: (p, i) is a candidate iff D_i > tau and
+// D_i >= max(M8_i, M9_{i-1}, M9_{i+1}) (> when strict), with -inf outside the image and
+// no plane beyond the first / last — cand26's rule (the maxima skip NaN, as cand26 does).
+// Each plane's rows are read once per output row (3 row loads per plane, the neighbouring
+// rows from L1/L2) instead of 27 scattered loads per (pixel, plane) in both passes of the
+// generic kernels.  Records go to the segment's slab in (x, scale) order; k_seg_scan and
+// k_nms_gather4<MHFD_NMS_26> (overflowing segments re-evaluated with cand26) follow.
+__global__ void __launch_bounds__(256) k_nms26_roll(NmsArgs a, int nseg, int32_t* __restrict__ segcnt, int row0,
+                                                    int row1, mhfd_blob* __restrict__ slab) {
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int W = a.W, H = a.H, n = a.n;
+  const int spr = W / kSeg;
+  const int grp = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (grp >= (row1 - row0) * spr) return;
+  const int y = row0 + grp / spr;
+  const int xseg = (grp % spr) * kSeg;
+  const int seg = ((y - row0) * W + xseg) / kSeg;
+  const int64_t plane = (int64_t)H * W;
+  const float* dog = a.dog + (int64_t)b * n * plane;
+  const float tau = a.tau;
+  const bool strict = a.strict != 0;
+  const bool up = y >= 1, dn = y + 1 < H;
+  mhfd_blob* sl = slab + ((int64_t)b * nseg + seg) * kSlab;
+  int parked = 0;
+  for (int step = 0; step < kSeg / 256; ++step) {
+    const int x = xseg + step * 256 + 8 * lane;
+    const bool lft = lane == 0 && x > 0, rgt = lane == 31 && x + 8 < W;
+    // plane j's centre row (8 values) and the max of its 8 spatial neighbours (M8)
+    auto load_plane = [&](int j, float (&c)[8], float (&m8)[8]) {
+      const float* q = dog + (int64_t)j * plane + (int64_t)y * W + x;
+      float u[10], cc[10], d[10];
+      auto ld = [&](const float* r, bool ok, float (&o)[10]) {
+        if (ok) {
+          const float4 p0 = __ldg(reinterpret_cast<const float4*>(r));
+          const float4 p1 = __ldg(reinterpret_cast<const float4*>(r + 4));
+          o[1] = p0.x; o[2] = p0.y; o[3] = p0.z; o[4] = p0.w;
+          o[5] = p1.x; o[6] = p1.y; o[7] = p1.z; o[8] = p1.w;
+          o[0] = lft ? __ldg(r - 1) : -INFINITY;
+          o[9] = rgt ? __ldg(r + 8) : -INFINITY;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 10; ++k) o[k] = -INFINITY;
+        }
+        const float hu = __shfl_up_sync(0xffffffffu, o[8], 1);
+        const float hd = __shfl_down_sync(0xffffffffu, o[1], 1);
+        if (lane != 0) o[0] = hu;
+        if (lane != 31) o[9] = hd;
+      };
+      ld(q - W, up, u);
+      ld(q, true, cc);
+      ld(q + W, dn, d);
+      float V[10];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) V[k] = fmaxf(u[k], d[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = cc[k + 1];
+        m8[k] = fmaxf(fmaxf(V[k], V[k + 1]), fmaxf(V[k + 2], fmaxf(cc[k], cc[k + 2])));
+      }
+    };
+    float c0[8], m80[8], m9p[8];
+    uint32_t bits[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m9p[k] = -INFINITY;
+      bits[k] = 0u;
+    }
+    load_plane(0, c0, m80);
+    for (int i = 0; i < n; ++i) {
+      float c1[8], m81[8];
+      if (i + 1 < n) {
+        load_plane(i + 1, c1, m81);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c1[k] = m81[k] = -INFINITY;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float m = fmaxf(m80[k], fmaxf(m9p[k], fmaxf(m81[k], c1[k])));   // 26 neighbours
+        const bool ok = (c0[k] > tau) && (strict ? (c0[k] > m) : (c0[k] >= m));
+        bits[k] |= (uint32_t)ok << i;
+        m9p[k] = fmaxf(m80[k], c0[k]);
+        c0[k] = c1[k];
+        m80[k] = m81[k];
+      }
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cnt += __popc(bits[k]);
+    int incl = cnt;
+#pragma unroll
+    for (int sh = 1; sh < 32; sh <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, sh);
+      if (lane >= sh) incl += t;
+    }
+    int pos = parked + incl - cnt;
+    parked += __shfl_sync(0xffffffffu, incl, 31);
+    if (cnt) {
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        uint32_t m = bits[k];
+        while (m) {
+          const int i = __ffs(m) - 1;
+          m &= m - 1;
+          if (pos < kSlab) {
+            mhfd_blob r;
+            r.x = x + k; r.y = y; r.scale = i;
+            r.response = __ldg(dog + (int64_t)i * plane + (int64_t)y * W + x + k);
+            sl[pos] = r;
+          }
+          ++pos;
+        }
+      }
+    }
+  }
+  if (lane == 0) segcnt[(int64_t)b * nseg + seg] = parked;
+}
+
 // Gather after the scan: one warp per segment copies its parked records to its final
 // offset; a segment with more than kSlab candidates (its slab overflowed) re-evaluates
 // its 1024 pixels with the full predicate instead (same records, same order).
@@ -635,6 +759,7 @@ __global__ void __launch_bounds__(256) k_nms_gather(NmsArgs a, int nseg, const i
 // ~5 records on the C4 tiles, so a warp per segment left most lanes idle): parked
 // records are copied by the segment's eight lanes; each overflowing segment is then
 // re-evaluated by the whole warp as in k_nms_gather.
+template <int MODE = MHFD_NMS_PAPER>
 __global__ void __launch_bounds__(256) k_nms_gather4(NmsArgs a, int nseg, const int32_t* __restrict__ segcnt,
                                                      const int32_t* __restrict__ segoff,
                                                      const mhfd_blob* __restrict__ slab, mhfd_blob* __restrict__ cand,
@@ -661,6 +786,21 @@ __global__ void __launch_bounds__(256) k_nms_gather4(NmsArgs a, int nseg, const 
     const int s2 = seg_base + (src >> 3);
     int64_t off = __shfl_sync(0xffffffffu, off0, src);
     const int64_t p0 = (int64_t)row0 * a.W + (int64_t)s2 * kSeg;
+    if (MODE == MHFD_NMS_26) {   // 0..n candidates per pixel, written in (x, scale) order
+      for (int k = 0; k < kSeg; k += 32) {
+        const int64_t p = p0 + k + lane;
+        const int cnt = pixel_cands<MHFD_NMS_26>(a, b, p, nullptr, 0, 0);
+        int incl = cnt;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, sh);
+          if (lane >= sh) incl += t;
+        }
+        if (cnt) pixel_cands<MHFD_NMS_26>(a, b, p, out, off + incl - cnt, cap);
+        off += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      continue;
+    }
     for (int k = 0; k < kSeg; k += 32) {
       const int64_t p = p0 + k + lane;
       const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);

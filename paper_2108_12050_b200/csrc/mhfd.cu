@@ -198,7 +198,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   // k_tc2: the stretched image as tiled fp16 hi/lo planes (rows padded to whole NR tiles)
   L.xtc = take(tc2_fit(c) ? 2 * t2_x_plane_bytes(c->p.width, tc2_nrt(c), c->tc2->NR) * rxb : 0);
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
-  L.slab = take(paper && c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);
+  L.slab = take(c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);   // both NMS modes
   L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
   L.total = o;
   return L;
@@ -282,6 +282,8 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
   mhfd_blob* slab = reinterpret_cast<mhfd_blob*>(ws + L.slab);
   dim3 gn((nseg + 7) / 8, B);
   const bool rows_fast = paper && (W % kSeg) == 0;   // segments are whole-row pieces
+  static const bool nms26_generic = getenv("MHFD_NMS26_GENERIC") != nullptr;   // A/B knob
+  const bool rows26 = !paper && (W % kSeg) == 0 && !nms26_generic;
   const dim3 gr((((row1 - row0 + kNmsRows - 1) / kNmsRows) * (W / kSeg) + 7) / 8, B);   // kNmsRows segments per warp
   // k_nms_roll<8> is the default count pass (NMS stage 1.695 -> 1.551 ms per 64 tiles
   // against k_nms_rows; <4> 1.603); MHFD_NMS_ROLL=0/4/8 selects for A/B runs
@@ -299,6 +301,9 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
     else k_nms_roll<1><<<g8, 256, 0, st>>>(na, nseg, segcnt, row0, row1, slab);
   } else if (rows_fast) {
     k_nms_rows<false><<<gr, 256, 0, st>>>(na, nseg, segcnt, nullptr, nullptr, 0, row0, row1, slab);
+  } else if (rows26) {
+    k_nms26_roll<<<dim3((unsigned)(((int64_t)(row1 - row0) * (W / kSeg) + 7) / 8), B), 256, 0, st>>>(
+        na, nseg, segcnt, row0, row1, slab);
   } else if (paper) {
     k_nms_count<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segcnt);
   } else {
@@ -311,6 +316,9 @@ mhfd_status run_nms(mhfd_ctx* c, int W, int H, int B, char* ws, const Layout& L,
     static const bool g1 = getenv("MHFD_NMS_GATHER1") != nullptr;   // A/B knob: one warp per segment
     if (g1) k_nms_gather<<<gn, 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
     else k_nms_gather4<<<dim3((nseg + 31) / 32, B), 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand, c->cap, row0);
+  } else if (rows26) {
+    k_nms_gather4<MHFD_NMS_26><<<dim3((nseg + 31) / 32, B), 256, 0, st>>>(na, nseg, segcnt, segoff, slab, cand,
+                                                                          c->cap, row0);
   } else if (paper) {
     k_nms_write<MHFD_NMS_PAPER><<<gn, 256, 0, st>>>(na, nseg, segoff, cand, c->cap);
   } else {

@@ -344,6 +344,39 @@ def test_c2_26_mode_parity():
     _full_parity(img, C3, nms="26")
 
 
+@pytest.mark.parametrize("strict,polarity,tau", [(False, "dark", 1e-6), (True, "bright", None)])
+def test_26_mode_row_kernel_parity(strict, polarity, tau):
+    """k_nms26_roll (26-neighbour count + park over whole 1024-pixel row segments) and
+    k_nms_gather4<26>: full parity at 1024^2 with a threshold low enough that many
+    segments overflow their 64-record slabs (re-evaluated in (x, scale) order), and with
+    the strict rule and bright polarity."""
+    img = synth.em_tile_np(1024, 1024, 1010, defocus=0.5, dose=300.0, bits=8)
+    s = _full_parity(img, C3, nms="26", strict=strict, polarity=polarity, tau=tau)
+    assert s["n_oracle"] > 1000
+    if tau is not None:   # the overflow path was taken: some row segment has > 64 candidates
+        det = mhfd.Detector(1024, 1024, threshold=tau, nms="26", strict=strict, polarity=polarity, **C3)
+        d = det.debug_dump(_to_t(img), dog=False, cands=True)
+        nc = int(d["ncand"][0])
+        c = d["cands"][0][:nc].cpu().numpy()
+        per_seg = np.bincount(c[:, 1].astype(np.int64) * 1 + (c[:, 0].astype(np.int64) // 1024), minlength=1024)
+        assert int(per_seg.max()) > 64, int(per_seg.max())
+
+
+def test_26_mode_batch_matches_single():
+    """26 mode on a batch of two 2048^2 tiles (two segments per row, image index in the
+    slab and offset arrays): the same kept blobs as two single-image calls."""
+    imgs = np.stack([synth.em_tile_np(2048, 2048, 1020 + k, defocus=1.0 * k, dose=300.0, bits=8) for k in range(2)])
+    det = mhfd.Detector(2048, 2048, threshold=_tau(C3), nms="26", **C3)
+    t = torch.from_numpy(imgs).cuda()
+    blobs, cnt, _ = det.detect(t)
+    torch.cuda.synchronize()
+    for k in range(2):
+        b1, c1, _ = det.detect(t[k:k + 1])
+        torch.cuda.synchronize()
+        n = int(c1[0])
+        assert n > 1000 and n == int(cnt[k]) and torch.equal(b1[0, :n], blobs[k, :n])
+
+
 # ------------------------------------------------------------------ f2: single-image bands
 @pytest.mark.parametrize("size,G", [(1024, 1), (1024, 3), (4096, 2), (4096, 8)])
 def test_band_sharding_matches_whole_image(size, G):
