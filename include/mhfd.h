@@ -117,8 +117,8 @@ typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
 /* Image boundary of the blur (ABI 3).  MHFD_BOUNDARY_PERIODIC: what the paper's FFT
  * computes (reading R7; default).  MHFD_BOUNDARY_REFLECT: half-sample
  * symmetric extension (scipy.ndimage 'reflect', reading R25), run on
- * the two-pass CUDA-core schedule: width % 256 == 0 required.  The NMS window keeps its
- * -inf padding either way. */
+ * k_tc for u8 DoG where it fits (mirrored tile windows), else on the two-pass CUDA-core
+ * schedule: width % 256 == 0 required.  The NMS window keeps its -inf padding either way. */
 typedef enum { MHFD_BOUNDARY_PERIODIC = 0, MHFD_BOUNDARY_REFLECT = 1 } mhfd_boundary;
 
 /* Schedule selection (ABI 4): which kernels compute rows a2-a6.  AUTO picks the fastest

@@ -63,10 +63,20 @@ __device__ __forceinline__ TcTile tc_tile(int t, int tx, int ty, int row_lo) {
   return r;
 }
 
+// Blur boundary index (P.reflect): periodic (reading R7) or half-sample symmetric
+// ... c b a | a b c ... (R25; one reflection: R_max < W, H)
+__device__ __forceinline__ int tc_bidx(int a, int m, int reflect) {
+  if (reflect) return a < 0 ? -a - 1 : (a >= m ? 2 * m - 1 - a : a);
+  return wrap_idx(a, m);
+}
+
 // Fetch the raw window of tile tt into `land` (LW x S bytes, row pitch LW): columns
-// x0 - H0 - off .. +LW, rows y0 - H0 .. +S, periodic.  Mode as band_fetch: 2 = TMA box,
-// 1 = bulk copies per row, 0 = plain loads (complete on return).
+// x0 - H0 - off .. +LW, rows y0 - H0 .. +S, periodic or mirrored.  Mode as band_fetch:
+// 2 = TMA box, 1 = bulk copies per row, 0 = plain loads (complete on return), 3 = bulk
+// copies of the in-image columns of mirrored rows (reflect), whose out-of-image columns
+// tc_reflect_cols fills inside `land` once the copies have landed.
 __device__ __forceinline__ void epi_sync();
+template <bool REFLECT>
 __device__ __forceinline__ int tc_fetch_epi(const TcTile& tt, uint8_t* land, uint64_t* bar, const uint8_t* images,
                                         const Shape& s, const CUtensorMap* tmap, int use_tmap, const TcPlan& P) {
   const int LW = tc_lw(P), S = P.S;
@@ -82,6 +92,15 @@ __device__ __forceinline__ int tc_fetch_epi(const TcTile& tt, uint8_t* land, uin
     return 2;
   }
   const uint8_t* img = images + (int64_t)tt.b * s.H * s.pitch;
+  if (REFLECT && bulk) {
+    const int cl = max(xr, 0), ch = min(xr + LW, s.W);
+    if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)(S * (ch - cl)));
+    epi_sync();   // expect_tx registered before any copy completes
+    for (int r = tid; r < S; r += kTcThreads)
+      bulk_g2s(land + (size_t)r * LW + (cl - xr), img + (int64_t)tc_bidx(yr + r, s.H, 1) * s.pitch + cl,
+               (uint32_t)(ch - cl), bar);
+    return 3;
+  }
   if (bulk) {
     if (tid == 0) mbar_arrive_expect_tx(bar, (uint32_t)(S * LW));
     epi_sync();   // expect_tx registered before any copy completes
@@ -100,10 +119,22 @@ __device__ __forceinline__ int tc_fetch_epi(const TcTile& tt, uint8_t* land, uin
   }
   const int warp = tid >> 5, lane = tid & 31;
   for (int r = warp; r < S; r += kTcThreads / 32) {
-    const uint8_t* row = img + (int64_t)wrap_idx(yr + r, s.H) * s.pitch;
-    for (int c = lane; c < LW; c += 32) land[(size_t)r * LW + c] = row[wrap_idx(xr + c, s.W)];
+    const uint8_t* row = img + (int64_t)tc_bidx(yr + r, s.H, REFLECT) * s.pitch;
+    for (int c = lane; c < LW; c += 32) land[(size_t)r * LW + c] = row[tc_bidx(xr + c, s.W, REFLECT)];
   }
   return 0;
+}
+
+// Mode 3 windows: out-of-image columns from their mirror images inside the window
+__device__ __noinline__ void tc_reflect_cols(uint8_t* land, const TcPlan& P, int xr, int W) {
+  const int LW = tc_lw(P), S = P.S;
+  if (xr >= 0 && xr + LW <= W) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < S; r += kTcThreads / 32)
+    for (int c = lane; c < LW; c += 32) {
+      const int x = xr + c;
+      if (x < 0 || x >= W) land[(size_t)r * LW + c] = land[(size_t)r * LW + (tc_bidx(x, W, 1) - xr)];
+    }
 }
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
@@ -207,7 +238,10 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 512;" :::
 // B1 is restaged after rowDone of the tile's last level (waited before its split).
 // DOG: also write every DoG plane to dog_out (26-neighbour NMS, dumps).  NP: level parts
 // per tile (1, or 2 for calls with few tiles; a template so the batch path pays nothing)
-template <bool DOG, int NP = 1>
+// REFLECT (reading R25, P.reflect): mirrored windows at the image edges (mode 3 fetches
+// and tc_reflect_cols); a separate instantiation, so the periodic kernels keep their
+// register allocation
+template <bool DOG, int NP = 1, bool REFLECT = false>
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
 k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par, const __grid_constant__ TcPlan P,
      const uint8_t* __restrict__ tabs, const __grid_constant__ CUtensorMap tmap, int use_tmap,
@@ -333,7 +367,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
     // expanded with tc_tile where needed: three ints instead of three TcTiles of state
     auto tile_of = [&](int u) { return tc_tile(u / nparts, tx, ty, row_lo); };
     int t = t0, ou = t0;
-    int mode = tc_fetch_epi(tile_of(t), land, &bars[0], images, s, &tmap, use_tmap, P);
+    int mode = tc_fetch_epi<REFLECT>(tile_of(t), land, &bars[0], images, s, &tmap, use_tmap, P);
     uint32_t land_phase = 0;
     float oinv = 0.f;
     int odeg = 0;
@@ -425,6 +459,10 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
           mbar_wait(&bars[0], land_phase);
           land_phase ^= 1u;
         }
+        if (REFLECT && mode == 3) {   // mirrored columns (rows were mirrored by the copies)
+          tc_reflect_cols(land, P, tile_of(t).x0 - P.H0 - tc_off(P), s.W);
+          epi_sync();
+        }
         epi_sync();
         ip = par[tile_of(t).b];
         tc_stage_b1(land, B1, S, LW, OFF, ip.lo, ip.hi, ip.lo + (ip.hi - ip.lo + 1) / 2);
@@ -433,7 +471,7 @@ k_tc(const uint8_t* __restrict__ images, Shape s, const ImgPar* __restrict__ par
         if (lane == 0) mbar_arrive1(&bars[7]);
         epi_sync();   // landing zone free
         tn = t + gridDim.x;
-        if (tn < ntiles) mode = tc_fetch_epi(tile_of(tn), land, &bars[0], images, s, &tmap, use_tmap, P);
+        if (tn < ntiles) mode = tc_fetch_epi<REFLECT>(tile_of(tn), land, &bars[0], images, s, &tmap, use_tmap, P);
       }
       // ---- DoG of level g-1.  At level 0 that is the previous tile's last level; it runs
       // before this level's column pass overwrites D2[g & 1] (= its L_{n-1}), and the

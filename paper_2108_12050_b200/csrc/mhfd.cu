@@ -391,14 +391,17 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   // k_tc also writes the DoG planes: for the 26-neighbour NMS and for debug dumps
   float* tc_dog = dog_dump ? dog_dump : (paper ? nullptr : reinterpret_cast<float*>(ws + L.dog));
   const bool dogr = c->p.response == MHFD_RESPONSE_DOG;
-  const int reflect = c->p.boundary == MHFD_BOUNDARY_REFLECT ? 1 : 0;   // reading R25: two-pass only
-  const bool fused_ok = dogr && !reflect;
-  if (fused_ok && bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
+  const int reflect = c->p.boundary == MHFD_BOUNDARY_REFLECT ? 1 : 0;   // reading R25: k_tc (u8) or two-pass
+  const bool fused_ok = dogr && !reflect;   // k_band: periodic only; k_tc mirrors its windows (P.reflect)
+  if (dogr && bpp == 1 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H) &&
       (!band || (paper && dog_dump == nullptr))) {
     const TcPlan& P = *c->tc;
     const size_t smem = tc_smem(P);
     const int nparts = (!band && paper && tc_parts(c, B)) ? 2 : 1;
-    auto kern = tc_dog ? (nparts > 1 ? k_tc<true, 2> : k_tc<true, 1>) : (nparts > 1 ? k_tc<false, 2> : k_tc<false, 1>);
+    auto kern = reflect ? (tc_dog ? (nparts > 1 ? k_tc<true, 2, true> : k_tc<true, 1, true>)
+                                  : (nparts > 1 ? k_tc<false, 2, true> : k_tc<false, 1, true>))
+                        : (tc_dog ? (nparts > 1 ? k_tc<true, 2> : k_tc<true, 1>)
+                                  : (nparts > 1 ? k_tc<false, 2> : k_tc<false, 1>));
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc attribute");
     // band mode: rows [band_lo - 1, band_hi + 1) on the whole image's 128-row tile grid, so
@@ -1031,6 +1034,7 @@ mhfd_status mhfd_create(const mhfd_params* p, mhfd_ctx** out) {
   // tensor-core plan and its Toeplitz tables (device copy owned by the context)
   c->tc = new (std::nothrow) TcPlan;
   if (c->tc && tc_plan_build(*c->tc, n + 1, R, t)) {
+    c->tc->reflect = p->boundary == MHFD_BOUNDARY_REFLECT ? 1 : 0;
     if (p->polarity == MHFD_BRIGHT)
       for (int i = 0; i <= n; ++i) c->tc->lev[i].tdog = -c->tc->lev[i].tdog;
     std::vector<std::vector<double>> wv(n + 1);
@@ -1338,8 +1342,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   if (c->p.response == MHFD_RESPONSE_LOG)
     return c->band_kind == 3 && tc2_fit(c) ? "k_tc2" : "k_rows_pair+k_cols_pair<log>";
-  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
+  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (c->band_kind == 3 && tc2_fit(c)) return "k_tc2";
   if (dtype == MHFD_U8 && paper && c->band_enabled && band_ok(W, H, c->tab->rmax, c->tab->ntaps_total))
     return "k_band";

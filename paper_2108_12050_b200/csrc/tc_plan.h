@@ -40,6 +40,7 @@ struct TcLevel {
 
 struct TcPlan {
   int32_t S, H0, nlev, rmax;
+  int32_t reflect;          // blur boundary: 0 periodic (R7), 1 half-sample symmetric (R25)
   int32_t tab_bytes;        // total bytes of all levels' tables
   int32_t max_level_bytes;  // largest single-level block (smem buffer size)
   TcLevel lev[kTcMaxLev];

@@ -99,6 +99,19 @@ def compare_candidates(gpu, ora, amb_xy: set, tie_xy: set, eps: float, mode: str
     return {"n_gpu": len(g), "n_oracle": len(o), "ambiguous": len(amb_xy), "flips_in_band": flips}
 
 
+def pruning_seeds(amb_xy, tie_xy, gpu_c, ora_c) -> list:
+    """Seeds of A' for the kept-set comparison: the ambiguous candidates (rule 2) plus the
+    candidates whose scale is exempt from comparison (top two scale responses within eps,
+    rule 2's last clause).  Such a candidate's scale, hence its radius sqrt(2) t, may
+    legitimately differ between the two sides, which changes its own kept record and the
+    greedy decisions of the blobs it overlaps exactly as an ambiguous candidate does
+    (reading R26)."""
+    pts = {(int(k[0]), int(k[1])) for k in amb_xy}
+    cand_xy = {(int(r[0]), int(r[1])) for r in list(gpu_c) + list(ora_c)}
+    pts |= {(int(x), int(y)) for (x, y) in tie_xy if (int(x), int(y)) in cand_xy}
+    return sorted(pts)
+
+
 def compare_pruned(gpu, ora, amb_pts, rad_max: float, rad, mode: str):
     """Kept sets equal outside A' = A + {blobs within r_p + r_max of a member of A}
     (SURVEY.md §8(c) parity rule 4: an ambiguous candidate can only change the greedy

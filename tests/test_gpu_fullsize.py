@@ -63,7 +63,7 @@ def _image_parity(img_np, cfg, tau, v_g, idx_g, lohi_g, cands_g, kept_g, count_g
     P.assert_prune_exact(cands_g, kept_g, cfg, OVERLAP)
     ora_k = P.oracle_rows(ref["blobs"])
     rad = P.radii(cfg["min_sigma"], cfg["max_sigma"], n)
-    pr = P.compare_pruned(kept_g, ora_k, sorted(amb_xy), max(rad), rad, "paper")
+    pr = P.compare_pruned(kept_g, ora_k, P.pruning_seeds(amb_xy, tie_xy, cands_g, ora_c), max(rad), rad, "paper")
     assert count_g == len(kept_g) and float(score_g) == float(count_g)
     P.assert_score(count_g, ref["count"])
     summ.update(label=label, v_err_rel=verr / Pk, count_gpu=count_g, count_oracle=ref["count"],

@@ -101,7 +101,8 @@ def _full_parity(img, cfg, nms="paper", overlap=0.5, strict=False, tau=None, sch
     gpu_k = P.gpu_rows(blobs[0], count)
     assert gpu_k == sorted(gpu_k, key=lambda r: (r[1], r[0], r[2]))
     ora_k = P.oracle_rows(ref["blobs"])
-    amb_pts = [(x, y) for (x, y, *_) in ([(k[0], k[1]) for k in amb_xy])]
+    amb_pts = (P.pruning_seeds(amb_xy, tie_xy, gpu_c, ora_c) if nms == "paper"
+               else [(x, y) for (x, y, *_) in ([(k[0], k[1]) for k in amb_xy])])
     rad = P.radii(cfg["min_sigma"], cfg["max_sigma"], n)
     P.compare_pruned(gpu_k, ora_k, amb_pts, max(rad), rad, nms)
     P.assert_score(count, ref["count"])
@@ -698,17 +699,33 @@ def test_f32_integer_valued_equals_u16():
 
 
 # ---------------------------------------------------------------- reflect boundary (f3)
-@pytest.mark.parametrize("nms,response", [("paper", "dog"), ("26", "dog"), ("paper", "log")])
-def test_reflect_boundary_full_parity(c1_img, nms, response):
-    """boundary="reflect" (reading R25) on the two-pass kernels: mirrored windows at all four
-    edges (row staging pixel by pixel at the left/right edges, mirrored rows top/bottom),
-    against the oracle's reflect blur; DoG in both NMS modes (the DoG variant writes its
-    planes for the 26-neighbour NMS) and the LoG response."""
+@pytest.mark.parametrize("nms,response,schedule", [("paper", "dog", None), ("26", "dog", None),
+                                                   ("paper", "dog", "band"), ("26", "dog", "band"),
+                                                   ("paper", "log", None)])
+def test_reflect_boundary_full_parity(c1_img, nms, response, schedule):
+    """boundary="reflect" (reading R25): mirrored windows at all four edges, against the
+    oracle's reflect blur; on k_tc (u8: mirrored rows by the window copies, mirrored
+    columns inside the staged window) and on the two-pass kernels (schedule="band"; row
+    staging pixel by pixel at the left/right edges, mirrored rows top/bottom); DoG in both
+    NMS modes and the LoG response (two-pass)."""
     tau = 0.1 if response == "log" else None
-    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response=response, boundary="reflect")
+    s = _full_parity(c1_img, C1, nms=nms, tau=tau, response=response, boundary="reflect", schedule=schedule)
     assert s["n_oracle"] > 100
-    det = mhfd.Detector(256, 256, threshold=0.08, boundary="reflect", **C1)
-    assert det.schedule("u8") == "k_rows_pair+k_cols_pair"
+    det = mhfd.Detector(256, 256, threshold=0.08, boundary="reflect", response=response, schedule=schedule, **C1)
+    want = "k_tc" if (schedule is None and response == "dog") else (
+        "k_rows_pair+k_cols_pair<log>" if response == "log" else "k_rows_pair+k_cols_pair")
+    assert det.schedule("u8") == want
+
+
+@pytest.mark.parametrize("w,h", [(1024, 1024), (2048, 1024)])
+def test_reflect_k_tc_multi_tile(w, h):
+    """Reflect on k_tc over many tiles: 1024^2 runs the level-split small-call variant
+    (64 tiles, two level parts), 2048 x 1024 the whole-level variant; full parity."""
+    img = synth.em_tile_np(h, w, 1030, defocus=0.5, dose=300.0, bits=8)
+    det = mhfd.Detector(w, h, threshold=_tau(C3), boundary="reflect", **C3)
+    assert det.schedule("u8") == "k_tc"
+    s = _full_parity(img, C3, boundary="reflect")
+    assert s["n_oracle"] > 1000
 
 
 def test_reflect_differs_from_periodic_only_near_edges():
