@@ -376,6 +376,15 @@ def other_configs(dev) -> dict:
                      "tflops_issued": fpp * SIZE * SIZE / (dms * 1e-3) / 1e12,
                      "flop_kind": ("tensor fp16 split products (dense-equivalent band tiles)" if det.schedule("u8") == "k_tc2"
                                    else "fp32 direct convolutions")}
+    # C3 in the 26-neighbour NMS mode (k_tc writes the DoG planes; k_nms26_roll) and with
+    # the reflect boundary (k_tc with mirrored windows)
+    for name, kw in (("C3_nms26", {"nms": "26"}), ("C3_reflect", {"boundary": "reflect"})):
+        det = mhfd.Detector(SIZE, SIZE, SIGMA[0], SIGMA[1], NSCALES, threshold=TAU, overlap=OVERLAP,
+                            device=dev.index, **kw)
+        dms, hms, score = timed(det, img.unsqueeze(0), img.unsqueeze(0).cpu().pin_memory())
+        out[name] = {"size": SIZE, "dtype": "u8", "sigma": list(SIGMA), "scales": NSCALES, **kw,
+                     "schedule": det.schedule("u8"), "device_ms": dms, "host_visible_ms": hms,
+                     "MPix_per_s_device": SIZE * SIZE / dms / 1e3, "score": score}
     return out
 
 
