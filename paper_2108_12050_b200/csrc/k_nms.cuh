@@ -799,23 +799,23 @@ __global__ void __launch_bounds__(256) k_nms_gather4(NmsArgs a, int nseg, const 
         if (cnt) pixel_cands<MHFD_NMS_26>(a, b, p, out, off + incl - cnt, cap);
         off += __shfl_sync(0xffffffffu, incl, 31);
       }
-      continue;
-    }
-    for (int k = 0; k < kSeg; k += 32) {
-      const int64_t p = p0 + k + lane;
-      const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);
-      float val = 0.f;
-      const bool c = paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val);
-      const uint32_t m = __ballot_sync(0xffffffffu, c);
-      if (c) {
-        const int64_t pos = off + __popc(m & ((1u << lane) - 1u));
-        if (pos < cap) {
-          mhfd_blob r;
-          r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
-          out[pos] = r;
+    } else {
+      for (int k = 0; k < kSeg; k += 32) {
+        const int64_t p = p0 + k + lane;
+        const int y = (int)(p / a.W), x = (int)(p - (int64_t)y * a.W);
+        float val = 0.f;
+        const bool c = paper_cand(a.v + (int64_t)b * plane, a.W, a.H, y, x, a.tau, a.strict, &val);
+        const uint32_t m = __ballot_sync(0xffffffffu, c);
+        if (c) {
+          const int64_t pos = off + __popc(m & ((1u << lane) - 1u));
+          if (pos < cap) {
+            mhfd_blob r;
+            r.x = x; r.y = y; r.scale = a.idx[(int64_t)b * plane + p]; r.response = val;
+            out[pos] = r;
+          }
         }
+        off += __popc(m);
       }
-      off += __popc(m);
     }
   }
 }
