@@ -109,16 +109,18 @@ typedef enum { MHFD_DARK = 0, MHFD_BRIGHT = 1 } mhfd_polarity;
  * d_xx by zero-sum sampled second-derivative taps w2(d) = w(d)(d^2 - m2)/t^4,
  * m2 = sum_d w(d) d^2, over the same support ceil(5 t) as the blur; same sign and
  * polarity conventions as Eq. 2, responses on the LoG scale (about 1/dt times Eq. 2's).
- * width % 256 == 0 and 2n <= 62 required.  LOG runs on "k_tc2" where it fits (periodic,
- * height % 16 == 0, width >= its staged window), else on the two-pass CUDA-core
+ * width % 256 == 0 and 2n <= 62 required.  LOG runs on "k_tc2" where it fits (height %
+ * 16 == 0, width >= its staged window; either boundary), else on the two-pass CUDA-core
  * schedule "k_rows_pair+k_cols_pair<log>". */
 typedef enum { MHFD_RESPONSE_DOG = 0, MHFD_RESPONSE_LOG = 1 } mhfd_response;
 
 /* Image boundary of the blur (ABI 3).  MHFD_BOUNDARY_PERIODIC: what the paper's FFT
  * computes (reading R7; default).  MHFD_BOUNDARY_REFLECT: half-sample
  * symmetric extension (scipy.ndimage 'reflect', reading R25), run on
- * k_tc for u8 DoG where it fits (mirrored tile windows), else on the two-pass CUDA-core
- * schedule: width % 256 == 0 required.  The NMS window keeps its -inf padding either way. */
+ * k_tc for u8 DoG where it fits (mirrored tile windows), on k_tc2 for u16 / f32 / LoG
+ * where it fits (the stretched image staged with mirrored margins), else on the two-pass
+ * CUDA-core schedule: width % 256 == 0 required.  The NMS window keeps its -inf padding
+ * either way. */
 typedef enum { MHFD_BOUNDARY_PERIODIC = 0, MHFD_BOUNDARY_REFLECT = 1 } mhfd_boundary;
 
 /* Schedule selection (ABI 4): which kernels compute rows a2-a6.  AUTO picks the fastest

@@ -63,30 +63,52 @@ __host__ __device__ inline size_t t2_rx_plane_bytes(int W, int H) { return (size
 // ---------------------------------------------------------------------------------
 // k_tc2_prep: one thread per (image, row, 8-column group); consecutive threads take
 // consecutive rows of one column group, so the 16-byte output pieces are contiguous.
+// Reflect (pg, pr > 0): the staged image has pg mirrored column groups of 8 on either
+// side and pr mirrored rows above and below (staged row r = image row r - pr, half-sample
+// symmetric, reading R25); periodic: pg = pr = 0.
 template <int BPP>
 __global__ void __launch_bounds__(256) k_tc2_prep(const uint8_t* __restrict__ images, Shape s,
                                                   const ImgPar* __restrict__ par, uint8_t* __restrict__ xt, int NR,
-                                                  int nrt, int batch) {
-  const int G = s.W / 8;
+                                                  int nrt, int batch, int pg = 0, int pr = 0) {
+  const int G = s.W / 8 + 2 * pg;
+  const int hx = s.H + 2 * pr;
   const int64_t rows_pad = (int64_t)nrt * NR;
   const int64_t per_img = rows_pad * G;
   const int64_t total = per_img * batch;
-  const size_t pb = t2_x_plane_bytes(s.W, nrt, NR);
+  const size_t pb = t2_x_plane_bytes(8 * G, nrt, NR);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / per_img);
     const int64_t r = i - (int64_t)b * per_img;
     const int rt = (int)(r / ((int64_t)NR * G));
     const int64_t r2 = r - (int64_t)rt * NR * G;
     const int cg = (int)(r2 / NR), n = (int)(r2 - (int64_t)cg * NR);
-    const int y = rt * NR + n;
+    const int ye = rt * NR + n;
     float f[8];
-    if (y < s.H) {
+    const int xe = 8 * (cg - pg);   // first image column of this group (reflect: may be outside)
+    if (ye < hx && pr + pg > 0 && (xe < 0 || xe + 8 > s.W || ye < pr || ye >= s.H + pr)) {
+      // mirrored margins, pixel by pixel (the same stretch as below)
+      const ImgPar ip = par[b];
+      const int y = ye - pr < 0 ? pr - ye - 1 : (ye - pr >= s.H ? 2 * s.H - 1 - (ye - pr) : ye - pr);
+      const uint8_t* row = images + ((int64_t)b * s.H + y) * s.pitch;
+      const float lo = BPP == 4 ? __int_as_float(ip.lo) : (float)ip.lo, inv = ip.inv;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int x0 = xe + k, x = x0 < 0 ? -x0 - 1 : (x0 >= s.W ? 2 * s.W - 1 - x0 : x0);
+        float q;
+        if (BPP == 4) q = __ldg(reinterpret_cast<const float*>(row) + x);
+        else if (BPP == 2) q = (float)__ldg(reinterpret_cast<const uint16_t*>(row) + x);
+        else q = (float)__ldg(row + x);
+        f[k] = kT2XScale * (fminf(fmaxf((q - lo) * inv, 0.f), 1.f) - 0.5f);
+      }
+    } else if (ye < hx) {
+      const int y = ye - pr;
       const ImgPar ip = par[b];
       const uint8_t* row = images + ((int64_t)b * s.H + y) * s.pitch;
+      const int cgi = cg - pg;   // the group's index in the image row
       if (BPP == 4) {
         const float lo = __int_as_float(ip.lo), inv = ip.inv;
-        const float4 a = __ldg(reinterpret_cast<const float4*>(row) + 2 * cg);
-        const float4 c = __ldg(reinterpret_cast<const float4*>(row) + 2 * cg + 1);
+        const float4 a = __ldg(reinterpret_cast<const float4*>(row) + 2 * cgi);
+        const float4 c = __ldg(reinterpret_cast<const float4*>(row) + 2 * cgi + 1);
         const float q[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
 #pragma unroll
         for (int k = 0; k < 8; ++k) f[k] = kT2XScale * (fminf(fmaxf((q[k] - lo) * inv, 0.f), 1.f) - 0.5f);
@@ -94,12 +116,12 @@ __global__ void __launch_bounds__(256) k_tc2_prep(const uint8_t* __restrict__ im
         const float lo = (float)ip.lo, inv = ip.inv;
         uint32_t p[8];
         if (BPP == 2) {
-          const uint4 q = __ldg(reinterpret_cast<const uint4*>(row) + cg);
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(row) + cgi);
           const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
           for (int k = 0; k < 8; ++k) p[k] = (w4[k >> 1] >> (16 * (k & 1))) & 0xffffu;
         } else {
-          const uint2 q = __ldg(reinterpret_cast<const uint2*>(row) + cg);
+          const uint2 q = __ldg(reinterpret_cast<const uint2*>(row) + cgi);
           const uint32_t w2[2] = {q.x, q.y};
 #pragma unroll
           for (int k = 0; k < 8; ++k) p[k] = (w2[k >> 2] >> (8 * (k & 3))) & 0xffu;
@@ -126,7 +148,9 @@ __global__ void __launch_bounds__(256) k_tc2_prep(const uint8_t* __restrict__ im
 // (tx), 6/7 table free (commit), 8 X full (tx), 9 X free (commit).
 __global__ void __launch_bounds__(kT2Threads, 1)
 k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, const uint8_t* __restrict__ tabs,
-           uint8_t* __restrict__ rx, int W, int H, int batch, int nrt, int rt_first, int rt_count) {
+           uint8_t* __restrict__ rx, int W, int H, int batch, int nrt, int rt_first, int rt_count, int pg = 0) {
+  // H: rows of Rx (reflect: the image's plus the mirrored margins); pg: the staged X's
+  // mirrored margin groups on either side (reflect), so windows never wrap
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int NR = P.NR, S = P.S, nlev = P.nlev;
   const size_t xplane = (size_t)(S / 8) * NR * 16;
@@ -206,10 +230,10 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
           tile_of(g / nlev, b, x0, rt);
           if (g > 0) mbar_wait(&bars[9], (uint32_t)(((g / nlev) - 1) & 1));
           mbar_arrive_expect_tx(&bars[8], (uint32_t)(2 * xplane));
-          const int Gc = W / 8, SG = S / 8;
-          int g0 = (x0 - P.H0) / 8;
+          const int Gc = W / 8 + 2 * pg, SG = S / 8;
+          int g0 = (x0 - P.H0) / 8 + pg;
           if (g0 < 0) g0 += Gc;
-          const size_t pb = t2_x_plane_bytes(W, nrt, NR);
+          const size_t pb = t2_x_plane_bytes(8 * Gc, nrt, NR);
           for (int p = 0; p < 2; ++p) {
             const uint8_t* src = xt + ((size_t)b * 2 + p) * pb + (size_t)rt * Gc * NR * 16;
             uint8_t* dst = xs + (size_t)p * xplane;
@@ -273,11 +297,15 @@ k_tc2_rows(const uint8_t* __restrict__ xt, const __grid_constant__ Tc2Plan P, co
 // sub-levels' column products: both accumulate into one TMEM accumulator (j), and the
 // epilogue takes the response from it directly (scaled and signed by lev[2j].tdog).
 // The row pass and the slab / table producer are the DoG ones, level for sub-level.
-template <bool DOG, bool LOG = false>
+template <bool DOG, bool LOG = false, bool REFL = false>
 __global__ void __launch_bounds__(kT2Threads, 1)
 k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const __grid_constant__ Tc2Plan P,
            const uint8_t* __restrict__ tabs, float* __restrict__ v_out, uint8_t* __restrict__ idx_out,
-           float* __restrict__ dog_out, int W, int H, int batch, int yt_first, int yt_count) {
+           float* __restrict__ dog_out, int W, int H, int batch, int yt_first, int yt_count, int hx, int pr) {
+  // REFL (reflect, reading R25): Rx has hx rows, image row 0 at Rx row pr (mirrored
+  // margins), and windows never wrap; periodic instantiations ignore hx / pr (a separate
+  // instantiation keeps their code as it was)
+  if (!REFL) hx = H, pr = 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nlev = P.nlev;
   uint8_t* ring = smem_raw;                                        // kT2Stages x (hi 4 KB | lo 4 KB)
@@ -291,7 +319,7 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
   if (t0 >= ntiles) return;
   const int my_tiles = (ntiles - 1 - t0) / gridDim.x + 1;
   const int G = my_tiles * nlev;
-  const size_t rxp = t2_rx_plane_bytes(W, H);
+  const size_t rxp = t2_rx_plane_bytes(W, hx);
 
   if (tid == kT2Epi) {
     for (int k = 0; k < 8 + 2 * kT2Stages; ++k) mbar_init(&bars[k], (k == 2 || k == 3) ? 16 : 1);
@@ -359,14 +387,15 @@ k_tc2_cols(const uint8_t* __restrict__ rx, const ImgPar* __restrict__ par, const
         bulk_g2s(tbuf + (size_t)(g & 1) * P.max_lev_bytes2, tabs + L.tab_off2, tb, &bars[4 + (g & 1)]);
         int b, x0, y0;
         tile_of(g / nlev, b, x0, y0);
-        const uint8_t* src = rx + ((size_t)b * nlev + lev) * 2 * rxp + (size_t)(x0 / kT2Cols) * (H / 16) * kT2SlabBytes;
-        int ws = y0 - L.R - L.s2;   // slab-aligned first window row (periodic)
-        while (ws < 0) ws += H;
+        const uint8_t* src = rx + ((size_t)b * nlev + lev) * 2 * rxp + (size_t)(x0 / kT2Cols) * (hx / 16) * kT2SlabBytes;
+        int ws = y0 - L.R - L.s2 + pr;   // slab-aligned first window row (periodic: wraps)
+        while (ws < 0) ws += hx;
         for (int j = 0; j < L.K2 / 16; ++j, ++cnt) {
           const uint32_t st = cnt % kT2Stages;
           if (cnt >= (uint32_t)kT2Stages) mbar_wait(&bars[8 + kT2Stages + st], ((cnt / kT2Stages) - 1) & 1u);
           int row = ws + 16 * j;
-          while (row >= H) row -= H;
+          if (REFL) row = min(row, hx - 16);   // rows past the margin feed only outputs y >= H
+          while (row >= hx) row -= hx;
           const uint8_t* s0 = src + (size_t)(row / 16) * kT2SlabBytes;
           uint8_t* dst = ring + (size_t)st * 2 * kT2SlabBytes;
           mbar_arrive_expect_tx(&bars[8 + st], 2 * kT2SlabBytes);

@@ -102,12 +102,28 @@ struct Layout {
 // k_tc2 (two-pass tensor-core schedule) applies: Eq. 2 DoG or LoG, periodic, plan built, widths
 // in whole 128-column tiles, heights in whole 16-row slabs, one periodic wrap of the
 // staged row window
-bool tc2_fit(const mhfd_ctx* c) {   // (a LoG context's plan holds its 2n sub-levels)
-  return c->tc2 && c->d_tc2tab && c->band_enabled &&
-         c->p.boundary == MHFD_BOUNDARY_PERIODIC && c->p.width % kT2Cols == 0 && c->p.height % kT2SlabRows == 0 &&
-         c->p.width >= c->tc2->S;
+bool tc2_fit(const mhfd_ctx* c) {   // (a LoG context's plan holds its 2n sub-levels; reflect: tc2_geom)
+  return c->tc2 && c->d_tc2tab && c->band_enabled && c->p.width % kT2Cols == 0 &&
+         c->p.height % kT2SlabRows == 0 && c->p.width >= c->tc2->S;
 }
-int tc2_nrt(const mhfd_ctx* c) { return (c->p.height + c->tc2->NR - 1) / c->tc2->NR; }
+// Reflect (reading R25) on k_tc2: the stretched image is staged with mirrored margins,
+// pg column groups of 8 left and right and pr rows above and below, so neither pass
+// wraps: Rx is computed for hx = H + 2 pr rows (slab row r = image row r - pr) and each
+// window is one contiguous run.  Periodic: pg = pr = 0, hx = H (the passes wrap).
+struct Tc2Geom {
+  int pg, pr, hx, xw;   // margin groups, margin rows, Rx rows, staged X width (pixels)
+};
+Tc2Geom tc2_geom(const mhfd_ctx* c) {
+  Tc2Geom g{0, 0, c->p.height, c->p.width};
+  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) {
+    g.pg = c->tc2->H0 / 8;
+    g.pr = (c->tc2->rmax + 16 + 15) / 16 * 16;
+    g.hx = c->p.height + 2 * g.pr;
+    g.xw = c->p.width + 16 * g.pg;
+  }
+  return g;
+}
+int tc2_nrt(const mhfd_ctx* c) { return (tc2_geom(c).hx + c->tc2->NR - 1) / c->tc2->NR; }
 
 // k_tc splits each tile's levels over two CTAs when the call has at most half as many
 // tiles as SMs (one 1024^2 tile: 64 tiles on 148 SMs), whole images only
@@ -194,9 +210,11 @@ Layout layout(const mhfd_ctx* c, int B) {
   // kRxBatch images (run_front chunks larger batches)
   const int64_t rxb = std::min(B, kRxBatch);
   const bool any2 = c->ltab || c->twopass || pair_fit(c);
-  L.rx = take(any2 || tc2_fit(c) ? sizeof(float) * plane * rxb * (c->ltab ? 2 * c->n : c->n + 1) : 0);
+  const int64_t rx_rows = tc2_fit(c) ? std::max<int64_t>(c->p.height, tc2_geom(c).hx) : c->p.height;
+  L.rx = take(any2 || tc2_fit(c) ? sizeof(float) * (int64_t)c->p.width * rx_rows * rxb * (c->ltab ? 2 * c->n : c->n + 1)
+                                 : 0);
   // k_tc2: the stretched image as tiled fp16 hi/lo planes (rows padded to whole NR tiles)
-  L.xtc = take(tc2_fit(c) ? 2 * t2_x_plane_bytes(c->p.width, tc2_nrt(c), c->tc2->NR) * rxb : 0);
+  L.xtc = take(tc2_fit(c) ? 2 * t2_x_plane_bytes(tc2_geom(c).xw, tc2_nrt(c), c->tc2->NR) * rxb : 0);
   // NMS fast path (W % kSeg == 0): every segment parks up to kSlab records during the count
   L.slab = take(c->p.width % kSeg == 0 ? sizeof(mhfd_blob) * kSlab * (size_t)nseg * B : 0);   // both NMS modes
   L.wl = take(sizeof(int32_t) * 8 * (size_t)wl_cap_of(c, B));   // pruning worklist (k_prune.cuh)
@@ -433,9 +451,10 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     return run_nms(c, W, H, B, ws, L, v, idx, paper ? nullptr : tc_dog, st, launches, ev, band_lo, band_hi);
   }
   // ---- a2-a6 on the two-pass tensor-core schedule (u16 / f32 images, u8 beyond k_tc's tile)
-  if (tc2_fit(c) && c->band_kind == 3 && (!band || (paper && dog_dump == nullptr))) {
+  if (tc2_fit(c) && c->band_kind == 3 && (!band || (paper && dog_dump == nullptr && !reflect))) {
     const Tc2Plan& P = *c->tc2;
     const int nrt = tc2_nrt(c);
+    const Tc2Geom gm = tc2_geom(c);   // reflect: mirrored margins, no wrap
     // row tiles of k_tc2_rows and output row tiles of k_tc2_cols: everything, or in band
     // mode (f2) only the 256-row output tiles that cover [band_lo - 1, band_hi + 1) on the
     // whole image's grid and the NR-row tiles holding the Rx rows their windows read (at
@@ -456,8 +475,10 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       }
     }
     const size_t sm1 = tc2_rows_smem(P), sm2 = tc2_cols_smem(P);
-    auto kc = dogr ? (tc_dog ? k_tc2_cols<true> : k_tc2_cols<false>)
-                   : (tc_dog ? k_tc2_cols<true, true> : k_tc2_cols<false, true>);
+    auto kc = reflect ? (dogr ? (tc_dog ? k_tc2_cols<true, false, true> : k_tc2_cols<false, false, true>)
+                              : (tc_dog ? k_tc2_cols<true, true, true> : k_tc2_cols<false, true, true>))
+                      : (dogr ? (tc_dog ? k_tc2_cols<true> : k_tc2_cols<false>)
+                              : (tc_dog ? k_tc2_cols<true, true> : k_tc2_cols<false, true>));
     cudaError_t ea = cudaFuncSetAttribute(k_tc2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     if (ea == cudaSuccess) ea = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     if (ea != cudaSuccess) return cuda_fail(ea, "k_tc2 attributes");
@@ -468,23 +489,23 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
       const int Bc = std::min(kRxBatch, B - b0);
       const uint8_t* ic = img + (int64_t)b0 * H * pitch;
       const ImgPar* pc = par + b0;
-      const int64_t work = (int64_t)Bc * nrt * P.NR * (W / 8);
+      const int64_t work = (int64_t)Bc * nrt * P.NR * (gm.xw / 8);
       const dim3 gp((unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)c->sms * 16));
-      if (bpp == 1) k_tc2_prep<1><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
-      else if (bpp == 2) k_tc2_prep<2><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
-      else k_tc2_prep<4><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc);
+      if (bpp == 1) k_tc2_prep<1><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc, gm.pg, gm.pr);
+      else if (bpp == 2) k_tc2_prep<2><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc, gm.pg, gm.pr);
+      else k_tc2_prep<4><<<gp, 256, 0, st>>>(ic, s, pc, xt, P.NR, nrt, Bc, gm.pg, gm.pr);
       LAUNCH_CHECK("k_tc2_prep");
       for (int k = 0; k < 2; ++k) {
         if (rr[k][1] <= rr[k][0]) continue;
         const int64_t t1 = (int64_t)(W / kT2Cols) * (rr[k][1] - rr[k][0]) * Bc;
         k_tc2_rows<<<(unsigned)std::min<int64_t>(t1, c->sms), kT2Threads, sm1, st>>>(
-            xt, P, c->d_tc2tab, rx, W, H, Bc, nrt, rr[k][0], rr[k][1] - rr[k][0]);
+            xt, P, c->d_tc2tab, rx, W, gm.hx, Bc, nrt, rr[k][0], rr[k][1] - rr[k][0], gm.pg);
         LAUNCH_CHECK("k_tc2_rows");
       }
       const int64_t t2 = (int64_t)(W / kT2Cols) * nyt * Bc;
       kc<<<(unsigned)std::min<int64_t>(t2, c->sms), kT2Threads, sm2, st>>>(
           rx, pc, P, c->d_tc2tab, paper ? v + (int64_t)b0 * plane : nullptr, paper ? idx + (int64_t)b0 * plane : nullptr,
-          tc_dog ? tc_dog + (int64_t)b0 * c->n * plane : nullptr, W, H, Bc, yt0, nyt);
+          tc_dog ? tc_dog + (int64_t)b0 * c->n * plane : nullptr, W, H, Bc, yt0, nyt, gm.hx, gm.pr);
       LAUNCH_CHECK("k_tc2_cols");
     }
     MARK(2);
@@ -1343,8 +1364,8 @@ const char* mhfd_schedule_name(const mhfd_ctx* c, int32_t dtype) {
   if (c->p.response == MHFD_RESPONSE_LOG)
     return c->band_kind == 3 && tc2_fit(c) ? "k_tc2" : "k_rows_pair+k_cols_pair<log>";
   if (dtype == MHFD_U8 && c->band_enabled && c->band_kind == 3 && c->d_tctab && tc_ok(*c->tc, W, H)) return "k_tc";
-  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (c->band_kind == 3 && tc2_fit(c)) return "k_tc2";
+  if (c->p.boundary == MHFD_BOUNDARY_REFLECT) return pair_fit(c) ? "k_rows_pair+k_cols_pair" : "none";
   if (dtype == MHFD_U8 && paper && c->band_enabled && band_ok(W, H, c->tab->rmax, c->tab->ntaps_total))
     return "k_band";
   if (pair_ok(c)) return "k_rows_pair+k_cols_pair";

@@ -712,9 +712,34 @@ def test_reflect_boundary_full_parity(c1_img, nms, response, schedule):
     s = _full_parity(c1_img, C1, nms=nms, tau=tau, response=response, boundary="reflect", schedule=schedule)
     assert s["n_oracle"] > 100
     det = mhfd.Detector(256, 256, threshold=0.08, boundary="reflect", response=response, schedule=schedule, **C1)
-    want = "k_tc" if (schedule is None and response == "dog") else (
-        "k_rows_pair+k_cols_pair<log>" if response == "log" else "k_rows_pair+k_cols_pair")
+    want = ("k_tc" if response == "dog" else "k_tc2") if schedule is None else "k_rows_pair+k_cols_pair"
     assert det.schedule("u8") == want
+
+
+@pytest.mark.parametrize("kind,nms,response", [("u16", "paper", "dog"), ("u16", "26", "dog"), ("f32", "paper", "dog"),
+                                               ("u16", "paper", "log")])
+def test_reflect_k_tc2_full_parity(kind, nms, response):
+    """Reflect on k_tc2 (u16 / f32 images, the LoG response): the stretched image is staged
+    with mirrored margins (pg column groups, pr rows) so neither pass wraps; full parity on
+    a 256 x 512 tile against the oracle's reflect blur."""
+    a = synth.em_tile_np(256, 512, 1040, defocus=0.5, dose=300.0, bits=16)
+    img = a if kind == "u16" else (a.astype(np.float32) * np.float32(0.25) + np.float32(3.5))
+    tau = 0.1 if response == "log" else None
+    det = mhfd.Detector(512, 256, threshold=0.1 if response == "log" else _tau(C1), boundary="reflect",
+                        response=response, nms=nms, **C1)
+    assert det.schedule(kind) == "k_tc2"
+    s = _full_parity(img, C1, nms=nms, tau=tau, response=response, boundary="reflect")
+    assert s["n_oracle"] > 100
+
+
+def test_reflect_k_tc2_multi_tile():
+    """Reflect on k_tc2 over many row and column tiles (1024 x 768 u16, sigma 1-10): full
+    parity."""
+    a = synth.em_tile_np(768, 1024, 1041, defocus=0.5, dose=300.0, bits=16)
+    det = mhfd.Detector(1024, 768, threshold=_tau(C3), boundary="reflect", **C3)
+    assert det.schedule("u16") == "k_tc2"
+    s = _full_parity(a, C3, boundary="reflect")
+    assert s["n_oracle"] > 1000
 
 
 @pytest.mark.parametrize("w,h", [(1024, 1024), (2048, 1024)])
