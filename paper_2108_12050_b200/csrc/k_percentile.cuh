@@ -66,11 +66,12 @@ __device__ __forceinline__ int select_bin_warp(const uint32_t* h, int64_t rank, 
 
 // Pass 1: 256-bin histogram of (u8 value) or (u16 value >> 8).
 // Pass 2 (u16 only, second=true): low-byte histograms of the two selected bins.
-// SELECT (u8): the image's last CTA to flush (a ticket after hist[b]'s 256 bins, zeroed
-// with the histogram) selects the two ranks itself, so percentiles take one launch.
+// SELECT: the image's last CTA to flush (a per-image ticket after the histograms, zeroed
+// with them) selects the two ranks itself: u8 percentiles take one launch, u16 two (pass 1
+// leaves the high bytes and remaining ranks in sel, pass 2 finishes).
 template <int BPP, bool SECOND, bool SELECT = false>
 __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images, Shape s, int rows_per_cta,
-                                              uint32_t* __restrict__ hist, const SelState* __restrict__ sel,
+                                              uint32_t* __restrict__ hist, SelState* __restrict__ sel,
                                               RankPar rk = RankPar{}, ImgPar* __restrict__ par = nullptr,
                                               uint32_t* __restrict__ ticket = nullptr) {
   constexpr int NH = SECOND ? 2 : 1;
@@ -86,33 +87,46 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
   const int y1 = min(s.H, y0 + rows_per_cta);
   const int row_bytes = s.W * BPP;
   const int nvec = (row_bytes + 15) >> 4;
-  if (!SECOND && (row_bytes & 15) == 0 && nvec <= (int)blockDim.x) {
-    // whole-vector rows of at most one vector per thread (u8 up to 4096 wide, u16 up to
-    // 2048): four rows' loads in flight per thread before their atomics, so a CTA's
-    // rows_per_cta rows are not a chain of dependent load latencies (8 x 4096^2: 0.10 ms)
-    const int v = threadIdx.x;
+  if ((row_bytes & 15) == 0) {
+    // whole-vector rows (any width), both radix passes: the CTA's (row, vector) items are
+    // walked four at a time per thread, so four loads are in flight before their atomics
+    // instead of a chain of dependent load latencies (u8 8 x 4096^2: 0.10 ms; one 4096^2
+    // u16 tile's two passes 0.055 -> 0.041 ms)
     uint32_t* hw = sh[warp];
-    for (int y = y0; y < y1; y += 4) {
-      uint4 q[4];
+    auto acc = [&](const uint4& q) {
+      const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        q[r] = (v < nvec && y + r < y1) ? __ldg(reinterpret_cast<const uint4*>(img + (int64_t)(y + r) * s.pitch) + v)
-                                        : make_uint4(0, 0, 0, 0);
+      for (int k = 0; k < 4; ++k) {
+        if (BPP == 1) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (v >= nvec || y + r >= y1) continue;
-        const uint32_t wds[4] = {q[r].x, q[r].y, q[r].z, q[r].w};
+          for (int j = 0; j < 4; ++j) atomicAdd(hw + ((wds[k] >> (8 * j)) & 255u), 1u);
+        } else if (!SECOND) {
+          atomicAdd(hw + ((wds[k] >> 8) & 255u), 1u);
+          atomicAdd(hw + (wds[k] >> 24), 1u);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (BPP == 1) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) atomicAdd(hw + ((wds[k] >> (8 * j)) & 255u), 1u);
-          } else {
-            atomicAdd(hw + ((wds[k] >> 8) & 255u), 1u);
-            atomicAdd(hw + (wds[k] >> 24), 1u);
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t val = (wds[k] >> (16 * j)) & 0xffffu, top = val >> 8;
+            if ((int)top == sel_lo) atomicAdd(hw + (val & 255u), 1u);
+            if ((int)top == sel_hi) atomicAdd(hw + 256 + (val & 255u), 1u);
           }
         }
       }
+    };
+    const int nvt = (nvec + blockDim.x - 1) / blockDim.x;   // vectors per thread and row
+    const int nit = (y1 - y0) * nvt;
+    for (int it = 0; it < nit; it += 4) {
+      uint4 q[4];
+      bool ok[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = it + r, yy = y0 + i / nvt, v = threadIdx.x + (i % nvt) * blockDim.x;
+        ok[r] = i < nit && v < nvec;
+        q[r] = ok[r] ? __ldg(reinterpret_cast<const uint4*>(img + (int64_t)yy * s.pitch) + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ok[r]) acc(q[r]);
     }
   } else
   for (int y = y0; y < y1; ++y) {
@@ -175,11 +189,24 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
     __syncthreads();
     if (last && threadIdx.x < 32) {
       __threadfence();
-      const uint32_t* h = hist + (int64_t)b * 256;   // every CTA's atomics have landed (L2; not in this L1)
-      int64_t rl, rh;
-      const int bl = select_bin_warp(h, rk.rank_lo, &rl);
-      const int bh = select_bin_warp(h, rk.rank_hi, &rh);
-      if (threadIdx.x == 0) finish(&par[b], bl, bh);
+      const uint32_t* h = hist + (int64_t)b * (NH * 256);   // every CTA's atomics have landed (L2; not in this L1)
+      if (SECOND) {   // u16 pass 2: low bytes under the selected high bytes (k_select2's work)
+        int64_t dummy;
+        const int lo = (sel[b].bin_lo << 8) | select_bin_warp(h, sel[b].rem_lo, &dummy);
+        const int hi = (sel[b].bin_hi << 8) | select_bin_warp(h + 256, sel[b].rem_hi, &dummy);
+        if (threadIdx.x == 0) finish(&par[b], lo, hi);
+      } else {
+        int64_t rl, rh;
+        const int bl = select_bin_warp(h, rk.rank_lo, &rl);
+        const int bh = select_bin_warp(h, rk.rank_hi, &rh);
+        if (threadIdx.x == 0) {
+          if (BPP == 1) {
+            finish(&par[b], bl, bh);
+          } else {   // u16 pass 1: the high bytes and the ranks left inside them (k_select1's work)
+            sel[b].bin_lo = bl; sel[b].bin_hi = bh; sel[b].rem_lo = rl; sel[b].rem_hi = rh;
+          }
+        }
+      }
     }
   }
 }

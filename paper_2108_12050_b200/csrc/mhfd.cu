@@ -181,7 +181,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.par = take(sizeof(ImgPar) * B);
   L.sel = take(sizeof(SelState) * B);
   L.hist1 = take(sizeof(uint32_t) * 257 * B);   // 256 bins per image, then per-image tickets (u8 select)
-  L.hist2 = take(sizeof(uint32_t) * 512 * B);
+  L.hist2 = take(sizeof(uint32_t) * 513 * B);   // 2 x 256 bins per image, then per-image tickets (u16 pass 2)
   L.fimg = take(sizeof(float) * plane * B);
   const bool paper = c->p.nms == MHFD_NMS_PAPER;
   L.v = take(paper ? sizeof(float) * plane * B : 0);
@@ -369,7 +369,7 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
   rp.rank_lo = std::min<int64_t>((int64_t)std::floor((double)c->p.sat_low * (double)N), N - 1);
   rp.rank_hi = N - 1 - std::min<int64_t>((int64_t)std::floor((double)c->p.sat_high * (double)N), N - 1);
   cudaError_t e = bpp == 4 ? cudaSuccess : cudaMemsetAsync(ws + L.hist1, 0, sizeof(uint32_t) * 257 * B, st);
-  if (e == cudaSuccess && bpp >= 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 512 * B, st);
+  if (e == cudaSuccess && bpp >= 2) e = cudaMemsetAsync(ws + L.hist2, 0, sizeof(uint32_t) * 513 * B, st);
   if (e != cudaSuccess) return cuda_fail(e, "memset hist");
   // ~2 CTAs per SM of rows (fewer, fuller CTAs: each flushes 256 global atomics)
   int rows_per_cta = std::max(1, (int)(((int64_t)H * B + 2 * c->sms - 1) / (2 * c->sms)));
@@ -390,14 +390,11 @@ mhfd_status run_front(mhfd_ctx* c, const void* d_images, int32_t dtype, int32_t 
     k_hist<1, false, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel, rp, par, h1 + 256 * B);
     LAUNCH_CHECK("k_hist");
   } else {
-    k_hist<2, false><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel);
+    // two radix passes, each selecting in its last CTA per image (no k_select1 / k_select2)
+    k_hist<2, false, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h1, sel, rp, par, h1 + 256 * B);
     LAUNCH_CHECK("k_hist");
-    k_select1<2><<<(B + 3) / 4, 128, 0, st>>>(h1, rp, sel, par, B);
-    LAUNCH_CHECK("k_select1");
-    k_hist<2, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel);
+    k_hist<2, true, true><<<hg, 256, 0, st>>>(img, s, rows_per_cta, h2, sel, rp, par, h2 + 512 * B);
     LAUNCH_CHECK("k_hist2");
-    k_select2<<<(B + 3) / 4, 128, 0, st>>>(h2, sel, par, B);
-    LAUNCH_CHECK("k_select2");
   }
 
   MARK(1);
