@@ -70,6 +70,8 @@ struct PruneArgs {
   int nseg, spr;            // segments per image, per row
   int cs_shift;             // cell edge cs = 1 << cs_shift (>= every dmax)
   int ncx, nbands;          // ceil(W / cs) cells per band, ceil(H / cs) bands
+  int nsk;                  // scale keys per cell: n (records of a cell sorted by scale, descending,
+                            // which enables scan_cells' reach test) or 1 (unsorted; too many keys)
   int32_t* cellstart;       // B x nbands x (ncx + 1): first crec index of cell (band, cx)
   int4* crec;               // B x cap: {x, y, scale, k} per candidate, band-major, cell-sorted
   int64_t* img_off;         // B + 1: prefix of effective candidate counts
@@ -112,7 +114,8 @@ __device__ __forceinline__ int image_of(const int64_t* off, int B, int64_t g) {
 
 constexpr int kNbMax = 6;   // neighbour indices kept per worklist record
 
-constexpr int kMaxCells = 2048;   // ncx + 1 per band (shared-memory counting sort)
+constexpr int kMaxCells = 2048;   // ncx + 1 per band
+constexpr int kMaxKeys = 6144;    // (cell, scale) keys of the shared-memory counting sort per band
 
 // Scan the candidates around blob k for higher-priority blobs that overlap it by more
 // than `overlap`: the records of cells cx-1..cx+1 in bands yb-1..yb+1 (three contiguous
@@ -121,7 +124,7 @@ constexpr int kMaxCells = 2048;   // ncx + 1 per band (shared-memory counting so
 // overlapping one to rec(q).
 // R: the image's cell-ordered records, or a shared-memory copy of a band window offset so
 // that R[i] is record i (k_prune round 0)
-template <class Rec>
+template <bool SORTED, class Rec>
 __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4 me4, const int4* R0p, const int4* R1p,
                                            const int4* R2p, int i0, int istep, bool* blocked, Rec rec, int round) {
   const uint8_t* st = a.st + (int64_t)b * a.cap;
@@ -134,66 +137,103 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
   const int b0 = max(0, yb - 1), b1 = min(a.nbands - 1, yb + 1);
   const int c0 = max(0, cx - 1), c1 = min(a.ncx, cx + 2);
   const int32_t* cst = a.cellstart + (int64_t)b * a.nbands * (a.ncx + 1);
-  int lo[3], hi[3];
+  // the test of one record o: true = k is REMOVED (o is a kept, higher-priority blob
+  // overlapping it by more than `overlap`)
+  auto test = [&](const int4& o, const float2 t2) -> bool {
+    const int dx = o.x - me.x, dy = o.y - me.y;
+    if (dx > Dm || dx < -Dm || dy > Dm || dy < -Dm) return false;
+    if (o.w == k) return false;
+    const bool higher = o.z > me.scale || (o.z == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
+    if (!higher) return false;
+    // frac(d) > overlap, frac decreasing in d: d^2 < lo -> yes, d^2 >= hi -> no, else
+    // evaluate the lens formula (the band is 1e-6 relative around the bisected root)
+    const float d2 = (float)(dx * dx + dy * dy);
+    const bool over = d2 < t2.x ? true
+                      : d2 >= t2.y ? false
+                                   : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.z]) > a.overlap;
+    if (over) {
+      const uint8_t s = st_vis(__ldcg(st + o.w), round, a.sync);
+      if (s == kKept) return true;
+      if (s == kUndecided) *blocked = true;
+      rec(o.w);
+    }
+    return false;
+  };
   // cst and R were written in phase 1b of this launch and are read-only since: plain
   // (L1-cached) loads are coherent here (no SM cached these lines before the barrier,
   // and L1 starts empty at launch), and neighbouring blobs share most of their windows
+  if (!SORTED) {   // cells c0 .. c1-1 of a band are one contiguous record range
+    int lo[3], hi[3];
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {   // six independent loads
-    const int bb = min(b0 + j, b1);
-    lo[j] = cst[(int64_t)bb * (a.ncx + 1) + c0];
-    hi[j] = b0 + j <= b1 ? cst[(int64_t)bb * (a.ncx + 1) + c1] : lo[j];
+    for (int j = 0; j < 3; ++j) {   // six independent loads
+      const int bb = min(b0 + j, b1);
+      lo[j] = cst[(int64_t)bb * (a.ncx + 1) + c0];
+      hi[j] = b0 + j <= b1 ? cst[(int64_t)bb * (a.ncx + 1) + c1] : lo[j];
+    }
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j) {
+      const int4* R = j == 0 ? R0p : j == 1 ? R1p : R2p;   // records of band b0 + j
+      if (PRUNE_STAMPS && hi[j] > lo[j] + i0) atomicAdd(&a.counters[8], (hi[j] - lo[j] - i0 + istep - 1) / istep);
+#pragma unroll 4
+      for (int i = lo[j] + i0; i < hi[j]; i += istep) {
+        const int4 o = R[i];   // {x, y, scale, k}
+        if (test(o, __ldg(th + o.z))) return true;
+      }
+    }
+    return false;
   }
+  // Scale-sorted cells (descending; large radii, where a cell is much larger than most
+  // blobs' reach): every later record of a cell has a scale <= o.z, so a lower-priority
+  // scale, or an overlap distance band thr_hi(s, s') (non-decreasing in s' >= s: the lens
+  // grows with the larger disk) that cannot reach the cell's nearest pixel, ends the cell
+  const int cs = 1 << a.cs_shift;
 #pragma unroll 1
   for (int j = 0; j < 3; ++j) {
+    if (b0 + j > b1) break;
     const int4* R = j == 0 ? R0p : j == 1 ? R1p : R2p;   // records of band b0 + j
-    if (PRUNE_STAMPS && hi[j] > lo[j] + i0) atomicAdd(&a.counters[8], (hi[j] - lo[j] - i0 + istep - 1) / istep);
-#pragma unroll 4
-    for (int i = lo[j] + i0; i < hi[j]; i += istep) {
-      const int4 o = R[i];   // {x, y, scale, k}
-      const int dx = o.x - me.x, dy = o.y - me.y;
-      if (dx > Dm || dx < -Dm || dy > Dm || dy < -Dm) continue;
-      if (o.w == k) continue;
-      const bool higher = o.z > me.scale || (o.z == me.scale && (o.y < me.y || (o.y == me.y && o.x < me.x)));
-      if (!higher) continue;
-      // frac(d) > overlap, frac decreasing in d: d^2 < lo -> yes, d^2 >= hi -> no, else
-      // evaluate the lens formula (the band is 1e-6 relative around the bisected root)
-      const float d2 = (float)(dx * dx + dy * dy);
-      const float2 t2 = __ldg(th + o.z);
-      const bool over = d2 < t2.x ? true
-                        : d2 >= t2.y ? false
-                                     : lens_fraction(sqrt((double)(dx * dx + dy * dy)), r, a.rad[o.z]) > a.overlap;
-      if (over) {
-        const uint8_t s = st_vis(__ldcg(st + o.w), round, a.sync);
-        if (s == kKept) return true;
-        if (s == kUndecided) *blocked = true;
-        rec(o.w);
+    const int32_t* cb = cst + (int64_t)(b0 + j) * (a.ncx + 1);
+    const int by0 = (b0 + j) * cs, ddy = me.y < by0 ? by0 - me.y : (me.y >= by0 + cs ? me.y - (by0 + cs - 1) : 0);
+#pragma unroll 1
+    for (int q = 0; q < c1 - c0; ++q) {
+      const int i_lo = cb[c0 + q], i_hi = cb[c0 + q + 1];   // the cell's records
+      const int cx0 = (c0 + q) * cs;
+      const int ddx = me.x < cx0 ? cx0 - me.x : (me.x >= cx0 + cs ? me.x - (cx0 + cs - 1) : 0);
+      const float dc2 = (float)(ddx * ddx + ddy * ddy);   // to the cell's nearest pixel
+      if (PRUNE_STAMPS && i_hi > i_lo + i0) atomicAdd(&a.counters[8], (i_hi - i_lo - i0 + istep - 1) / istep);
+#pragma unroll 1
+      for (int i = i_lo + i0; i < i_hi; i += istep) {
+        const int4 o = R[i];
+        const float2 t2 = __ldg(th + o.z);
+        if (o.z < me.scale || dc2 >= t2.y) break;
+        if (test(o, t2)) return true;
       }
     }
   }
   return false;
 }
 
-template <class Rec>
+template <bool SORTED, class Rec>
 __device__ __forceinline__ bool scan_rows(const PruneArgs& a, int b, int64_t k, int i0, int istep, bool* blocked,
                                           Rec rec, int round) {
   const mhfd_blob m = a.cand[(int64_t)b * a.cap + k];
   const int4* R = a.crec + (int64_t)b * a.cap;
-  return scan_cells(a, b, make_int4(m.x, m.y, m.scale, (int)k), R, R, R, i0, istep, blocked, rec, round);
+  return scan_cells<SORTED>(a, b, make_int4(m.x, m.y, m.scale, (int)k), R, R, R, i0, istep, blocked, rec, round);
 }
 
+template <bool SORTED>
 __device__ uint8_t decide(const PruneArgs& a, int b, int64_t k, int round) {
   bool blocked = false;
-  if (scan_rows(a, b, k, 0, 1, &blocked, [](int) {}, round)) return kRemoved;
+  if (scan_rows<SORTED>(a, b, k, 0, 1, &blocked, [](int) {}, round)) return kRemoved;
   return blocked ? kUndecided : kKept;
 }
 
 // round-0 decision of blob k that also records its overlapping higher-priority
 // neighbours (all of them: a blob that stays UNDECIDED scanned every row)
+template <bool SORTED>
 __device__ uint8_t decide_collect(const PruneArgs& a, int b, int64_t k, int* nq, int (&qs)[kNbMax]) {
   bool blocked = false;
   int n = 0;
-  if (scan_rows(
+  if (scan_rows<SORTED>(
           a, b, k, 0, 1, &blocked,
           [&](int q) {
             if (n < kNbMax) qs[n] = q;
@@ -221,6 +261,7 @@ __device__ uint8_t decide_list(const PruneArgs& a, int b, const int4& r0, const 
   return blocked ? kUndecided : kKept;
 }
 
+template <bool SORTED>
 __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   cg::grid_group grid = cg::this_grid();
   int pst_ = 0;
@@ -313,8 +354,10 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   // column cell in shared memory (order inside a cell is irrelevant: decisions do not
   // depend on it) and writes the cell starts and the cell-ordered records.
   if (a.prune) {
-    __shared__ int32_t cell[kMaxCells];
+    __shared__ int32_t cell[kMaxKeys];
     const int cs = 1 << a.cs_shift;
+    const int nk = a.ncx * a.nsk + 1;   // keys (cell cx, scale s) -> cx nsk + (nsk - 1 - s), + the end
+    auto key_of = [&](int x, int sc) { return (x >> a.cs_shift) * a.nsk + (a.nsk > 1 ? a.nsk - 1 - sc : 0); };
     for (int64_t item = blockIdx.x; item < (int64_t)a.B * a.nbands; item += gridDim.x) {
       const int b = (int)(item / a.nbands), j = (int)(item % a.nbands);
       const int64_t nb_ = img_off[b + 1] - img_off[b];
@@ -326,33 +369,33 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
       const mhfd_blob* C = a.cand + (int64_t)b * a.cap;
       if (seg_rows)
         for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) a.st[(int64_t)b * a.cap + k] = kUndecided;
-      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cell[c] = 0;
+      for (int c = threadIdx.x; c < nk; c += blockDim.x) cell[c] = 0;
       __syncthreads();
-      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&cell[C[k].x >> a.cs_shift], 1);
+      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) atomicAdd(&cell[key_of(C[k].x, C[k].scale)], 1);
       __syncthreads();
-      if (threadIdx.x < 32) {   // exclusive scan of ncx + 1 counts by one warp
+      if (threadIdx.x < 32) {   // exclusive scan of the key counts by one warp
         int carry = 0;
-        for (int c0 = 0; c0 <= a.ncx; c0 += 32) {
+        for (int c0 = 0; c0 < nk; c0 += 32) {
           const int c = c0 + threadIdx.x;
-          const int v = c <= a.ncx ? cell[c] : 0;
+          const int v = c < nk ? cell[c] : 0;
           int x = v;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, x, o);
             if ((int)threadIdx.x >= o) x += t;
           }
-          if (c <= a.ncx) cell[c] = k0 + carry + x - v;
+          if (c < nk) cell[c] = k0 + carry + x - v;
           carry += __shfl_sync(0xffffffffu, x, 31);
         }
       }
       __syncthreads();
       int32_t* cst = a.cellstart + ((int64_t)b * a.nbands + j) * (a.ncx + 1);
-      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cst[c] = cell[c];
+      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cst[c] = cell[c * a.nsk];   // first key of each cell
       __syncthreads();
       int4* R = a.crec + (int64_t)b * a.cap;
       for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         const mhfd_blob m = C[k];
-        const int pos = atomicAdd(&cell[m.x >> a.cs_shift], 1);
+        const int pos = atomicAdd(&cell[key_of(m.x, m.scale)], 1);
         R[pos] = make_int4(m.x, m.y, m.scale, k);
       }
       __syncthreads();
@@ -393,7 +436,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         if (in) {
           b = image_of(img_off, a.B, g);
           k = g - img_off[b];
-          rem = scan_rows(
+          rem = scan_rows<SORTED>(
               a, b, k, gl, G, &blocked,
               [&](int q) {
                 const int pos = atomicAdd(&wq[wib][grp][kNbMax], 1);
@@ -438,7 +481,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         if (in) {
           b = image_of(img_off, a.B, g);
           k = g - img_off[b];
-          d = decide_collect(a, b, k, &nq, qs);
+          d = decide_collect<SORTED>(a, b, k, &nq, qs);
           if (d != kUndecided) __stcg(a.st + (int64_t)b * a.cap + k, st_enc(d, 0, a.sync));
         }
         const bool und = in && d == kUndecided;
@@ -489,7 +532,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
           const int64_t k = g - img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
           if ((__ldcg(sp) & 3u) != kUndecided) continue;
-          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], 1) : decide(a, b, k, 1);
+          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], 1) : decide<SORTED>(a, b, k, 1);
           if (d != kUndecided) __stcg(sp, d); else more = true;
         }
         if (more) {
@@ -510,7 +553,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
           const int64_t k = g - img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
           if ((__ldcg(sp) & 3u) != kUndecided) continue;
-          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], round) : decide(a, b, k, round);
+          const uint8_t d = r0.y <= kNbMax ? decide_list(a, b, r0, a.wl[2 * i + 1], round) : decide<SORTED>(a, b, k, round);
           if (d != kUndecided) __stcg(sp, st_enc(d, round, a.sync)); else ++undecided;
         }
       } else {
@@ -519,7 +562,7 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
           const int64_t k = g - img_off[b];
           uint8_t* sp = a.st + (int64_t)b * a.cap + k;
           if ((__ldcg(sp) & 3u) != kUndecided) continue;
-          const uint8_t d = decide(a, b, k, round);
+          const uint8_t d = decide<SORTED>(a, b, k, round);
           if (d != kUndecided) __stcg(sp, st_enc(d, round, a.sync)); else ++undecided;
         }
       }
