@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
   for (int i = threadIdx.x; i < 8 * NH * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
   int sel_lo = -1, sel_hi = -1;
   if (SECOND) { sel_lo = sel[b].bin_lo; sel_hi = sel[b].bin_hi; }
+  const uint32_t sel_lo2 = (uint32_t)(sel_lo & 0xff) * 0x10001u, sel_hi2 = (uint32_t)(sel_hi & 0xff) * 0x10001u;
   __syncthreads();
   const uint8_t* img = images + (int64_t)b * s.H * s.pitch;
   const int y0 = blockIdx.x * rows_per_cta;
@@ -104,11 +105,16 @@ __global__ void __launch_bounds__(256) k_hist(const uint8_t* __restrict__ images
           atomicAdd(hw + ((wds[k] >> 8) & 255u), 1u);
           atomicAdd(hw + (wds[k] >> 24), 1u);
         } else {
+          // both 16-bit values' high bytes against the two selected bins at once (SIMD
+          // compare): almost every word matches neither and costs four instructions
+          const uint32_t hb = (wds[k] >> 8) & 0x00ff00ffu;
+          if (__vcmpeq2(hb, sel_lo2) | __vcmpeq2(hb, sel_hi2)) {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint32_t val = (wds[k] >> (16 * j)) & 0xffffu, top = val >> 8;
-            if ((int)top == sel_lo) atomicAdd(hw + (val & 255u), 1u);
-            if ((int)top == sel_hi) atomicAdd(hw + 256 + (val & 255u), 1u);
+            for (int j = 0; j < 2; ++j) {
+              const uint32_t val = (wds[k] >> (16 * j)) & 0xffffu, top = val >> 8;
+              if ((int)top == sel_lo) atomicAdd(hw + (val & 255u), 1u);
+              if ((int)top == sel_hi) atomicAdd(hw + 256 + (val & 255u), 1u);
+            }
           }
         }
       }
