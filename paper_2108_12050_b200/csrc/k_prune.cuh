@@ -72,7 +72,9 @@ struct PruneArgs {
   int ncx, nbands;          // ceil(W / cs) cells per band, ceil(H / cs) bands
   int nsk;                  // scale keys per cell: n (records of a cell sorted by scale, descending,
                             // which enables scan_cells' reach test) or 1 (unsorted; too many keys)
-  int32_t* cellstart;       // B x nbands x (ncx + 1): first crec index of cell (band, cx)
+  int32_t* cellstart;       // B x nbands x cst_stride: first crec index of cell (band, cx); k_prune<false>:
+                            // two classes per band, scale >= 1 (cells 0..ncx) then scale 0 (ncx+1 ..)
+  int cst_stride;           // ncx + 1 (k_prune<true>) or 2 (ncx + 1) (k_prune<false>)
   int4* crec;               // B x cap: {x, y, scale, k} per candidate, band-major, cell-sorted
   int64_t* img_off;         // B + 1: prefix of effective candidate counts
   int64_t* chunk_off;       // B + 1: prefix of chunk counts
@@ -136,7 +138,7 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
   const int yb = me.y >> a.cs_shift, cx = me.x >> a.cs_shift;
   const int b0 = max(0, yb - 1), b1 = min(a.nbands - 1, yb + 1);
   const int c0 = max(0, cx - 1), c1 = min(a.ncx, cx + 2);
-  const int32_t* cst = a.cellstart + (int64_t)b * a.nbands * (a.ncx + 1);
+  const int32_t* cst = a.cellstart + (int64_t)b * a.nbands * a.cst_stride;
   // the test of one record o: true = k is REMOVED (o is a kept, higher-priority blob
   // overlapping it by more than `overlap`)
   auto test = [&](const int4& o, const float2 t2) -> bool {
@@ -162,13 +164,18 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
   // cst and R were written in phase 1b of this launch and are read-only since: plain
   // (L1-cached) loads are coherent here (no SM cached these lines before the barrier,
   // and L1 starts empty at launch), and neighbouring blobs share most of their windows
-  if (!SORTED) {   // cells c0 .. c1-1 of a band are one contiguous record range
+  if (!SORTED) {
+    // Two classes per band.  Records of scales >= 1: cells c0 .. c1-1 of a band are one
+    // contiguous range, scanned over the 3 x 3 cell window (the largest reach).  Records
+    // of scale 0 (most blobs at small scales, e.g. 87 % on the C3 tiles): lower priority
+    // than any blob of scale >= 1, so only a scale-0 blob scans them, and only the cells
+    // within its reach of a scale-0 neighbour (sqrt thr_hi(0, 0), about a pixel).
     int lo[3], hi[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {   // six independent loads
       const int bb = min(b0 + j, b1);
-      lo[j] = cst[(int64_t)bb * (a.ncx + 1) + c0];
-      hi[j] = b0 + j <= b1 ? cst[(int64_t)bb * (a.ncx + 1) + c1] : lo[j];
+      lo[j] = cst[(int64_t)bb * a.cst_stride + c0];
+      hi[j] = b0 + j <= b1 ? cst[(int64_t)bb * a.cst_stride + c1] : lo[j];
     }
 #pragma unroll 1
     for (int j = 0; j < 3; ++j) {
@@ -178,6 +185,23 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
       for (int i = lo[j] + i0; i < hi[j]; i += istep) {
         const int4 o = R[i];   // {x, y, scale, k}
         if (test(o, __ldg(th + o.z))) return true;
+      }
+    }
+    if (me.scale == 0) {
+      const int rr = (int)ceilf(sqrtf(__ldg(th).y));   // reach to a scale-0 neighbour (>= 0)
+      const int ya = max(0, (me.y - rr) >> a.cs_shift), yz = min(a.nbands - 1, (me.y + rr) >> a.cs_shift);
+      const int xa = max(0, (me.x - rr) >> a.cs_shift), xz = min(a.ncx - 1, (me.x + rr) >> a.cs_shift);
+#pragma unroll 1
+      for (int bb = ya; bb <= yz; ++bb) {
+        const int j = bb - b0;   // within the 3 x 3 window: rr <= dmax <= cs
+        const int4* R = j == 0 ? R0p : j == 1 ? R1p : R2p;
+        const int32_t* cs0 = cst + (int64_t)bb * a.cst_stride + (a.ncx + 1);
+        const int s_lo = cs0[xa], s_hi = cs0[xz + 1];
+#pragma unroll 2
+        for (int i = s_lo + i0; i < s_hi; i += istep) {
+          const int4 o = R[i];
+          if (test(o, __ldg(th))) return true;
+        }
       }
     }
     return false;
@@ -191,7 +215,7 @@ __device__ __forceinline__ bool scan_cells(const PruneArgs& a, int b, const int4
   for (int j = 0; j < 3; ++j) {
     if (b0 + j > b1) break;
     const int4* R = j == 0 ? R0p : j == 1 ? R1p : R2p;   // records of band b0 + j
-    const int32_t* cb = cst + (int64_t)(b0 + j) * (a.ncx + 1);
+    const int32_t* cb = cst + (int64_t)(b0 + j) * a.cst_stride;
     const int by0 = (b0 + j) * cs, ddy = me.y < by0 ? by0 - me.y : (me.y >= by0 + cs ? me.y - (by0 + cs - 1) : 0);
 #pragma unroll 1
     for (int q = 0; q < c1 - c0; ++q) {
@@ -356,8 +380,13 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
   if (a.prune) {
     __shared__ int32_t cell[kMaxKeys];
     const int cs = 1 << a.cs_shift;
-    const int nk = a.ncx * a.nsk + 1;   // keys (cell cx, scale s) -> cx nsk + (nsk - 1 - s), + the end
-    auto key_of = [&](int x, int sc) { return (x >> a.cs_shift) * a.nsk + (a.nsk > 1 ? a.nsk - 1 - sc : 0); };
+    // keys: k_prune<true> (cell cx, scale s) -> cx nsk + (nsk - 1 - s), + the end;
+    // k_prune<false> two classes: scale >= 1 -> cx, scale 0 -> ncx + 1 + cx (each with an end key)
+    const int nk = SORTED ? a.ncx * a.nsk + 1 : 2 * (a.ncx + 1);
+    auto key_of = [&](int x, int sc) {
+      return SORTED ? (x >> a.cs_shift) * a.nsk + (a.nsk > 1 ? a.nsk - 1 - sc : 0)
+                    : (sc == 0 ? a.ncx + 1 : 0) + (x >> a.cs_shift);
+    };
     for (int64_t item = blockIdx.x; item < (int64_t)a.B * a.nbands; item += gridDim.x) {
       const int b = (int)(item / a.nbands), j = (int)(item % a.nbands);
       const int64_t nb_ = img_off[b + 1] - img_off[b];
@@ -389,8 +418,11 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
         }
       }
       __syncthreads();
-      int32_t* cst = a.cellstart + ((int64_t)b * a.nbands + j) * (a.ncx + 1);
-      for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cst[c] = cell[c * a.nsk];   // first key of each cell
+      int32_t* cst = a.cellstart + ((int64_t)b * a.nbands + j) * a.cst_stride;
+      if (SORTED)
+        for (int c = threadIdx.x; c <= a.ncx; c += blockDim.x) cst[c] = cell[c * a.nsk];   // first key of each cell
+      else
+        for (int c = threadIdx.x; c < nk; c += blockDim.x) cst[c] = cell[c];
       __syncthreads();
       int4* R = a.crec + (int64_t)b * a.cap;
       for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {

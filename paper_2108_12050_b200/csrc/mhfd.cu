@@ -197,7 +197,7 @@ Layout layout(const mhfd_ctx* c, int B) {
   L.cand = take(sizeof(mhfd_blob) * c->cap * B);
   L.st = take(c->cap * B);
   L.rowstart = take(sizeof(int32_t) * (c->p.height + 1) * (size_t)B);
-  L.cellstart = take(sizeof(int32_t) * (size_t)c->nbands * (c->ncx + 1) * (size_t)B);   // pruning cell index
+  L.cellstart = take(sizeof(int32_t) * (size_t)c->nbands * 2 * (c->ncx + 1) * (size_t)B);   // pruning cell index
   L.crec = take(sizeof(int4) * c->cap * (size_t)B);
   L.imgoff = take(sizeof(int64_t) * (B + 1));
   L.chunkoff = take(sizeof(int64_t) * (B + 1));
@@ -738,6 +738,7 @@ mhfd_status run_prune(mhfd_ctx* c, int32_t B, char* ws, const Layout& L, mhfd_bl
   // cell ranges for small ones (the per-cell loop cost more than it skipped at sigma 1-10)
   const bool sorted = c->cs_shift >= 6 && (int64_t)c->ncx * c->n + 1 <= kMaxKeys;
   pa.nsk = sorted ? c->n : 1;
+  pa.cst_stride = sorted ? c->ncx + 1 : 2 * (c->ncx + 1);
   pa.cellstart = reinterpret_cast<int32_t*>(ws + L.cellstart);
   pa.crec = reinterpret_cast<int4*>(ws + L.crec);
   pa.img_off = reinterpret_cast<int64_t*>(ws + L.imgoff);
