@@ -452,7 +452,10 @@ __global__ void __launch_bounds__(256, 4) k_prune(PruneArgs a) {
     // thread's window scan).  Measured alternative that lost: each CTA copying a band
     // piece's window into shared memory and scanning it there.
     int G = 1;
-    while (G < 32 && total * G < gsize * 4) G <<= 1;
+    // G doubles while total * G < 2 x threads, up to 16 (measured after the two-class cell
+    // index: one 4096^2 tile takes G = 2, 0.066 -> 0.064 ms; one 1024^2 tile G = 16, 0.032
+    // -> 0.030 ms; batches G = 1)
+    while (G < 16 && total * G < gsize * 2) G <<= 1;
     if (G > 1) {   // a group of G lanes per blob, striding over its window's records
       __shared__ int wq[8][32][kNbMax + 1];
       const int wib = threadIdx.x >> 5, grp = lane0 / G, gl = lane0 & (G - 1);
