@@ -512,7 +512,7 @@ __device__ __forceinline__ void nms_roll_fast(const NmsArgs& a, const float* __r
 }
 
 template <int NR>
-__global__ void __launch_bounds__(256, 3) k_nms_roll(NmsArgs a, int nseg, int32_t* __restrict__ segcnt, int row0,
+__global__ void __launch_bounds__(256, NR <= 2 ? 4 : 3) k_nms_roll(NmsArgs a, int nseg, int32_t* __restrict__ segcnt, int row0,
                                                     int row1, mhfd_blob* __restrict__ slab) {
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31;
